@@ -1,0 +1,138 @@
+/*
+ * mapfuse_b200.h -- the C-ABI boundary of the B200 fused-sequence engine.
+ *
+ * This is the drop-in replacement for the reference's execution boundary
+ *
+ *     LaunchResult vm::launch(const kernel::KernelIR&, const DeviceConfig&,
+ *                             const LaunchArgs&)
+ *         /root/reference/proj/include/mapfuse/vm.hpp:94  (interpreter:
+ *         proj/src/vm.cpp:450-479)
+ *
+ * and of the compile pipeline that feeds it (the
+ * reference's pipeline.cpp is listed in proj/CMakeLists.txt:48 but absent).
+ * Plain C: opaque handles, plain pointers and sizes, no C++ or torch types.
+ *
+ * Error model (mirrors the reference's exceptions):
+ *   MF_OK            0
+ *   MF_ERR_FAULT     1  vm::VmFault (proj/include/mapfuse/vm.hpp:21): bad or
+ *                       missing binding, shape mismatch, CUDA failure
+ *   MF_ERR_INVALID   2  ir::ParseError / invalid argument
+ *                       (proj/include/mapfuse/ir.hpp:35-43) and library /
+ *                       script validation diagnostics
+ * The message of the last failure on the calling thread: mf_last_error().
+ *
+ * Buffers are row-major fp32, padded so both dimensions are multiples of 32
+ * (proj/include/mapfuse/blas.hpp:29-30).  Unlike vm::launch, reduction
+ * outputs need NOT be pre-zeroed (vm.hpp:91-93): every output is fully
+ * overwritten, deterministically.  Intermediates of a multi-kernel plan that
+ * the caller does not bind are allocated in the plan's device workspace.
+ */
+#ifndef MAPFUSE_B200_H
+#define MAPFUSE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MF_OK 0
+#define MF_ERR_FAULT 1
+#define MF_ERR_INVALID 2
+
+/* Planner modes for mf_compile. */
+#define MF_MODE_FUSED 0   /* planner-selected fusion partition (reference mode) */
+#define MF_MODE_UNFUSED 1 /* one kernel per elementary call (the baseline chain) */
+
+typedef struct mf_plan mf_plan;
+
+/* Replaces vm::GlobalBuffer{rows, cols, std::vector<float>*}
+ * (proj/include/mapfuse/vm.hpp:25-28).  `data` is a DEVICE pointer for
+ * mf_launch / mf_launch_kernel and a HOST pointer for mf_launch_host. */
+typedef struct {
+  const char* name;
+  int rows;
+  int cols;
+  float* data;
+} mf_buffer;
+
+/* Replaces LaunchArgs::scalars (vm.hpp:32). */
+typedef struct {
+  const char* name;
+  float value;
+} mf_scalar;
+
+/* Replaces ExecutionStats' traffic counters (vm.hpp:41-56): algorithmic bytes
+ * of the launched kernels (each distinct input read once, each output written
+ * once -- SURVEY.md 8d), kernel count, and device time when measured. */
+typedef struct {
+  uint64_t bytes_loaded;
+  uint64_t bytes_stored;
+  double ms; /* filled by mf_launch_host (synchronous); 0 for async launches */
+  int kernels;
+} mf_stats;
+
+/* Script text -> parse, dependency graph, fusion planning, combination
+ * selection, code generation (KernelIR per kernel) and lowering onto the
+ * sm_100a kernel families.  rows/cols are the logical problem size (padded
+ * to 32 internally, as blas::make_problem does, proj/src/blas.cpp:109-110).
+ * manifest == NULL uses the built-in elementary-function library. */
+int mf_compile(const char* script_text, const char* manifest, int rows, int cols, int mode,
+               mf_plan** out);
+
+/* Convenience: compile one of the shipped Table-1 sequences by name
+ * (blas::build_sequence, proj/include/mapfuse/blas.hpp:27). */
+int mf_compile_sequence(const char* sequence, int rows, int cols, int mode, mf_plan** out);
+
+/* One kernel given as KernelIR text (kernel::emit_pseudo_source format,
+ * proj/src/kernel.cpp:33-65) -> single-kernel plan.  This is the exact
+ * vm::launch(KernelIR, ...) boundary.  rows/cols: the padded domain. */
+int mf_plan_create(const char* kernel_ir_text, int rows, int cols, mf_plan** out);
+
+void mf_plan_destroy(mf_plan* plan);
+
+int mf_plan_num_kernels(const mf_plan* plan);
+/* JSON description of the plan (kernels, fused calls, buffers, roles,
+ * algorithmic bytes).  Returns the needed size (including NUL); copies if
+ * cap is large enough. */
+int mf_plan_describe(const mf_plan* plan, char* buf, int cap);
+/* Emitted KernelIR text of kernel k (same size convention). */
+int mf_plan_kernel_text(const mf_plan* plan, int k, char* buf, int cap);
+/* Comma-separated names kernel k produces by a column (cross-row) reduction;
+ * under row sharding these are all-reduced before use. */
+int mf_plan_kernel_column_outputs(const mf_plan* plan, int k, char* buf, int cap);
+
+/* Launches every kernel of the plan on `stream` (a cudaStream_t; NULL = the
+ * legacy default stream).  Asynchronous.  Buffers: device pointers. */
+int mf_launch(const mf_plan* plan, const mf_buffer* buffers, int nbuf, const mf_scalar* scalars,
+              int nscalars, void* stream, mf_stats* stats);
+
+/* Launches kernel k only (sharded execution interleaves collectives). */
+int mf_launch_kernel(const mf_plan* plan, int k, const mf_buffer* buffers, int nbuf,
+                     const mf_scalar* scalars, int nscalars, void* stream, mf_stats* stats);
+
+/* vm::launch's exact contract with host memory: copies inputs host->device,
+ * runs the plan, copies every bound output back, synchronizes.  stats->ms is
+ * the device time of the kernels alone. */
+int mf_launch_host(const mf_plan* plan, const mf_buffer* host_buffers, int nbuf,
+                   const mf_scalar* scalars, int nscalars, mf_stats* stats);
+
+/* Counter-based synthetic data on the device, identical to the CPU checker's
+ * generator: out[r*ld + c] = U(seed, (row0 + r) * ncols_global + c). */
+int mf_generate(float* dev, int64_t rows, int64_t cols, int64_t ld, uint64_t seed, int64_t row0,
+                int64_t ncols_global, void* stream);
+
+/* Engine options: "matrix_k" (2|4 float4 slots per thread), "f64acc" (0|1:
+ * accumulate matrix reductions in fp64), "occupancy" (CTAs per SM). */
+int mf_set_option(const char* key, int value);
+int mf_get_option(const char* key);
+
+const char* mf_last_error(void);
+const char* mf_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MAPFUSE_B200_H */

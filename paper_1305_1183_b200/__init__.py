@@ -1,0 +1,13 @@
+"""mapfuse-b200: B200-native fused map/reduce BLAS-1/BLAS-2 sequences.
+
+The hot path of arxiv 1305.1183 ("mapfuse"): elementary-function library ->
+call-sequence script -> fusion planner -> generated kernels, with every
+planner-selected fusion executed by a hand-written sm_100a kernel.  The
+native engine (libmapfuse_b200.so: reference-compatible C++ host API +
+CUDA kernels + C-ABI) is required; there is no CPU fallback.
+"""
+from .runtime import (MapfuseError, ParseError, Plan, VmFault, generate, get_option, lib,
+                      set_option, version)
+
+__all__ = ["Plan", "MapfuseError", "VmFault", "ParseError", "generate", "set_option",
+           "get_option", "lib", "version"]

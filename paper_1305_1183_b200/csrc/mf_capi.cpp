@@ -1,0 +1,272 @@
+// mf_capi.cpp -- extern "C" surface declared in include/mapfuse_b200.h.
+#include "mapfuse_b200.h"
+
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "mf_builtin.hpp"
+#include "mf_compile.hpp"
+#include "mf_exec.hpp"
+#include "mf_kernels.cuh"
+
+using namespace mapfuse::b200;
+
+struct mf_plan {
+  NativePlan plan;
+  mutable Workspace ws;
+};
+
+namespace {
+
+thread_local std::string g_error;
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return MF_OK;
+  } catch (const Invalid& e) {
+    g_error = e.what();
+    return MF_ERR_INVALID;
+  } catch (const Fault& e) {
+    g_error = e.what();
+    return MF_ERR_FAULT;
+  } catch (const std::invalid_argument& e) {
+    g_error = e.what();
+    return MF_ERR_INVALID;
+  } catch (const std::exception& e) {
+    g_error = e.what();
+    return classify_exception(e);
+  } catch (...) {
+    g_error = "unknown error";
+    return MF_ERR_FAULT;
+  }
+}
+
+int copy_out(const std::string& s, char* buf, int cap) {
+  const int need = (int)s.size() + 1;
+  if (buf && cap >= need) std::memcpy(buf, s.c_str(), (size_t)need);
+  return need;
+}
+
+BufMap to_map(const mf_buffer* b, int n) {
+  BufMap m;
+  for (int i = 0; i < n; ++i) {
+    if (!b[i].name) throw Invalid("buffer without a name");
+    DevBuf d;
+    d.ptr = b[i].data;
+    d.rows = b[i].rows;
+    d.cols = b[i].cols;
+    m[b[i].name] = d;
+  }
+  return m;
+}
+
+ScalarMap to_scalars(const mf_scalar* s, int n) {
+  ScalarMap m;
+  for (int i = 0; i < n; ++i) {
+    if (!s[i].name) throw Invalid("scalar without a name");
+    m[s[i].name] = (double)s[i].value;
+  }
+  return m;
+}
+
+void fill_stats(const NativePlan& p, int k0, int k1, const BufMap& b, mf_stats* st) {
+  if (!st) return;
+  st->bytes_loaded = 0;
+  st->bytes_stored = 0;
+  st->kernels = k1 - k0;
+  st->ms = 0.0;
+  for (int k = k0; k < k1; ++k) {
+    const auto& kern = p.kernels[k];
+    int64_t m = p.rows, n = p.cols;
+    if (kern.kind == NativeKernel::Kind::Matrix) {
+      auto it = b.find(kern.matrix.mats[0]);
+      if (it != b.end()) {
+        m = it->second.rows;
+        n = it->second.cols;
+      }
+      st->bytes_loaded += kern.bytes_loaded(m, n);
+      st->bytes_stored += kern.bytes_stored(m, n);
+    } else {
+      auto it = b.find(kern.stream.inputs[0]);
+      int64_t len = it != b.end() ? it->second.size() : n;
+      st->bytes_loaded += kern.bytes_loaded(1, len);
+      st->bytes_stored += kern.bytes_stored(1, len);
+    }
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* mf_last_error(void) { return g_error.c_str(); }
+const char* mf_version(void) { return "mapfuse-b200 0.1 (sm_100a)"; }
+
+int mf_compile(const char* script_text, const char* manifest, int rows, int cols, int mode,
+               mf_plan** out) {
+  return guarded([&] {
+    if (!script_text || !out) throw Invalid("null argument");
+    auto p = std::make_unique<mf_plan>();
+    p->plan = compile_script(script_text, manifest ? std::string(manifest) : std::string(), rows,
+                             cols, mode);
+    *out = p.release();
+  });
+}
+
+int mf_compile_sequence(const char* sequence, int rows, int cols, int mode, mf_plan** out) {
+  return guarded([&] {
+    if (!sequence || !out) throw Invalid("null argument");
+    auto p = std::make_unique<mf_plan>();
+    if (mode == 10 || mode == 11)  // hand-derived plans (test cross-check only)
+      p->plan = builtin_plan(sequence, rows, cols, mode == 10);
+    else
+      p->plan = compile_sequence(sequence, rows, cols, mode);
+    *out = p.release();
+  });
+}
+
+int mf_plan_create(const char* kernel_ir_text, int rows, int cols, mf_plan** out) {
+  return guarded([&] {
+    if (!kernel_ir_text || !out) throw Invalid("null argument");
+    auto p = std::make_unique<mf_plan>();
+    p->plan = plan_from_kernel_text(kernel_ir_text, rows, cols);
+    *out = p.release();
+  });
+}
+
+void mf_plan_destroy(mf_plan* plan) { delete plan; }
+
+int mf_plan_num_kernels(const mf_plan* plan) {
+  return plan ? (int)plan->plan.kernels.size() : -1;
+}
+
+int mf_plan_describe(const mf_plan* plan, char* buf, int cap) {
+  if (!plan) return -1;
+  return copy_out(plan->plan.describe_json(), buf, cap);
+}
+
+int mf_plan_kernel_text(const mf_plan* plan, int k, char* buf, int cap) {
+  if (!plan || k < 0 || k >= (int)plan->plan.kernels.size()) return -1;
+  std::string s = k < (int)plan->plan.kernel_ir.size() ? plan->plan.kernel_ir[k] : std::string();
+  return copy_out(s, buf, cap);
+}
+
+int mf_plan_kernel_column_outputs(const mf_plan* plan, int k, char* buf, int cap) {
+  if (!plan || k < 0 || k >= (int)plan->plan.kernels.size()) return -1;
+  std::string s;
+  for (const auto& n : plan->plan.kernels[k].column_outputs()) s += (s.empty() ? "" : ",") + n;
+  return copy_out(s, buf, cap);
+}
+
+int mf_launch(const mf_plan* plan, const mf_buffer* buffers, int nbuf, const mf_scalar* scalars,
+              int nscalars, void* stream, mf_stats* stats) {
+  return guarded([&] {
+    if (!plan) throw Invalid("null plan");
+    BufMap b = complete_bindings(plan->plan, to_map(buffers, nbuf), plan->ws);
+    ScalarMap s = to_scalars(scalars, nscalars);
+    auto st = static_cast<cudaStream_t>(stream);
+    for (int k = 0; k < (int)plan->plan.kernels.size(); ++k) run_kernel(plan->plan, k, b, s, st, plan->ws);
+    fill_stats(plan->plan, 0, (int)plan->plan.kernels.size(), b, stats);
+  });
+}
+
+int mf_launch_kernel(const mf_plan* plan, int k, const mf_buffer* buffers, int nbuf,
+                     const mf_scalar* scalars, int nscalars, void* stream, mf_stats* stats) {
+  return guarded([&] {
+    if (!plan) throw Invalid("null plan");
+    BufMap b = complete_bindings(plan->plan, to_map(buffers, nbuf), plan->ws);
+    run_kernel(plan->plan, k, b, to_scalars(scalars, nscalars), static_cast<cudaStream_t>(stream),
+               plan->ws);
+    fill_stats(plan->plan, k, k + 1, b, stats);
+  });
+}
+
+int mf_launch_host(const mf_plan* plan, const mf_buffer* host_buffers, int nbuf,
+                   const mf_scalar* scalars, int nscalars, mf_stats* stats) {
+  return guarded([&] {
+    if (!plan) throw Invalid("null plan");
+    const NativePlan& P = plan->plan;
+    BufMap dev;
+    for (int i = 0; i < nbuf; ++i) {
+      const mf_buffer& h = host_buffers[i];
+      if (!h.name || !h.data) throw Invalid("host buffer without name or data");
+      DevBuf d;
+      d.rows = h.rows;
+      d.cols = h.cols;
+      d.ptr = plan->ws.named(std::string("__host__") + h.name, (int64_t)h.rows * h.cols);
+      dev[h.name] = d;
+    }
+    cudaStream_t st = nullptr;
+    for (int i = 0; i < nbuf; ++i) {
+      const mf_buffer& h = host_buffers[i];
+      const BufferSpec* spec = P.find(h.name);
+      if (spec && spec->role != Role::Input) continue;  // outputs are overwritten
+      check_cuda(cudaMemcpyAsync(dev[h.name].ptr, h.data, sizeof(float) * (size_t)h.rows * h.cols,
+                                 cudaMemcpyHostToDevice, st),
+                 "cudaMemcpy H2D");
+    }
+    BufMap b = complete_bindings(P, dev, plan->ws);
+    ScalarMap s = to_scalars(scalars, nscalars);
+    cudaEvent_t e0, e1;
+    check_cuda(cudaEventCreate(&e0), "cudaEventCreate");
+    check_cuda(cudaEventCreate(&e1), "cudaEventCreate");
+    check_cuda(cudaEventRecord(e0, st), "cudaEventRecord");
+    for (int k = 0; k < (int)P.kernels.size(); ++k) run_kernel(P, k, b, s, st, plan->ws);
+    check_cuda(cudaEventRecord(e1, st), "cudaEventRecord");
+    for (int i = 0; i < nbuf; ++i) {
+      const mf_buffer& h = host_buffers[i];
+      const BufferSpec* spec = P.find(h.name);
+      if (spec && spec->role == Role::Input) continue;
+      check_cuda(cudaMemcpyAsync(h.data, dev[h.name].ptr, sizeof(float) * (size_t)h.rows * h.cols,
+                                 cudaMemcpyDeviceToHost, st),
+                 "cudaMemcpy D2H");
+    }
+    check_cuda(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    fill_stats(P, 0, (int)P.kernels.size(), b, stats);
+    if (stats) stats->ms = ms;
+  });
+}
+
+int mf_generate(float* dev, int64_t rows, int64_t cols, int64_t ld, uint64_t seed, int64_t row0,
+                int64_t ncols_global, void* stream) {
+  return guarded([&] {
+    if (!dev) throw Invalid("null device pointer");
+    check_cuda(launch_generate(dev, rows, cols, ld, seed, row0, ncols_global,
+                               static_cast<cudaStream_t>(stream)),
+               "generate");
+  });
+}
+
+int mf_set_option(const char* key, int value) {
+  return guarded([&] {
+    std::string k = key ? key : "";
+    if (k == "matrix_k") {
+      if (value != 2 && value != 4) throw Invalid("matrix_k must be 2 or 4");
+      options().matrix_k = value;
+    } else if (k == "f64acc") {
+      options().f64acc = value ? 1 : 0;
+    } else if (k == "occupancy") {
+      if (value < 1 || value > 8) throw Invalid("occupancy must be 1..8");
+      options().occupancy = value;
+    } else {
+      throw Invalid("unknown option '" + k + "'");
+    }
+  });
+}
+
+int mf_get_option(const char* key) {
+  std::string k = key ? key : "";
+  if (k == "matrix_k") return options().matrix_k;
+  if (k == "f64acc") return options().f64acc;
+  if (k == "occupancy") return options().occupancy;
+  return -1;
+}
+
+}  // extern "C"

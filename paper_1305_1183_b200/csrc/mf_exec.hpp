@@ -1,0 +1,69 @@
+// mf_exec.hpp -- binds a NativePlan to device buffers and launches it.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "mf_native.hpp"
+
+namespace mapfuse::b200 {
+
+// vm::VmFault analogue (proj/include/mapfuse/vm.hpp:21-23).
+struct Fault : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+// ir::ParseError / invalid-argument analogue.
+struct Invalid : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+struct DevBuf {
+  float* ptr = nullptr;
+  int64_t rows = 0, cols = 0;
+  int64_t size() const { return rows * cols; }
+};
+using BufMap = std::map<std::string, DevBuf>;
+using ScalarMap = std::map<std::string, double>;
+
+struct EngineOptions {
+  int matrix_k = 2;
+  int f64acc = 0;
+  int occupancy = 2;
+};
+EngineOptions& options();
+
+// Device scratch owned by one plan: cross-CTA partials, barrier / ticket
+// counters, unbound intermediates, and (for host launches) device mirrors of
+// host buffers.  Launches of one plan on one stream are serialized by the
+// stream; the mutex guards the allocation tables.
+class Workspace {
+ public:
+  ~Workspace();
+  void* scratch(size_t bytes, cudaStream_t s);   // grows on demand
+  unsigned* counters(cudaStream_t s);            // zeroed once, self-resetting
+  float* named(const std::string& key, int64_t words);  // persistent per key
+  std::mutex mu;
+
+ private:
+  void* scratch_ = nullptr;
+  size_t scratch_bytes_ = 0;
+  unsigned* counters_ = nullptr;
+  std::map<std::string, std::pair<float*, int64_t>> named_;
+};
+
+// Launches plan.kernels[k]; throws Fault / Invalid.
+void run_kernel(const NativePlan& plan, int k, const BufMap& bufs, const ScalarMap& scalars,
+                cudaStream_t stream, Workspace& ws);
+// Binds any plan intermediates the caller left unbound (workspace-backed).
+BufMap complete_bindings(const NativePlan& plan, const BufMap& bufs, Workspace& ws);
+
+int device_sm_count();
+void check_cuda(cudaError_t e, const char* what);
+
+}  // namespace mapfuse::b200

@@ -1,0 +1,552 @@
+// mf_kernels.cu -- hand-written sm_100a kernels for fused map/reduce BLAS-1/2.
+//
+// Everything here is HBM-bound (<= 1 flop/byte): no tensor cores, no GEMM
+// reshaping.  The design levers are the ones the roofline rewards:
+//   * every matrix element is read from HBM exactly once per fused kernel
+//     (128-bit, evict-first loads), every output written once;
+//   * persistent grids sized to the SM count (148 on B200) x occupancy;
+//   * intermediates stay in registers (the paper's register rule, section
+//     3.2.3): a thread owns fixed column slots of the matrix for the whole
+//     pass, so column reductions (sgemtv, A^T r) need no transpose through
+//     shared memory -- the reference's stride-33 tile transpose
+//     (proj/data/blas_library.mf:325-335) disappears;
+//   * row reductions (sgemv, A p) are batched R rows at a time:
+//     register partials -> warp butterfly (log2 R shuffles per value) ->
+//     one shared-memory combine per batch;
+//   * cross-CTA combination is deterministic: per-CTA partials land in L2,
+//     one grid barrier (cooperative launch), then every CTA finalizes a
+//     slice -- no float atomics, results are run-to-run reproducible
+//     (the reference's VM is deterministic too, proj/include/mapfuse/vm.hpp:15).
+#include "mf_kernels.cuh"
+
+#include <algorithm>
+#include <cstdio>
+
+namespace mapfuse::b200 {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+
+// Streaming 128-bit load: bypass L1 allocation and mark the L2 line
+// evict-first -- matrix and stream operands are touched exactly once.
+__device__ __forceinline__ unsigned long long evict_first_policy() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+__device__ __forceinline__ float4 ld_stream(const float4* p) {
+  float4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p), "l"(evict_first_policy()));
+  return v;
+}
+
+__device__ __forceinline__ void st_stream(float4* p, float4 v) {
+  asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x),
+               "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
+
+__device__ __forceinline__ float comp(const float4& v, int c) {
+  return c == 0 ? v.x : (c == 1 ? v.y : (c == 2 ? v.z : v.w));
+}
+__device__ __forceinline__ void set_comp(float4& v, int c, float x) {
+  if (c == 0) v.x = x;
+  else if (c == 1) v.y = x;
+  else if (c == 2) v.z = x;
+  else v.w = x;
+}
+
+// ---------------------------------------------------------------------------
+// Grid barrier for co-resident (cooperatively launched) grids.  bar[0] counts
+// arrivals, bar[1] is a generation number; self-resetting across launches.
+__device__ __forceinline__ void grid_barrier(unsigned* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* gen = bar + 1;
+    unsigned g = *gen;
+    __threadfence();
+    unsigned arrived = atomicAdd(bar, 1u);
+    if (arrived == gridDim.x - 1) {
+      atomicExch(bar, 0u);
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (*gen == g) __nanosleep(64);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// Depth-1 stream kernel.
+
+template <int NIN, int NOUT, bool DOT>
+struct StreamBody {
+  __device__ __forceinline__ static void apply(const StreamArgs& a, const float4 (&v)[NIN],
+                                               long long idx, double& acc) {
+    float4 o[NOUT > 0 ? NOUT : 1];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      double x[NIN];
+#pragma unroll
+      for (int k = 0; k < NIN; ++k) x[k] = (double)comp(v[k], c);
+#pragma unroll
+      for (int q = 0; q < NOUT; ++q) {
+        // left-to-right, no contraction: sum_k coef_k * x_k as the reference
+        // evaluates its fp64 formulas (blas.cpp:190, :258, :264)
+        double s = __dmul_rn(a.coef[q][0], x[0]);
+#pragma unroll
+        for (int k = 1; k < NIN; ++k) s = __dadd_rn(s, __dmul_rn(a.coef[q][k], x[k]));
+        set_comp(o[q], c, (float)s);
+      }
+      if constexpr (DOT) {
+        double p = __dmul_rn(a.da[0], x[0]);
+        double q2 = __dmul_rn(a.db[0], x[0]);
+#pragma unroll
+        for (int k = 1; k < NIN; ++k) {
+          p = __dadd_rn(p, __dmul_rn(a.da[k], x[k]));
+          q2 = __dadd_rn(q2, __dmul_rn(a.db[k], x[k]));
+        }
+        acc = fma(p, q2, acc);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < NOUT; ++q) st_stream(a.out[q] + idx, o[q]);
+  }
+};
+
+template <int NIN, int NOUT, bool DOT>
+__global__ void __launch_bounds__(kThreads) stream_kernel(StreamArgs a) {
+  constexpr int U = (NIN <= 2) ? 4 : 2;  // float4 loads in flight per input per thread
+  const long long stride = (long long)gridDim.x * kThreads;
+  long long i = (long long)blockIdx.x * kThreads + threadIdx.x;
+  double acc = 0.0;
+  for (; i + (U - 1) * stride < a.n4; i += U * stride) {
+    float4 v[U][NIN];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int k = 0; k < NIN; ++k) v[u][k] = ld_stream(a.in[k] + i + u * stride);
+#pragma unroll
+    for (int u = 0; u < U; ++u) StreamBody<NIN, NOUT, DOT>::apply(a, v[u], i + u * stride, acc);
+  }
+  for (; i < a.n4; i += stride) {
+    float4 v[NIN];
+#pragma unroll
+    for (int k = 0; k < NIN; ++k) v[k] = ld_stream(a.in[k] + i);
+    StreamBody<NIN, NOUT, DOT>::apply(a, v, i, acc);
+  }
+  if constexpr (DOT) {
+    __shared__ double wsum[kWarps];
+    __shared__ bool last;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double s = 0.0;
+      for (int w = 0; w < kWarps; ++w) s += wsum[w];
+      a.part[blockIdx.x] = s;
+      __threadfence();
+      last = (atomicAdd(a.ticket, 1u) == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (last) {  // deterministic: fixed assignment of partials + fixed tree
+      __threadfence();
+      double s = 0.0;
+      for (int b = threadIdx.x; b < (int)gridDim.x; b += kThreads) s += __ldcg(a.part + b);
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+      if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = s;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < kWarps; ++w) t += wsum[w];
+        *a.r = (float)t;
+        *a.ticket = 0u;  // ready for the next launch
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Depth-2 matrix kernel.
+//
+// Mapping: a CTA owns a tile = (column chunk cb) x (row band rb).  Thread t
+// owns the K float4 column slots c_k = cb*4*T*K + 4*(t + T*k) for the whole
+// band: the matching slices of the row-reduction vectors x (and of the rank
+// vectors v1, v2) and the column-reduction accumulators live in registers.
+// Rows stream through in batches of R: all R*K (x NMAT) 128-bit loads of a
+// batch are issued before any arithmetic.
+
+// Butterfly reduce-scatter: NV values per lane (NV power of two <= 32) ->
+// lane l ends up holding the warp total of value index (l >> (5 - log2 NV)).
+template <typename T, int NV>
+__device__ __forceinline__ T butterfly(T (&v)[NV], int lane) {
+  static_assert((NV & (NV - 1)) == 0 && NV <= 32, "NV must be a power of two <= 32");
+  int width = NV;
+  int mask = 16;
+#pragma unroll
+  for (int step = 0; (NV >> step) > 1; ++step) {
+    const int half = (NV >> step) >> 1;
+    const bool hi = (lane & mask) != 0;
+#pragma unroll
+    for (int j = 0; j < half; ++j) {
+      T send = hi ? v[j] : v[j + half];
+      T keep = hi ? v[j + half] : v[j];
+      v[j] = keep + __shfl_xor_sync(0xffffffffu, send, mask);
+    }
+    mask >>= 1;
+    width >>= 1;
+  }
+  T r = v[0];
+  for (; mask > 0; mask >>= 1) r += __shfl_xor_sync(0xffffffffu, r, mask);
+  return r;
+}
+
+template <typename ACC>
+__device__ __forceinline__ ACC fmacc(ACC a, ACC b, ACC c);
+template <>
+__device__ __forceinline__ float fmacc<float>(float a, float b, float c) {
+  return fmaf(a, b, c);
+}
+template <>
+__device__ __forceinline__ double fmacc<double>(double a, double b, double c) {
+  return fma(a, b, c);
+}
+
+template <int NMAT, int NRANK, bool STORE, int NROW, int NCOL, int K, int R, typename ACC>
+__global__ void __launch_bounds__(kThreads, 2) matrix_kernel(MatrixArgs a) {
+  constexpr int NV = (NROW > 0 ? NROW : 1) * R;
+  constexpr long long C = 4LL * kThreads * K;
+  __shared__ ACC red[2][kWarps][NV];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  ACC* colpart = static_cast<ACC*>(a.colpart);
+  ACC* rowpart = static_cast<ACC*>(a.rowpart);
+  int buf = 0;
+
+  for (int tile = blockIdx.x; tile < a.tiles; tile += gridDim.x) {
+    const int cb = tile % a.CB, rb = tile / a.CB;
+    const long long r0 = (long long)rb * a.m / a.RB, r1 = (long long)(rb + 1) * a.m / a.RB;
+    long long col[K];
+    bool ok[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      col[k] = (long long)cb * C + 4LL * (tid + kThreads * k);
+      ok[k] = col[k] < a.n;
+    }
+    const float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 xs[NROW > 0 ? NROW : 1][K];
+    float4 vs[NRANK > 0 ? NRANK : 1][K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+#pragma unroll
+      for (int o = 0; o < NROW; ++o)
+        xs[o][k] = ok[k] ? __ldg(reinterpret_cast<const float4*>(a.xr[o] + col[k])) : zero4;
+#pragma unroll
+      for (int q = 0; q < NRANK; ++q)
+        vs[q][k] = ok[k] ? __ldg(reinterpret_cast<const float4*>(a.v[q] + col[k])) : zero4;
+    }
+    ACC cacc[NCOL > 0 ? NCOL : 1][K][4];
+#pragma unroll
+    for (int c = 0; c < NCOL; ++c)
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) cacc[c][k][e] = ACC(0);
+
+    for (long long i0 = r0; i0 < r1; i0 += R) {
+      float us[NRANK > 0 ? NRANK : 1][R];
+      float xcs[NCOL > 0 ? NCOL : 1][R];
+      float4 av[R][NMAT][K];
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) {
+        const long long i = i0 + rr;
+        const bool rv = i < r1;
+#pragma unroll
+        for (int q = 0; q < NRANK; ++q) us[q][rr] = rv ? __ldg(a.u[q] + i) : 0.f;
+#pragma unroll
+        for (int c = 0; c < NCOL; ++c) xcs[c][rr] = rv ? __ldg(a.xc[c] + i) : 0.f;
+#pragma unroll
+        for (int mt = 0; mt < NMAT; ++mt)
+#pragma unroll
+          for (int k = 0; k < K; ++k)
+            av[rr][mt][k] = (rv && ok[k])
+                                ? ld_stream(reinterpret_cast<const float4*>(a.M[mt] + i * a.ld + col[k]))
+                                : zero4;
+      }
+      ACC rp[NV];
+#pragma unroll
+      for (int j = 0; j < NV; ++j) rp[j] = ACC(0);
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          float4 st;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            ACC ev[NMAT];
+#pragma unroll
+            for (int mt = 0; mt < NMAT; ++mt) ev[mt] = (ACC)comp(av[rr][mt][k], e);
+            if constexpr (NRANK > 0) {
+              // ger2 in fp64, rounded once: bit-identical to the reference's
+              // B = A + u1 v1^T + u2 v2^T (blas.cpp:230-233)
+              double d = (double)comp(av[rr][0][k], e);
+#pragma unroll
+              for (int q = 0; q < NRANK; ++q)
+                d = __dadd_rn(d, __dmul_rn((double)us[q][rr], (double)comp(vs[q][k], e)));
+              if constexpr (STORE) set_comp(st, e, (float)d);
+              ev[0] = (ACC)d;
+            }
+#pragma unroll
+            for (int o = 0; o < NROW; ++o) {
+              const int mt = (NMAT == 2) ? o : 0;
+              rp[o * R + rr] = fmacc<ACC>(ev[mt], (ACC)comp(xs[o][k], e), rp[o * R + rr]);
+            }
+#pragma unroll
+            for (int c = 0; c < NCOL; ++c) {
+              const int mt = (NMAT == 2) ? c : 0;
+              cacc[c][k][e] = fmacc<ACC>(ev[mt], (ACC)xcs[c][rr], cacc[c][k][e]);
+            }
+          }
+          if constexpr (STORE) {
+            const long long i = i0 + rr;
+            if (i < r1 && ok[k]) st_stream(reinterpret_cast<float4*>(a.E + i * a.ld + col[k]), st);
+          }
+        }
+      }
+      if constexpr (NROW > 0) {
+        ACC wsum = butterfly<ACC, NV>(rp, lane);
+        constexpr int group = 32 / NV;  // lanes holding the same value index
+        if ((lane & (group - 1)) == 0) red[buf][warp][lane / group] = wsum;
+        __syncthreads();
+        if (tid < NV) {
+          ACC s = red[buf][0][tid];
+#pragma unroll
+          for (int w = 1; w < kWarps; ++w) s += red[buf][w][tid];
+          const int o = tid / R, rr = tid % R;
+          const long long i = i0 + rr;
+          if (i < r1) {
+            if (a.CB == 1) a.yr[o][i] = (float)(a.ar[o] * (double)s);
+            else rowpart[((long long)o * a.CB + cb) * a.m + i] = s;
+          }
+        }
+        buf ^= 1;
+      }
+    }
+    // column partials of this tile
+#pragma unroll
+    for (int c = 0; c < NCOL; ++c)
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+        if (ok[k]) {
+          ACC* dst = colpart + ((long long)c * a.RB + rb) * a.n + col[k];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) dst[e] = cacc[c][k][e];
+        }
+  }
+
+  if constexpr (NCOL > 0 || NROW > 0) {
+    const bool need_rows = (NROW > 0) && a.CB > 1;
+    if (NCOL == 0 && !need_rows) return;
+    grid_barrier(a.bar);
+    const long long n4 = a.n / 4, m4 = a.m / 4;
+    const long long col_slots = (long long)NCOL * n4;
+    const long long total = col_slots + (need_rows ? (long long)NROW * m4 : 0);
+    for (long long s = (long long)blockIdx.x * kThreads + tid; s < total;
+         s += (long long)gridDim.x * kThreads) {
+      if (s < col_slots) {
+        const int c = (int)(s / n4);
+        const long long j = (s % n4) * 4;
+        ACC t[4] = {ACC(0), ACC(0), ACC(0), ACC(0)};
+        for (int b = 0; b < a.RB; ++b) {
+          const ACC* p = colpart + ((long long)c * a.RB + b) * a.n + j;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) t[e] += __ldcg(p + e);
+        }
+        float4 o;
+        o.x = (float)(a.ac[c] * (double)t[0]);
+        o.y = (float)(a.ac[c] * (double)t[1]);
+        o.z = (float)(a.ac[c] * (double)t[2]);
+        o.w = (float)(a.ac[c] * (double)t[3]);
+        *reinterpret_cast<float4*>(a.yc[c] + j) = o;
+      } else {
+        const long long q = s - col_slots;
+        const int o = (int)(q / m4);
+        const long long i = (q % m4) * 4;
+        ACC t[4] = {ACC(0), ACC(0), ACC(0), ACC(0)};
+        for (int b = 0; b < a.CB; ++b) {
+          const ACC* p = rowpart + ((long long)o * a.CB + b) * a.m + i;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) t[e] += __ldcg(p + e);
+        }
+        float4 r;
+        r.x = (float)(a.ar[o] * (double)t[0]);
+        r.y = (float)(a.ar[o] * (double)t[1]);
+        r.z = (float)(a.ar[o] * (double)t[2]);
+        r.w = (float)(a.ar[o] * (double)t[3]);
+        *reinterpret_cast<float4*>(a.yr[o] + i) = r;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Synthetic data (counter-based, matches oracle/mf_oracle.c).
+
+__device__ __forceinline__ unsigned long long splitmix64(unsigned long long x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+__global__ void generate_kernel(float* out, long long rows, long long cols, long long ld,
+                                unsigned long long seed, long long row0, long long ncg) {
+  const unsigned long long hs = splitmix64(seed);
+  const long long total = rows * cols;
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long r = t / cols, c = t % cols;
+    const unsigned long long idx = (unsigned long long)(row0 + r) * (unsigned long long)ncg + c;
+    const unsigned long long h = splitmix64(idx ^ hs);
+    const unsigned k = (unsigned)(h >> 40);
+    out[r * ld + c] = (float)k * (1.0f / 8388608.0f) - 1.0f;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Dispatch tables.
+
+using MatrixFn = void (*)(MatrixArgs);
+
+template <int NMAT, int NRANK, bool STORE, int NROW, int NCOL>
+MatrixFn pick(const MatrixTuning& t) {
+  // Register budget (<= 128 at 2 CTAs/SM): shapes carrying a second matrix
+  // or the rank-2 update halve the rows per batch.
+  // Rows per batch R is cut for the shapes carrying the rank-2 update (fp64
+  // element math + the store path) or a second matrix.
+  constexpr int R2 = (NRANK > 0) ? 2 : (NMAT == 2 ? 4 : 8);
+  if (t.f64acc) return matrix_kernel<NMAT, NRANK, STORE, NROW, NCOL, 2, (R2 > 4 ? 4 : 2), double>;
+  if (t.K == 4) return matrix_kernel<NMAT, NRANK, STORE, NROW, NCOL, 4, (R2 / 2), float>;
+  return matrix_kernel<NMAT, NRANK, STORE, NROW, NCOL, 2, R2, float>;
+}
+
+MatrixFn matrix_fn(const MatrixShape& s, const MatrixTuning& t) {
+  // The instantiations the planner can emit (SURVEY.md 2.2 kernel family T1).
+  if (s == MatrixShape{1, 0, 0, 1, 0}) return pick<1, 0, false, 1, 0>(t);  // sgemv(s)
+  if (s == MatrixShape{1, 0, 0, 0, 1}) return pick<1, 0, false, 0, 1>(t);  // sgemtv
+  if (s == MatrixShape{1, 0, 0, 1, 1}) return pick<1, 0, false, 1, 1>(t);  // BiCGK
+  if (s == MatrixShape{1, 0, 0, 2, 0}) return pick<1, 0, false, 2, 0>(t);  // 2x sgemv on A
+  if (s == MatrixShape{1, 0, 0, 0, 2}) return pick<1, 0, false, 0, 2>(t);  // 2x sgemtv on A
+  if (s == MatrixShape{1, 2, 1, 0, 1}) return pick<1, 2, true, 0, 1>(t);   // ger2+sgemtv
+  if (s == MatrixShape{1, 2, 1, 0, 0}) return pick<1, 2, true, 0, 0>(t);   // ger2
+  if (s == MatrixShape{2, 0, 0, 2, 0}) return pick<2, 0, false, 2, 0>(t);  // GESUMMV
+  return nullptr;
+}
+
+template <int NIN, int NOUT, bool DOT>
+cudaError_t go_stream(const StreamArgs& a, int grid, cudaStream_t s) {
+  stream_kernel<NIN, NOUT, DOT><<<grid, kThreads, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+int stream_grid(long long n4, int sms) {
+  long long want = (long long)sms * 4;
+  long long need = (n4 + kThreads - 1) / kThreads;
+  return (int)std::max(1LL, std::min(want, need));
+}
+
+cudaError_t launch_stream(int nin, int nout, bool dot, const StreamArgs& a, int grid,
+                          cudaStream_t s) {
+#define MF_STREAM_CASE(I, O, D) \
+  if (nin == I && nout == O && dot == D) return go_stream<I, O, D>(a, grid, s);
+  MF_STREAM_CASE(1, 1, false)
+  MF_STREAM_CASE(2, 1, false)
+  MF_STREAM_CASE(3, 1, false)
+  MF_STREAM_CASE(4, 1, false)
+  MF_STREAM_CASE(2, 2, false)
+  MF_STREAM_CASE(3, 2, false)
+  MF_STREAM_CASE(4, 2, false)
+  MF_STREAM_CASE(2, 0, true)
+  MF_STREAM_CASE(3, 0, true)
+  MF_STREAM_CASE(2, 1, true)
+  MF_STREAM_CASE(3, 1, true)
+  MF_STREAM_CASE(4, 1, true)
+  MF_STREAM_CASE(4, 2, true)
+#undef MF_STREAM_CASE
+  return cudaErrorNotSupported;
+}
+
+bool matrix_shape_supported(const MatrixShape& sh) {
+  return matrix_fn(sh, MatrixTuning{}) != nullptr;
+}
+
+size_t matrix_acc_bytes(const MatrixTuning& t) { return t.f64acc ? 8 : 4; }
+
+cudaError_t matrix_config(const MatrixShape& sh, const MatrixTuning& t, long long m, long long n,
+                          int sms, MatrixArgs* a, int* grid) {
+  MatrixFn fn = matrix_fn(sh, t);
+  if (!fn) return cudaErrorNotSupported;
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, 0);
+  if (e != cudaSuccess) return e;
+  per_sm = std::max(1, std::min(per_sm, t.occupancy));
+  const int K = t.f64acc ? 2 : t.K;
+  const long long C = 4LL * kThreads * K;
+  const int CB = (int)((n + C - 1) / C);
+  const long long G = (long long)sms * per_sm;  // co-resident CTAs
+  // Row bands: the tile count (CB * RB) should be a whole multiple of the
+  // grid (no tail wave) with at least ~8 rows per band.  Search grids from G
+  // down to G/2 for one whose lcm with CB gives such a band count.
+  long long RB = 0, g = 0;
+  for (long long cand = G; cand >= std::max(1LL, G / 2) && RB == 0; --cand) {
+    long long a0 = cand, b0 = CB;
+    while (b0) { long long t0 = a0 % b0; a0 = b0; b0 = t0; }
+    const long long l = cand / a0 * CB;  // lcm(cand, CB)
+    const long long rb = l / CB;
+    if (rb <= std::max(1LL, m / 8)) { RB = rb; g = cand; }
+  }
+  if (RB == 0) {  // small problems: fewer CTAs than SMs is fine
+    RB = std::max(1LL, std::min(m / 4, std::max(1LL, G / CB)));
+    g = std::min<long long>(G, (long long)CB * RB);
+  }
+  const long long tiles = (long long)CB * RB;
+  a->CB = CB;
+  a->RB = (int)RB;
+  a->tiles = (int)tiles;
+  *grid = (int)g;
+  return cudaSuccess;
+}
+
+cudaError_t launch_matrix(const MatrixShape& sh, const MatrixTuning& t, const MatrixArgs& a,
+                          int grid, cudaStream_t s) {
+  MatrixFn fn = matrix_fn(sh, t);
+  if (!fn) return cudaErrorNotSupported;
+  const bool needs_barrier = sh.ncol > 0 || (sh.nrow > 0 && a.CB > 1);
+  MatrixArgs copy = a;
+  void* args[] = {&copy};
+  if (needs_barrier)
+    return cudaLaunchCooperativeKernel((const void*)fn, dim3(grid), dim3(kThreads), args, 0, s);
+  fn<<<grid, kThreads, 0, s>>>(copy);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_generate(float* out, long long rows, long long cols, long long ld,
+                            unsigned long long seed, long long row0, long long ncols_global,
+                            cudaStream_t s) {
+  long long total = rows * cols;
+  int grid = (int)std::max(1LL, std::min<long long>((total + 255) / 256, 148LL * 16));
+  generate_kernel<<<grid, 256, 0, s>>>(out, rows, cols, ld, seed, row0, ncols_global);
+  return cudaGetLastError();
+}
+
+}  // namespace mapfuse::b200

@@ -1,0 +1,82 @@
+// mf_kernels.cuh -- launch-side view of the sm_100a kernel families.
+//
+// Argument blocks are plain structs passed by value; the host side
+// (mf_exec.cpp) fills them from a NativeKernel + bound device buffers.
+#pragma once
+
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace mapfuse::b200 {
+
+constexpr int kStreamMaxIn = 4;
+constexpr int kStreamMaxOut = 2;
+
+// Depth-1 streaming kernel: out_o = sum_i coef[o][i] * in_i  (fp64 arithmetic,
+// one rounding to fp32 per stored value -- bit-identical to the reference's
+// fp64 formulas, proj/src/blas.cpp:185-265), plus optional
+// r = sum (da . in)(db . in) in fp64 with a deterministic two-level reduce.
+struct StreamArgs {
+  long long n4 = 0;                       // float4 slots per stream
+  const float4* in[kStreamMaxIn] = {};
+  float4* out[kStreamMaxOut] = {};
+  double coef[kStreamMaxOut][kStreamMaxIn] = {};
+  double da[kStreamMaxIn] = {}, db[kStreamMaxIn] = {};
+  float* r = nullptr;                     // 1x1 dot output
+  double* part = nullptr;                 // [gridDim.x] per-CTA partials
+  unsigned* ticket = nullptr;             // last-CTA-done counter (self-resetting)
+};
+
+// Depth-2 single-pass matrix kernel (see mf_kernels.cu for the mapping).
+struct MatrixArgs {
+  long long m = 0, n = 0, ld = 0;   // rows, cols, row stride (floats)
+  const float* M[2] = {};
+  const float* u[2] = {};
+  const float* v[2] = {};
+  float* E = nullptr;               // stored rank-updated matrix (ger2 output)
+  const float* xr[2] = {};          // row-reduction vectors (length n)
+  float* yr[2] = {};                // row outputs (length m)
+  double ar[2] = {1.0, 1.0};
+  const float* xc[2] = {};          // column-reduction vectors (length m)
+  float* yc[2] = {};                // column outputs (length n)
+  double ac[2] = {1.0, 1.0};
+  void* colpart = nullptr;          // [NCOL][RB][n] accumulator type
+  void* rowpart = nullptr;          // [NROW][CB][m] accumulator type
+  unsigned* bar = nullptr;          // grid barrier {count, generation}
+  int CB = 1, RB = 1, tiles = 1;    // column chunks, row bands, CB*RB
+};
+
+// Shape of a matrix-kernel instantiation.
+struct MatrixShape {
+  int nmat = 1, nrank = 0, store = 0, nrow = 0, ncol = 0;
+  bool operator==(const MatrixShape&) const = default;
+};
+
+struct MatrixTuning {
+  int K = 2;           // float4 column slots per thread (chunk width 1024*K columns)
+  int R = 8;           // rows per reduction batch
+  bool f64acc = false; // accumulate reductions in fp64
+  int occupancy = 2;   // CTAs per SM targeted
+};
+
+// Launchers; return cudaSuccess or the launch error.  `sms` = SM count.
+cudaError_t launch_stream(int nin, int nout, bool dot, const StreamArgs& a, int grid,
+                          cudaStream_t s);
+int stream_grid(long long n4, int sms);
+
+// Fills CB/RB/tiles and returns the grid size (co-resident for the barrier).
+cudaError_t matrix_config(const MatrixShape& sh, const MatrixTuning& t, long long m, long long n,
+                          int sms, MatrixArgs* a, int* grid);
+cudaError_t launch_matrix(const MatrixShape& sh, const MatrixTuning& t, const MatrixArgs& a,
+                          int grid, cudaStream_t s);
+bool matrix_shape_supported(const MatrixShape& sh);
+size_t matrix_acc_bytes(const MatrixTuning& t);
+
+// Counter-based synthetic data (identical to oracle/mf_oracle.c
+// mfo_hash_uniform): out[r*ld + c] = U(seed, (row0 + r) * ncols_global + c).
+cudaError_t launch_generate(float* out, long long rows, long long cols, long long ld,
+                            unsigned long long seed, long long row0, long long ncols_global,
+                            cudaStream_t s);
+
+}  // namespace mapfuse::b200

@@ -1,0 +1,216 @@
+// mf_native.cpp -- coefficient algebra, traffic accounting, plan description.
+#include "mf_native.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <set>
+#include <sstream>
+#include <stdexcept>
+
+namespace mapfuse::b200 {
+
+Coef Coef::operator*(const Coef& o) const {
+  Coef r;
+  for (const auto& a : terms)
+    for (const auto& b : o.terms) {
+      Term t{a.c * b.c, a.syms};
+      t.syms.insert(t.syms.end(), b.syms.begin(), b.syms.end());
+      std::sort(t.syms.begin(), t.syms.end());
+      r.terms.push_back(std::move(t));
+    }
+  return r;
+}
+
+Coef Coef::operator+(const Coef& o) const {
+  Coef r = *this;
+  for (const auto& t : o.terms) {
+    bool merged = false;
+    for (auto& x : r.terms)
+      if (x.syms == t.syms) {
+        x.c += t.c;
+        merged = true;
+        break;
+      }
+    if (!merged) r.terms.push_back(t);
+  }
+  r.terms.erase(std::remove_if(r.terms.begin(), r.terms.end(),
+                               [](const Term& t) { return t.c == 0.0; }),
+                r.terms.end());
+  return r;
+}
+
+double Coef::eval(const std::map<std::string, double>& scalars) const {
+  double s = 0.0;
+  bool first = true;
+  for (const auto& t : terms) {
+    double v = t.c;
+    for (const auto& n : t.syms) {
+      auto it = scalars.find(n);
+      if (it == scalars.end()) throw std::runtime_error("unbound scalar '" + n + "'");
+      v *= it->second;
+    }
+    s = first ? v : s + v;
+    first = false;
+  }
+  return s;
+}
+
+std::string Coef::str() const {
+  if (terms.empty()) return "0";
+  std::ostringstream os;
+  for (size_t i = 0; i < terms.size(); ++i) {
+    if (i) os << " + ";
+    os << terms[i].c;
+    for (const auto& s : terms[i].syms) os << "*" << s;
+  }
+  return os.str();
+}
+
+std::vector<std::string> NativeKernel::inputs() const {
+  std::vector<std::string> v;
+  auto add = [&](const std::string& s) {
+    if (!s.empty() && std::find(v.begin(), v.end(), s) == v.end()) v.push_back(s);
+  };
+  if (kind == Kind::Stream) {
+    for (const auto& s : stream.inputs) add(s);
+  } else {
+    for (const auto& s : matrix.mats) add(s);
+    for (const auto& [u, w] : matrix.rank) {
+      add(u);
+      add(w);
+    }
+    for (const auto& r : matrix.rows) add(r.x);
+    for (const auto& c : matrix.cols) add(c.x);
+  }
+  return v;
+}
+
+std::vector<std::string> NativeKernel::outputs() const {
+  std::vector<std::string> v;
+  if (kind == Kind::Stream) {
+    for (const auto& o : stream.outs) v.push_back(o.name);
+    if (stream.has_dot) v.push_back(stream.dot_out);
+  } else {
+    if (!matrix.store.empty()) v.push_back(matrix.store);
+    for (const auto& r : matrix.rows) v.push_back(r.y);
+    for (const auto& c : matrix.cols) v.push_back(c.y);
+  }
+  return v;
+}
+
+std::vector<std::string> NativeKernel::column_outputs() const {
+  std::vector<std::string> v;
+  if (kind == Kind::Stream) {
+    if (stream.has_dot) v.push_back(stream.dot_out);
+  } else {
+    for (const auto& c : matrix.cols) v.push_back(c.y);
+  }
+  return v;
+}
+
+uint64_t NativeKernel::bytes_loaded(int64_t m, int64_t n) const {
+  if (kind == Kind::Stream) return 4ull * (uint64_t)stream.inputs.size() * (uint64_t)n;
+  uint64_t b = 4ull * (uint64_t)matrix.mats.size() * (uint64_t)(m * n);
+  std::set<std::string> seen;
+  for (const auto& [u, v] : matrix.rank) {
+    if (seen.insert(u).second) b += 4ull * m;
+    if (seen.insert(v).second) b += 4ull * n;
+  }
+  for (const auto& r : matrix.rows)
+    if (seen.insert(r.x).second) b += 4ull * n;
+  for (const auto& c : matrix.cols)
+    if (seen.insert(c.x).second) b += 4ull * m;
+  return b;
+}
+
+uint64_t NativeKernel::bytes_stored(int64_t m, int64_t n) const {
+  if (kind == Kind::Stream)
+    return 4ull * (uint64_t)stream.outs.size() * (uint64_t)n + (stream.has_dot ? 4ull : 0ull);
+  uint64_t b = matrix.store.empty() ? 0 : 4ull * (uint64_t)(m * n);
+  b += 4ull * m * matrix.rows.size() + 4ull * n * matrix.cols.size();
+  return b;
+}
+
+static int64_t stream_len(const NativePlan& p, const NativeKernel& k) {
+  const std::string& first = k.stream.inputs.empty() ? std::string() : k.stream.inputs[0];
+  const BufferSpec* b = p.find(first);
+  return b ? (int64_t)b->rows * b->cols : p.cols;
+}
+
+uint64_t NativePlan::bytes_loaded() const {
+  uint64_t b = 0;
+  for (const auto& k : kernels)
+    b += k.kind == NativeKernel::Kind::Stream ? k.bytes_loaded(1, stream_len(*this, k))
+                                              : k.bytes_loaded(rows, cols);
+  return b;
+}
+
+uint64_t NativePlan::bytes_stored() const {
+  uint64_t b = 0;
+  for (const auto& k : kernels)
+    b += k.kind == NativeKernel::Kind::Stream ? k.bytes_stored(1, stream_len(*this, k))
+                                              : k.bytes_stored(rows, cols);
+  return b;
+}
+
+static std::string jstr(const std::string& s) {
+  std::string o = "\"";
+  for (char c : s) {
+    if (c == '"' || c == '\\') o += '\\';
+    if (c == '\n') {
+      o += "\\n";
+      continue;
+    }
+    o += c;
+  }
+  return o + "\"";
+}
+
+std::string NativePlan::describe_json() const {
+  std::ostringstream os;
+  os << "{\"sequence\":" << jstr(sequence) << ",\"rows\":" << rows << ",\"cols\":" << cols
+     << ",\"bytes_loaded\":" << bytes_loaded() << ",\"bytes_stored\":" << bytes_stored()
+     << ",\"kernels\":[";
+  for (size_t i = 0; i < kernels.size(); ++i) {
+    const auto& k = kernels[i];
+    if (i) os << ",";
+    os << "{\"name\":" << jstr(k.name) << ",\"kind\":"
+       << (k.kind == NativeKernel::Kind::Stream ? "\"stream\"" : "\"matrix\"") << ",\"calls\":[";
+    for (size_t j = 0; j < k.calls.size(); ++j) os << (j ? "," : "") << k.calls[j];
+    os << "],\"inputs\":[";
+    auto in = k.inputs();
+    for (size_t j = 0; j < in.size(); ++j) os << (j ? "," : "") << jstr(in[j]);
+    os << "],\"outputs\":[";
+    auto out = k.outputs();
+    for (size_t j = 0; j < out.size(); ++j) os << (j ? "," : "") << jstr(out[j]);
+    os << "],\"column_outputs\":[";
+    auto co = k.column_outputs();
+    for (size_t j = 0; j < co.size(); ++j) os << (j ? "," : "") << jstr(co[j]);
+    os << "]";
+    if (k.kind == NativeKernel::Kind::Matrix) {
+      os << ",\"shape\":{\"mats\":" << k.matrix.mats.size() << ",\"rank\":" << k.matrix.rank.size()
+         << ",\"store\":" << (k.matrix.store.empty() ? 0 : 1) << ",\"rows\":" << k.matrix.rows.size()
+         << ",\"cols\":" << k.matrix.cols.size() << "}";
+    } else {
+      os << ",\"shape\":{\"inputs\":" << k.stream.inputs.size() << ",\"outs\":"
+         << k.stream.outs.size() << ",\"dot\":" << (k.stream.has_dot ? 1 : 0) << "}";
+    }
+    os << "}";
+  }
+  os << "],\"buffers\":[";
+  for (size_t i = 0; i < buffers.size(); ++i) {
+    const auto& b = buffers[i];
+    if (i) os << ",";
+    os << "{\"name\":" << jstr(b.name) << ",\"rows\":" << b.rows << ",\"cols\":" << b.cols
+       << ",\"role\":\""
+       << (b.role == Role::Input ? "input" : (b.role == Role::Output ? "output" : "intermediate"))
+       << "\",\"scalar\":" << (b.scalar ? "true" : "false")
+       << ",\"row_indexed\":" << (b.row_indexed ? "true" : "false") << "}";
+  }
+  os << "],\"scalars\":[";
+  for (size_t i = 0; i < scalars.size(); ++i) os << (i ? "," : "") << jstr(scalars[i]);
+  os << "]}";
+  return os.str();
+}
+
+}  // namespace mapfuse::b200

@@ -1,0 +1,261 @@
+"""Python binding of the C-ABI (include/mapfuse_b200.h) -- the ctypes stub a
+maintainer of the reference would add next to its (placeholder) pybind module
+(/root/reference/proj/bindings/module.cpp:1-2).
+
+The native library is mandatory: if ``libmapfuse_b200.so`` is missing or
+fails to load, every entry point raises -- there is no CPU fallback.
+Device buffers are passed as torch CUDA tensors (torch is plumbing only: it
+owns device memory and streams); host launches take numpy arrays.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+import os
+import threading
+from typing import Dict, Mapping, Optional
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libmapfuse_b200.so")
+
+MF_OK, MF_ERR_FAULT, MF_ERR_INVALID = 0, 1, 2
+MODES = {"fused": 0, "unfused": 1, "builtin_fused": 10, "builtin_unfused": 11}
+
+
+class MapfuseError(RuntimeError):
+    """Raised for MF_ERR_* returns; ``code`` is the C status."""
+
+    def __init__(self, code: int, msg: str):
+        super().__init__(msg)
+        self.code = code
+
+
+class VmFault(MapfuseError):
+    """MF_ERR_FAULT -- the vm::VmFault analogue (proj/include/mapfuse/vm.hpp:21)."""
+
+
+class ParseError(MapfuseError):
+    """MF_ERR_INVALID -- ir::ParseError / validation (proj/include/mapfuse/ir.hpp:35)."""
+
+
+class MfBuffer(C.Structure):
+    _fields_ = [("name", C.c_char_p), ("rows", C.c_int), ("cols", C.c_int), ("data", C.c_void_p)]
+
+
+class MfScalar(C.Structure):
+    _fields_ = [("name", C.c_char_p), ("value", C.c_float)]
+
+
+class MfStats(C.Structure):
+    _fields_ = [("bytes_loaded", C.c_uint64), ("bytes_stored", C.c_uint64), ("ms", C.c_double),
+                ("kernels", C.c_int)]
+
+    def as_dict(self):
+        return {"bytes_loaded": int(self.bytes_loaded), "bytes_stored": int(self.bytes_stored),
+                "ms": float(self.ms), "kernels": int(self.kernels)}
+
+
+_lib = None
+_lock = threading.Lock()
+
+EXPORTS = [
+    "mf_compile", "mf_compile_sequence", "mf_plan_create", "mf_plan_destroy",
+    "mf_plan_num_kernels", "mf_plan_describe", "mf_plan_kernel_text",
+    "mf_plan_kernel_column_outputs", "mf_launch", "mf_launch_kernel", "mf_launch_host",
+    "mf_generate", "mf_set_option", "mf_get_option", "mf_last_error", "mf_version",
+]
+
+
+def lib() -> C.CDLL:
+    """Loads the native engine (raises if it is not built)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError("mapfuse-b200 native library missing (%s); build it with "
+                               "`python -m paper_1305_1183_b200.build`" % LIB_PATH)
+        L = C.CDLL(LIB_PATH)
+        P = C.POINTER
+        L.mf_compile.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_int, C.c_int, P(C.c_void_p)]
+        L.mf_compile_sequence.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int, P(C.c_void_p)]
+        L.mf_plan_create.argtypes = [C.c_char_p, C.c_int, C.c_int, P(C.c_void_p)]
+        L.mf_plan_destroy.argtypes = [C.c_void_p]
+        L.mf_plan_num_kernels.argtypes = [C.c_void_p]
+        for fn in ("mf_plan_describe",):
+            getattr(L, fn).argtypes = [C.c_void_p, C.c_char_p, C.c_int]
+        for fn in ("mf_plan_kernel_text", "mf_plan_kernel_column_outputs"):
+            getattr(L, fn).argtypes = [C.c_void_p, C.c_int, C.c_char_p, C.c_int]
+        L.mf_launch.argtypes = [C.c_void_p, P(MfBuffer), C.c_int, P(MfScalar), C.c_int,
+                                C.c_void_p, P(MfStats)]
+        L.mf_launch_kernel.argtypes = [C.c_void_p, C.c_int, P(MfBuffer), C.c_int, P(MfScalar),
+                                       C.c_int, C.c_void_p, P(MfStats)]
+        L.mf_launch_host.argtypes = [C.c_void_p, P(MfBuffer), C.c_int, P(MfScalar), C.c_int,
+                                     P(MfStats)]
+        L.mf_generate.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_uint64,
+                                  C.c_int64, C.c_int64, C.c_void_p]
+        L.mf_set_option.argtypes = [C.c_char_p, C.c_int]
+        L.mf_get_option.argtypes = [C.c_char_p]
+        L.mf_last_error.restype = C.c_char_p
+        L.mf_version.restype = C.c_char_p
+        _lib = L
+        return L
+
+
+def _check(rc: int) -> None:
+    if rc == MF_OK:
+        return
+    msg = lib().mf_last_error().decode(errors="replace")
+    if rc == MF_ERR_FAULT:
+        raise VmFault(rc, msg)
+    if rc == MF_ERR_INVALID:
+        raise ParseError(rc, msg)
+    raise MapfuseError(rc, msg)
+
+
+def _string(fn, *args) -> str:
+    need = fn(*args, None, 0)
+    if need < 0:
+        raise MapfuseError(-1, "invalid plan or index")
+    buf = C.create_string_buffer(need)
+    fn(*args, buf, need)
+    return buf.value.decode()
+
+
+def _shape(t):
+    if t.dim() == 1:
+        return 1, int(t.shape[0])
+    if t.dim() == 2:
+        return int(t.shape[0]), int(t.shape[1])
+    if t.numel() == 1:
+        return 1, 1
+    raise ValueError("buffers must be 1-D or 2-D")
+
+
+def _stream_ptr(stream) -> Optional[int]:
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+class Plan:
+    """A compiled fused-sequence plan: one or more sm_100a kernels."""
+
+    def __init__(self, handle: int):
+        self.h = C.c_void_p(handle)
+
+    def __del__(self):
+        try:
+            if self.h and _lib is not None:
+                _lib.mf_plan_destroy(self.h)
+        except Exception:
+            pass
+
+    # -- construction --------------------------------------------------------
+    @classmethod
+    def compile(cls, script: str, rows: int, cols: int, mode: str = "fused",
+                manifest: Optional[str] = None) -> "Plan":
+        h = C.c_void_p()
+        _check(lib().mf_compile(script.encode(), manifest.encode() if manifest else None, rows,
+                                cols, MODES[mode], C.byref(h)))
+        return cls(h.value)
+
+    @classmethod
+    def sequence(cls, name: str, rows: int, cols: int, mode: str = "fused") -> "Plan":
+        h = C.c_void_p()
+        _check(lib().mf_compile_sequence(name.encode(), rows, cols, MODES[mode], C.byref(h)))
+        return cls(h.value)
+
+    @classmethod
+    def from_kernel_text(cls, text: str, rows: int, cols: int) -> "Plan":
+        h = C.c_void_p()
+        _check(lib().mf_plan_create(text.encode(), rows, cols, C.byref(h)))
+        return cls(h.value)
+
+    # -- introspection ---------------------------------------------------------
+    @property
+    def num_kernels(self) -> int:
+        return lib().mf_plan_num_kernels(self.h)
+
+    def describe(self) -> dict:
+        return json.loads(_string(lib().mf_plan_describe, self.h))
+
+    def kernel_text(self, k: int) -> str:
+        return _string(lib().mf_plan_kernel_text, self.h, k)
+
+    def column_outputs(self, k: int):
+        s = _string(lib().mf_plan_kernel_column_outputs, self.h, k)
+        return [x for x in s.split(",") if x]
+
+    # -- launches ----------------------------------------------------------------
+    @staticmethod
+    def _args(buffers: Mapping[str, object], scalars: Mapping[str, float], host: bool):
+        keep = []
+        arr = (MfBuffer * max(1, len(buffers)))()
+        for i, (name, t) in enumerate(buffers.items()):
+            nb = name.encode()
+            keep.append(nb)
+            if host:
+                import numpy as np
+                if not (isinstance(t, np.ndarray) and t.dtype == np.float32 and t.flags.c_contiguous):
+                    raise TypeError("host buffer %r must be a C-contiguous float32 ndarray" % name)
+                r, c = (1, t.size) if t.ndim == 1 else (t.shape[0], t.shape[1])
+                arr[i] = MfBuffer(nb, r, c, t.ctypes.data)
+            else:
+                if not t.is_cuda or not t.is_contiguous() or str(t.dtype) != "torch.float32":
+                    raise TypeError("device buffer %r must be a contiguous float32 CUDA tensor" % name)
+                r, c = _shape(t)
+                arr[i] = MfBuffer(nb, r, c, t.data_ptr())
+        sc = (MfScalar * max(1, len(scalars)))()
+        for i, (name, v) in enumerate(scalars.items()):
+            nb = name.encode()
+            keep.append(nb)
+            sc[i] = MfScalar(nb, float(v))
+        return arr, len(buffers), sc, len(scalars), keep
+
+    def launch(self, buffers: Mapping[str, object], scalars: Mapping[str, float] = {},
+               stream=None) -> Dict[str, float]:
+        arr, nb, sc, ns, _keep = self._args(buffers, scalars, host=False)
+        st = MfStats()
+        _check(lib().mf_launch(self.h, arr, nb, sc, ns, C.c_void_p(_stream_ptr(stream)),
+                               C.byref(st)))
+        return st.as_dict()
+
+    def launch_kernel(self, k: int, buffers: Mapping[str, object],
+                      scalars: Mapping[str, float] = {}, stream=None) -> Dict[str, float]:
+        arr, nb, sc, ns, _keep = self._args(buffers, scalars, host=False)
+        st = MfStats()
+        _check(lib().mf_launch_kernel(self.h, k, arr, nb, sc, ns,
+                                      C.c_void_p(_stream_ptr(stream)), C.byref(st)))
+        return st.as_dict()
+
+    def launch_host(self, buffers: Mapping[str, object],
+                    scalars: Mapping[str, float] = {}) -> Dict[str, float]:
+        """vm::launch's contract: host arrays in, outputs written back in place."""
+        arr, nb, sc, ns, _keep = self._args(buffers, scalars, host=True)
+        st = MfStats()
+        _check(lib().mf_launch_host(self.h, arr, nb, sc, ns, C.byref(st)))
+        return st.as_dict()
+
+
+def generate(t, seed: int, row0: int = 0, ncols_global: Optional[int] = None, stream=None) -> None:
+    """Fills a CUDA tensor with the counter-based U(-1,1) stream (device-side)."""
+    r, c = _shape(t)
+    _check(lib().mf_generate(C.c_void_p(t.data_ptr()), r, c, c, seed, row0,
+                             ncols_global if ncols_global is not None else c,
+                             C.c_void_p(_stream_ptr(stream))))
+
+
+def set_option(key: str, value: int) -> None:
+    _check(lib().mf_set_option(key.encode(), int(value)))
+
+
+def get_option(key: str) -> int:
+    return lib().mf_get_option(key.encode())
+
+
+def version() -> str:
+    return lib().mf_version().decode()

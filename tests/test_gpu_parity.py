@@ -1,0 +1,181 @@
+"""GPU parity: the sm_100a kernels vs the pinned oracle, through the C-ABI.
+
+Each golden fixture (produced by the unmodified reference) is replayed:
+  fused plan   vs reference_execute (blas.cpp:178)   -- maps bit-exact,
+                                                       reductions within tau*S
+  unfused plan vs reference_run_script (per-call)     -- same bars
+Larger random problems are checked against the C restatement.
+"""
+import numpy as np
+import pytest
+
+from golden_util import all_goldens
+from gpu_util import check_output, scale_bound
+from oracle import COracle
+
+pytestmark = pytest.mark.gpu
+GOLDENS = all_goldens()
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+    import paper_1305_1183_b200 as mf
+    mf.lib()
+    return torch, mf, COracle()
+
+
+def run_plan(torch, plan, vals, outputs_shape):
+    bufs = {}
+    scal = {}
+    for k, v in vals.items():
+        if isinstance(v, np.ndarray):
+            bufs[k] = torch.from_numpy(np.ascontiguousarray(v, np.float32)).cuda()
+        else:
+            scal[k] = float(v)
+    for k, shp in outputs_shape.items():
+        bufs[k] = torch.full(shp, float("nan"), device="cuda", dtype=torch.float32)
+    plan.launch(bufs, scal)
+    torch.cuda.synchronize()
+    return {k: bufs[k].cpu().numpy() for k in outputs_shape}
+
+
+def out_shapes(plan):
+    d = plan.describe()
+    return {b["name"]: ((b["rows"], b["cols"]) if b["rows"] > 1 else (b["cols"],))
+            for b in d["buffers"] if b["role"] == "output"}
+
+
+@pytest.mark.parametrize("mode", ["fused", "unfused"])
+@pytest.mark.parametrize("g", GOLDENS, ids=lambda g: g.name)
+def test_golden(env, g, mode):
+    torch, mf, co = env
+    plan = mf.Plan.sequence(g.seq, g.meta["requested"][0], g.meta["requested"][1], mode)
+    shapes = out_shapes(plan)
+    got = run_plan(torch, plan, g.values(), shapes)
+    want = g.out if mode == "fused" else g.call
+    S = scale_bound(co, g.seq, g.m, g.n, g.values())
+    for name in want:
+        check_output(g.seq, name, got[name], want[name], S[name])
+
+
+def rand_inputs(seq, m, n, seed):
+    rng = np.random.default_rng(seed)
+    U = lambda *s: rng.uniform(-1, 1, s).astype(np.float32)
+    S = seq.upper()
+    sc = {"alpha": float(np.float32(0.25 + 0.5 * rng.random())),
+          "beta": float(np.float32(0.25 + 0.5 * rng.random()))}
+    if S == "BICGK":
+        return {"A": U(m, n), "p": U(n), "r": U(m)}
+    if S == "ATAX":
+        return {"A": U(m, n), "x": U(n)}
+    if S == "GEMVER":
+        return {"A": U(m, n), "u1": U(m), "v1": U(n), "u2": U(m), "v2": U(n), "y": U(m),
+                "z": U(n), **sc}
+    if S == "GESUMMV":
+        return {"A": U(m, n), "B": U(m, n), "x": U(n), **sc}
+    if S == "AXPYDOT":
+        return {"w": U(n), "v": U(n), "u": U(n), "alpha": sc["alpha"]}
+    if S == "VADD":
+        return {"w": U(n), "y": U(n), "z": U(n)}
+    if S == "WAXPBY":
+        return {"x": U(n), "y": U(n), **sc}
+    raise KeyError(seq)
+
+
+@pytest.mark.parametrize("seq,m,n", [
+    ("BICGK", 1024, 2048), ("BICGK", 2048, 1024), ("BICGK", 4096, 4096), ("BICGK", 96, 20000),
+    ("ATAX", 1536, 1024), ("GEMVER", 1024, 1536), ("GESUMMV", 1024, 1024),
+    ("GESUMMV", 512, 12288), ("AXPYDOT", 1, 1 << 20), ("VADD", 1, 1 << 20),
+    ("WAXPBY", 1, (1 << 20) + 32), ("AXPYDOT", 1, 32),
+])
+@pytest.mark.parametrize("mode", ["fused", "unfused"])
+def test_random_vs_oracle(env, seq, m, n, mode):
+    torch, mf, co = env
+    vals = rand_inputs(seq, m, n, 1234 + m + n)
+    plan = mf.Plan.sequence(seq, m, n, mode)
+    got = run_plan(torch, plan, vals, out_shapes(plan))
+    want = co.execute(seq, m, n, vals)
+    S = scale_bound(co, seq, m, n, vals)
+    for name in want:
+        # the unfused chain rounds at call boundaries: maps downstream of a
+        # reduction are tolerance-checked, first-call maps stay exact
+        exact = None if mode == "fused" else (None if seq.upper() != "GEMVER" else name == "B")
+        if mode == "unfused" and seq.upper() in ("WAXPBY", "VADD"):
+            exact = False
+        check_output(seq, name, got[name], want[name], S[name], exact=exact)
+
+
+@pytest.mark.parametrize("f64acc", [0, 1])
+@pytest.mark.parametrize("k", [2, 4])
+def test_tuning_variants(env, k, f64acc):
+    torch, mf, co = env
+    mf.set_option("matrix_k", k)
+    mf.set_option("f64acc", f64acc)
+    try:
+        for seq, m, n in [("BICGK", 1024, 3072), ("GEMVER", 512, 4096), ("GESUMMV", 256, 8192),
+                          ("ATAX", 768, 640)]:
+            vals = rand_inputs(seq, m, n, 7)
+            plan = mf.Plan.sequence(seq, m, n, "fused")
+            got = run_plan(torch, plan, vals, out_shapes(plan))
+            want = co.execute(seq, m, n, vals)
+            S = scale_bound(co, seq, m, n, vals)
+            for name in want:
+                check_output(seq, name, got[name], want[name], S[name])
+    finally:
+        mf.set_option("matrix_k", 2)
+        mf.set_option("f64acc", 0)
+
+
+def test_deterministic(env):
+    torch, mf, co = env
+    vals = rand_inputs("BICGK", 2048, 4096, 3)
+    plan = mf.Plan.sequence("BICGK", 2048, 4096, "fused")
+    a = run_plan(torch, plan, vals, out_shapes(plan))
+    b = run_plan(torch, plan, vals, out_shapes(plan))
+    for k in a:
+        assert np.array_equal(a[k], b[k])
+    vals = rand_inputs("AXPYDOT", 1, 1 << 18, 3)
+    plan = mf.Plan.sequence("AXPYDOT", 1, 1 << 18, "fused")
+    a = run_plan(torch, plan, vals, out_shapes(plan))
+    b = run_plan(torch, plan, vals, out_shapes(plan))
+    assert np.array_equal(a["r"], b["r"])
+
+
+def test_faults(env):
+    torch, mf, co = env
+    plan = mf.Plan.sequence("BICGK", 64, 64, "fused")
+    A = torch.zeros(64, 64, device="cuda")
+    p = torch.zeros(64, device="cuda")
+    with pytest.raises(mf.VmFault, match="unbound buffer 'r'"):
+        plan.launch({"A": A, "p": p, "q": torch.zeros(64, device="cuda"),
+                     "s": torch.zeros(64, device="cuda")})
+    with pytest.raises(mf.VmFault, match="expected 64"):
+        plan.launch({"A": A, "p": torch.zeros(32, device="cuda"), "r": p,
+                     "q": torch.zeros(64, device="cuda"), "s": torch.zeros(64, device="cuda")})
+    plan = mf.Plan.sequence("WAXPBY", 1, 64, "fused")
+    with pytest.raises(mf.VmFault, match="unbound scalar"):
+        plan.launch({"x": p, "y": p, "w": torch.zeros(64, device="cuda")}, {"alpha": 1.0})
+
+
+def test_generator_matches_host(env):
+    torch, mf, co = env
+    t = torch.empty(37, 96, device="cuda")
+    mf.generate(t, seed=5, row0=11, ncols_global=96)
+    want = co.hash_fill(5, 11 * 96, 37 * 96).reshape(37, 96)
+    assert np.array_equal(t.cpu().numpy(), want)
+
+
+def test_host_launch_matches_device(env):
+    torch, mf, co = env
+    vals = rand_inputs("GEMVER", 256, 384, 9)
+    plan = mf.Plan.sequence("GEMVER", 256, 384, "fused")
+    host = {k: v for k, v in vals.items() if isinstance(v, np.ndarray)}
+    outs = {"B": np.zeros((256, 384), np.float32), "x": np.zeros(384, np.float32),
+            "w": np.zeros(256, np.float32)}
+    host.update(outs)
+    st = plan.launch_host(host, {"alpha": vals["alpha"], "beta": vals["beta"]})
+    assert st["ms"] > 0 and st["kernels"] == 3
+    dev = run_plan(torch, plan, vals, out_shapes(plan))
+    for k in outs:
+        assert np.array_equal(outs[k], dev[k])

@@ -252,6 +252,8 @@ int mf_set_option(const char* key, int value) {
       options().matrix_k = value;
     } else if (k == "f64acc") {
       options().f64acc = value ? 1 : 0;
+    } else if (k == "tma") {
+      options().tma = value < 0 ? -1 : (value ? 1 : 0);
     } else if (k == "occupancy") {
       if (value < 1 || value > 8) throw Invalid("occupancy must be 1..8");
       options().occupancy = value;
@@ -266,6 +268,7 @@ int mf_get_option(const char* key) {
   if (k == "matrix_k") return options().matrix_k;
   if (k == "f64acc") return options().f64acc;
   if (k == "occupancy") return options().occupancy;
+  if (k == "tma") return options().tma;
   return -1;
 }
 

@@ -21,6 +21,7 @@ EngineOptions& options() {
     if (const char* v = std::getenv("MF_MATRIX_K")) e.matrix_k = std::atoi(v);
     if (const char* v = std::getenv("MF_F64ACC")) e.f64acc = std::atoi(v);
     if (const char* v = std::getenv("MF_OCCUPANCY")) e.occupancy = std::atoi(v);
+    if (const char* v = std::getenv("MF_TMA")) e.tma = std::atoi(v);
     return e;
   }();
   return o;
@@ -213,9 +214,22 @@ void run_matrix(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc, 
   t.K = eo.matrix_k == 4 ? 4 : 2;
   t.f64acc = eo.f64acc != 0;
   t.occupancy = std::max(1, eo.occupancy);
+  // Variant choice (the implementation generator's role):
+  // shapes that stream a matrix back out (ger2's B) or carry the rank-2
+  // update need the deep TMA ring to keep enough bytes in flight; read-only
+  // reduction shapes reach roofline from registers alone (measured on B200,
+  // profiles/r01_variants.txt).  tma = -1 auto, 0 register-fed, 1 TMA.
+  const bool heavy = sh.nrank > 0 || sh.store;
+  t.tma = eo.tma < 0 ? heavy : eo.tma != 0;
+  if (t.tma && eo.tma < 0 && eo.matrix_k == 2) t.K = 4;
+  if (t.tma && !tma_supported(sh, t)) t.tma = false;
   int grid = 0;
-  check_cuda(matrix_config(sh, t, m, n, device_sm_count(), &a, &grid),
-             ("configure " + k.name).c_str());
+  if (t.tma)
+    check_cuda(matrix_tma_config(sh, t, m, n, device_sm_count(), &a, &grid),
+               ("configure " + k.name).c_str());
+  else
+    check_cuda(matrix_config(sh, t, m, n, device_sm_count(), &a, &grid),
+               ("configure " + k.name).c_str());
   const size_t acc = matrix_acc_bytes(t);
   const size_t colb = acc * (size_t)sh.ncol * (size_t)a.RB * (size_t)n;
   const size_t rowb = (a.CB > 1) ? acc * (size_t)sh.nrow * (size_t)a.CB * (size_t)m : 0;
@@ -223,7 +237,8 @@ void run_matrix(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc, 
   a.colpart = base;
   a.rowpart = base + ((colb + 255) & ~size_t(255));
   a.bar = ws.counters(s);
-  check_cuda(launch_matrix(sh, t, a, grid, s), ("launch " + k.name).c_str());
+  if (t.tma) check_cuda(launch_matrix_tma(sh, t, a, grid, s), ("launch " + k.name).c_str());
+  else check_cuda(launch_matrix(sh, t, a, grid, s), ("launch " + k.name).c_str());
 }
 
 }  // namespace

@@ -35,6 +35,7 @@ struct EngineOptions {
   int matrix_k = 2;
   int f64acc = 0;
   int occupancy = 2;
+  int tma = -1;  // matrix kernels: -1 auto (by shape), 1 = TMA ring, 0 = register-fed
 };
 EngineOptions& options();
 

@@ -18,6 +18,7 @@
 //     slice -- no float atomics, results are run-to-run reproducible
 //     (the reference's VM is deterministic too, proj/include/mapfuse/vm.hpp:15).
 #include "mf_kernels.cuh"
+#include "mf_device.cuh"
 
 #include <algorithm>
 #include <cstdio>
@@ -25,62 +26,10 @@
 namespace mapfuse::b200 {
 namespace {
 
+using namespace dev;
+
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-
-// Streaming 128-bit load: bypass L1 allocation and mark the L2 line
-// evict-first -- matrix and stream operands are touched exactly once.
-__device__ __forceinline__ unsigned long long evict_first_policy() {
-  unsigned long long p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-
-__device__ __forceinline__ float4 ld_stream(const float4* p) {
-  float4 v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-               : "l"(p), "l"(evict_first_policy()));
-  return v;
-}
-
-__device__ __forceinline__ void st_stream(float4* p, float4 v) {
-  asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x),
-               "f"(v.y), "f"(v.z), "f"(v.w)
-               : "memory");
-}
-
-__device__ __forceinline__ float comp(const float4& v, int c) {
-  return c == 0 ? v.x : (c == 1 ? v.y : (c == 2 ? v.z : v.w));
-}
-__device__ __forceinline__ void set_comp(float4& v, int c, float x) {
-  if (c == 0) v.x = x;
-  else if (c == 1) v.y = x;
-  else if (c == 2) v.z = x;
-  else v.w = x;
-}
-
-// ---------------------------------------------------------------------------
-// Grid barrier for co-resident (cooperatively launched) grids.  bar[0] counts
-// arrivals, bar[1] is a generation number; self-resetting across launches.
-__device__ __forceinline__ void grid_barrier(unsigned* bar) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    volatile unsigned* gen = bar + 1;
-    unsigned g = *gen;
-    __threadfence();
-    unsigned arrived = atomicAdd(bar, 1u);
-    if (arrived == gridDim.x - 1) {
-      atomicExch(bar, 0u);
-      __threadfence();
-      atomicAdd(bar + 1, 1u);
-    } else {
-      while (*gen == g) __nanosleep(64);
-    }
-    __threadfence();
-  }
-  __syncthreads();
-}
 
 // ---------------------------------------------------------------------------
 // Depth-1 stream kernel.
@@ -184,42 +133,6 @@ __global__ void __launch_bounds__(kThreads) stream_kernel(StreamArgs a) {
 // Rows stream through in batches of R: all R*K (x NMAT) 128-bit loads of a
 // batch are issued before any arithmetic.
 
-// Butterfly reduce-scatter: NV values per lane (NV power of two <= 32) ->
-// lane l ends up holding the warp total of value index (l >> (5 - log2 NV)).
-template <typename T, int NV>
-__device__ __forceinline__ T butterfly(T (&v)[NV], int lane) {
-  static_assert((NV & (NV - 1)) == 0 && NV <= 32, "NV must be a power of two <= 32");
-  int width = NV;
-  int mask = 16;
-#pragma unroll
-  for (int step = 0; (NV >> step) > 1; ++step) {
-    const int half = (NV >> step) >> 1;
-    const bool hi = (lane & mask) != 0;
-#pragma unroll
-    for (int j = 0; j < half; ++j) {
-      T send = hi ? v[j] : v[j + half];
-      T keep = hi ? v[j + half] : v[j];
-      v[j] = keep + __shfl_xor_sync(0xffffffffu, send, mask);
-    }
-    mask >>= 1;
-    width >>= 1;
-  }
-  T r = v[0];
-  for (; mask > 0; mask >>= 1) r += __shfl_xor_sync(0xffffffffu, r, mask);
-  return r;
-}
-
-template <typename ACC>
-__device__ __forceinline__ ACC fmacc(ACC a, ACC b, ACC c);
-template <>
-__device__ __forceinline__ float fmacc<float>(float a, float b, float c) {
-  return fmaf(a, b, c);
-}
-template <>
-__device__ __forceinline__ double fmacc<double>(double a, double b, double c) {
-  return fma(a, b, c);
-}
-
 template <int NMAT, int NRANK, bool STORE, int NROW, int NCOL, int K, int R, typename ACC>
 __global__ void __launch_bounds__(kThreads, 2) matrix_kernel(MatrixArgs a) {
   constexpr int NV = (NROW > 0 ? NROW : 1) * R;
@@ -242,15 +155,18 @@ __global__ void __launch_bounds__(kThreads, 2) matrix_kernel(MatrixArgs a) {
     }
     const float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
     float4 xs[NROW > 0 ? NROW : 1][K];
-    float4 vs[NRANK > 0 ? NRANK : 1][K];
+    double vd[NRANK > 0 ? NRANK : 1][K][4];  // rank vectors, widened once per tile
 #pragma unroll
     for (int k = 0; k < K; ++k) {
 #pragma unroll
       for (int o = 0; o < NROW; ++o)
         xs[o][k] = ok[k] ? __ldg(reinterpret_cast<const float4*>(a.xr[o] + col[k])) : zero4;
 #pragma unroll
-      for (int q = 0; q < NRANK; ++q)
-        vs[q][k] = ok[k] ? __ldg(reinterpret_cast<const float4*>(a.v[q] + col[k])) : zero4;
+      for (int q = 0; q < NRANK; ++q) {
+        const float4 v4 = ok[k] ? __ldg(reinterpret_cast<const float4*>(a.v[q] + col[k])) : zero4;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) vd[q][k][e] = (double)comp(v4, e);
+      }
     }
     ACC cacc[NCOL > 0 ? NCOL : 1][K][4];
 #pragma unroll
@@ -261,7 +177,7 @@ __global__ void __launch_bounds__(kThreads, 2) matrix_kernel(MatrixArgs a) {
         for (int e = 0; e < 4; ++e) cacc[c][k][e] = ACC(0);
 
     for (long long i0 = r0; i0 < r1; i0 += R) {
-      float us[NRANK > 0 ? NRANK : 1][R];
+      double us[NRANK > 0 ? NRANK : 1][R];
       float xcs[NCOL > 0 ? NCOL : 1][R];
       float4 av[R][NMAT][K];
 #pragma unroll
@@ -269,7 +185,7 @@ __global__ void __launch_bounds__(kThreads, 2) matrix_kernel(MatrixArgs a) {
         const long long i = i0 + rr;
         const bool rv = i < r1;
 #pragma unroll
-        for (int q = 0; q < NRANK; ++q) us[q][rr] = rv ? __ldg(a.u[q] + i) : 0.f;
+        for (int q = 0; q < NRANK; ++q) us[q][rr] = rv ? (double)__ldg(a.u[q] + i) : 0.0;
 #pragma unroll
         for (int c = 0; c < NCOL; ++c) xcs[c][rr] = rv ? __ldg(a.xc[c] + i) : 0.f;
 #pragma unroll
@@ -296,12 +212,15 @@ __global__ void __launch_bounds__(kThreads, 2) matrix_kernel(MatrixArgs a) {
             if constexpr (NRANK > 0) {
               // ger2 in fp64, rounded once: bit-identical to the reference's
               // B = A + u1 v1^T + u2 v2^T (blas.cpp:230-233)
+              // u*v is exact in fp64, so fma(u, v, d) == d + u*v rounded once:
+              // the same two fp64 roundings as the reference's expression.
               double d = (double)comp(av[rr][0][k], e);
 #pragma unroll
-              for (int q = 0; q < NRANK; ++q)
-                d = __dadd_rn(d, __dmul_rn((double)us[q][rr], (double)comp(vs[q][k], e)));
-              if constexpr (STORE) set_comp(st, e, (float)d);
-              ev[0] = (ACC)d;
+              for (int q = 0; q < NRANK; ++q) d = fma(us[q][rr], vd[q][k][e], d);
+              const float df = (float)d;
+              if constexpr (STORE) set_comp(st, e, df);
+              if constexpr (sizeof(ACC) == 4) ev[0] = df;
+              else ev[0] = (ACC)d;
             }
 #pragma unroll
             for (int o = 0; o < NROW; ++o) {
@@ -355,44 +274,7 @@ __global__ void __launch_bounds__(kThreads, 2) matrix_kernel(MatrixArgs a) {
     const bool need_rows = (NROW > 0) && a.CB > 1;
     if (NCOL == 0 && !need_rows) return;
     grid_barrier(a.bar);
-    const long long n4 = a.n / 4, m4 = a.m / 4;
-    const long long col_slots = (long long)NCOL * n4;
-    const long long total = col_slots + (need_rows ? (long long)NROW * m4 : 0);
-    for (long long s = (long long)blockIdx.x * kThreads + tid; s < total;
-         s += (long long)gridDim.x * kThreads) {
-      if (s < col_slots) {
-        const int c = (int)(s / n4);
-        const long long j = (s % n4) * 4;
-        ACC t[4] = {ACC(0), ACC(0), ACC(0), ACC(0)};
-        for (int b = 0; b < a.RB; ++b) {
-          const ACC* p = colpart + ((long long)c * a.RB + b) * a.n + j;
-#pragma unroll
-          for (int e = 0; e < 4; ++e) t[e] += __ldcg(p + e);
-        }
-        float4 o;
-        o.x = (float)(a.ac[c] * (double)t[0]);
-        o.y = (float)(a.ac[c] * (double)t[1]);
-        o.z = (float)(a.ac[c] * (double)t[2]);
-        o.w = (float)(a.ac[c] * (double)t[3]);
-        *reinterpret_cast<float4*>(a.yc[c] + j) = o;
-      } else {
-        const long long q = s - col_slots;
-        const int o = (int)(q / m4);
-        const long long i = (q % m4) * 4;
-        ACC t[4] = {ACC(0), ACC(0), ACC(0), ACC(0)};
-        for (int b = 0; b < a.CB; ++b) {
-          const ACC* p = rowpart + ((long long)o * a.CB + b) * a.m + i;
-#pragma unroll
-          for (int e = 0; e < 4; ++e) t[e] += __ldcg(p + e);
-        }
-        float4 r;
-        r.x = (float)(a.ar[o] * (double)t[0]);
-        r.y = (float)(a.ar[o] * (double)t[1]);
-        r.z = (float)(a.ar[o] * (double)t[2]);
-        r.w = (float)(a.ar[o] * (double)t[3]);
-        *reinterpret_cast<float4*>(a.yr[o] + i) = r;
-      }
-    }
+    finalize<NROW, NCOL, ACC>(a, tid, kThreads);
   }
 }
 

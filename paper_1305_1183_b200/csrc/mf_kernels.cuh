@@ -57,7 +57,8 @@ struct MatrixTuning {
   int K = 2;           // float4 column slots per thread (chunk width 1024*K columns)
   int R = 8;           // rows per reduction batch
   bool f64acc = false; // accumulate reductions in fp64
-  int occupancy = 2;   // CTAs per SM targeted
+  int occupancy = 2;   // CTAs per SM targeted (register-fed variant)
+  bool tma = true;     // TMA/mbarrier shared-memory ring (mf_matrix_tma.cu)
 };
 
 // Launchers; return cudaSuccess or the launch error.  `sms` = SM count.
@@ -71,6 +72,14 @@ cudaError_t matrix_config(const MatrixShape& sh, const MatrixTuning& t, long lon
 cudaError_t launch_matrix(const MatrixShape& sh, const MatrixTuning& t, const MatrixArgs& a,
                           int grid, cudaStream_t s);
 bool matrix_shape_supported(const MatrixShape& sh);
+
+// TMA-fed variant (mf_matrix_tma.cu).
+cudaError_t matrix_tma_config(const MatrixShape& sh, const MatrixTuning& t, long long m,
+                              long long n, int sms, MatrixArgs* a, int* grid);
+cudaError_t launch_matrix_tma(const MatrixShape& sh, const MatrixTuning& t, const MatrixArgs& a,
+                              int grid, cudaStream_t s);
+int tma_stages(const MatrixShape& sh, const MatrixTuning& t);
+bool tma_supported(const MatrixShape& sh, const MatrixTuning& t);  // fits a >= 2-stage ring
 size_t matrix_acc_bytes(const MatrixTuning& t);
 
 // Counter-based synthetic data (identical to oracle/mf_oracle.c

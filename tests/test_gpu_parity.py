@@ -106,12 +106,14 @@ def test_random_vs_oracle(env, seq, m, n, mode):
         check_output(seq, name, got[name], want[name], S[name], exact=exact)
 
 
+@pytest.mark.parametrize("tma", [-1, 0, 1])
 @pytest.mark.parametrize("f64acc", [0, 1])
 @pytest.mark.parametrize("k", [2, 4])
-def test_tuning_variants(env, k, f64acc):
+def test_tuning_variants(env, k, f64acc, tma):
     torch, mf, co = env
     mf.set_option("matrix_k", k)
     mf.set_option("f64acc", f64acc)
+    mf.set_option("tma", tma)
     try:
         for seq, m, n in [("BICGK", 1024, 3072), ("GEMVER", 512, 4096), ("GESUMMV", 256, 8192),
                           ("ATAX", 768, 640)]:
@@ -125,6 +127,7 @@ def test_tuning_variants(env, k, f64acc):
     finally:
         mf.set_option("matrix_k", 2)
         mf.set_option("f64acc", 0)
+        mf.set_option("tma", -1)
 
 
 def test_deterministic(env):

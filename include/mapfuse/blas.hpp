@@ -49,6 +49,8 @@ Problem make_problem(const script::Script& s, int rows, int cols, uint32_t seed)
 // cols, depth-1 calls share lengths).  The reference's first-use rule
 // (blas.cpp:75-103) mis-sizes SGEMV / GESUMMV / SGEMVT vectors for
 // rectangular problems; for square problems both agree.
+// 'r' row-indexed vector, 'c' column-indexed vector, 't' tile, 's' scalar.
+std::map<std::string, char> vector_roles(const script::Script& s, const lib::Library& lib);
 std::map<std::string, std::pair<int, int>> infer_shapes(const script::Script& s,
                                                         const lib::Library& lib, int rows,
                                                         int cols);

@@ -1,0 +1,133 @@
+// mapfuse/planner.hpp -- the optimizer: fusion planner, code generator,
+// B200 cost model, combination selector and the compile pipeline.
+//
+// The reference declares these modules in its build (proj/CMakeLists.txt:40-48:
+// planner.cpp, implgen.cpp, costmodel.cpp, selector.cpp, codegen.cpp,
+// pipeline.cpp) but ships none of their sources; their contract is SPEC.md
+// :181-533.  This is a new implementation of that contract, retargeted to
+// B200: every kernel the selector chooses is lowered onto a hand-written
+// sm_100a kernel family, and the cost model predicts HBM time from
+// algorithmic bytes and measured per-family efficiency.
+#pragma once
+
+#include <cstdint>
+#include <map>
+#include <optional>
+#include <string>
+#include <vector>
+
+#include "mapfuse/device.hpp"
+#include "mapfuse/kernel.hpp"
+#include "mapfuse/library.hpp"
+#include "mapfuse/script.hpp"
+#include "mf_native.hpp"
+
+namespace mapfuse::plan {
+
+struct Sizes {
+  int64_t rows = 0, cols = 0;  // padded problem size
+};
+
+// ---------------------------------------------------------------- planner
+struct Fusion {
+  std::vector<int> calls;              // sorted call ids (size >= 2)
+  std::vector<script::Edge> internal;  // dataflow kept on chip
+  std::vector<std::string> shared;     // read-only inputs read by several members
+  int64_t saved_words = 0;
+};
+
+// Rule ids: nesting-mismatch | global-barrier-required |
+// no-savings | block-capacity.  A non-convex set (a path leaves the set and
+// re-enters it) also needs a global barrier and reports that rule.
+struct ConstraintViolation {
+  std::string rule;
+  std::vector<int> nodes;
+  std::string explanation;
+};
+
+std::optional<ConstraintViolation> fusibility(const std::vector<int>& nodes,
+                                              const script::Script& s,
+                                              const script::DataDependencyGraph& g,
+                                              const lib::Library& L);
+inline bool is_fusible(const std::vector<int>& nodes, const script::Script& s,
+                       const script::DataDependencyGraph& g, const lib::Library& L) {
+  return !fusibility(nodes, s, g, L).has_value();
+}
+
+// Words each script name occupies at the padded size (tiles m*n, vectors m
+// or n by role, scalars 1).
+std::map<std::string, int64_t> element_words(const script::Script& s, const lib::Library& L,
+                                             Sizes sz);
+
+// (words moved by the members unfused) - (words moved fused).
+int64_t transfer_savings(const Fusion& f, const script::Script& s,
+                         const script::DataDependencyGraph& g, const lib::Library& L, Sizes sz);
+
+// All connected (edges + shared inputs), fusible subsets of size 2..max_size
+// with positive savings, sorted by call ids.
+std::vector<Fusion> enumerate_fusions(const script::Script& s, const script::DataDependencyGraph& g,
+                                      const lib::Library& L, Sizes sz, int max_size = 6);
+
+// ---------------------------------------------------------------- codegen
+struct CodegenParams {
+  int by = 8;          // block rows for depth-2 kernels (BY macro)
+  int instances = 4;   // instances per block for depth-1 kernels (IPB)
+  int iterations = 1;  // serial iterations (ITERS)
+  bool barriers = true;  // test hook: suppress barrier insertion
+};
+
+// Algorithm 1 / 2 kernel for a set of calls (one call = unfused kernel).
+kernel::KernelIR generate_kernel(const std::vector<int>& calls, const script::Script& s,
+                                 const script::DataDependencyGraph& g, const lib::Library& L,
+                                 const CodegenParams& p = {});
+
+// ---------------------------------------------------------------- lowering
+// KernelIR -> the sm_100a kernel family and its operand roles.  Throws
+// std::invalid_argument when no hand-written template covers the kernel.
+b200::NativeKernel lower_kernel(const kernel::KernelIR& k);
+bool stream_template_exists(int nin, int nout, bool dot);
+bool matrix_template_exists(int nmat, int nrank, int store, int nrow, int ncol);
+
+// ---------------------------------------------------------------- cost model
+// t = max(bytes / (eta * BW), flops / F) + launch.  eta per kernel family
+// and variant comes from the benchmark table (measured on B200; overridable
+// with MF_COST_DB=<file of "key eta" lines>).
+struct CostModel {
+  vm::B200Device dev;
+  std::map<std::string, double> eta;
+
+  static CostModel defaults();
+  // Picks the best variant for the kernel, stores it in k.variant, returns us.
+  double predict_us(b200::NativeKernel& k, int64_t m, int64_t n) const;
+};
+
+// ---------------------------------------------------------------- selector
+struct Item {
+  std::vector<int> calls;
+  kernel::KernelIR kir;
+  b200::NativeKernel native;
+  double predicted_us = 0;
+};
+
+struct Combination {
+  std::vector<Item> kernels;  // launch order (topological over the condensed DAG)
+  double predicted_us = 0;
+};
+
+// k best exact covers of the script's calls by lowerable fusions and single
+// calls, ascending predicted time (ties: fewer kernels, then call ids).
+std::vector<Combination> enumerate_combinations(const script::Script& s,
+                                                const script::DataDependencyGraph& g,
+                                                const lib::Library& L, Sizes sz,
+                                                const CostModel& cm, int k,
+                                                bool allow_fusion = true);
+uint64_t count_combinations(const script::Script& s, const script::DataDependencyGraph& g,
+                            const lib::Library& L, Sizes sz);
+
+// ---------------------------------------------------------------- pipeline
+// parse -> graph -> validate -> plan -> select -> codegen -> lower.
+// mode: 0 fused (planner's choice), 1 unfused (one kernel per call).
+b200::NativePlan compile(const std::string& script_text, const lib::Library& L, int rows, int cols,
+                         int mode);
+
+}  // namespace mapfuse::plan

@@ -61,8 +61,7 @@ const std::vector<float>& Problem::buffer(const std::string& name) const {
   return it->second;
 }
 
-std::map<std::string, std::pair<int, int>> infer_shapes(const script::Script& s,
-                                                        const lib::Library& L, int rows, int cols) {
+std::map<std::string, char> vector_roles(const script::Script& s, const lib::Library& L) {
   // union-find over vector names tied together by depth-1 calls
   std::map<std::string, std::string> parent;
   std::function<std::string(const std::string&)> root = [&](const std::string& x) {
@@ -71,50 +70,53 @@ std::map<std::string, std::pair<int, int>> infer_shapes(const script::Script& s,
     return it->second = root(it->second);
   };
   auto unite = [&](const std::string& a, const std::string& b) { parent[root(a)] = root(b); };
-  std::map<std::string, int> len;  // root -> rows / cols
   for (const auto& [n, spec] : s.declarations) parent[n] = n;
+  auto bound = [&](const script::CallStatement& c, const lib::ElementaryFunction* f) {
+    std::vector<std::pair<std::string, const lib::ElementDecl*>> v;
+    for (size_t i = 0; i < c.arguments.size() && i < f->args.size(); ++i)
+      if (!f->args[i].is_scalar) v.push_back({c.arguments[i], f->element(f->args[i].name)});
+    for (size_t i = 0; i < c.results.size() && i < f->results.size(); ++i)
+      v.push_back({c.results[i], f->element(f->results[i])});
+    return v;
+  };
   for (const auto& c : s.calls) {
     const lib::ElementaryFunction* f = L.find(c.function);
-    if (!f) continue;
-    std::vector<std::pair<std::string, const lib::ElementDecl*>> bound;
-    size_t ai = 0;
-    for (size_t i = 0; i < c.arguments.size() && i < f->args.size(); ++i) {
-      if (f->args[i].is_scalar) continue;
-      bound.push_back({c.arguments[i], f->element(f->args[i].name)});
-      ++ai;
-    }
-    for (size_t i = 0; i < c.results.size() && i < f->results.size(); ++i)
-      bound.push_back({c.results[i], f->element(f->results[i])});
-    if (f->depth == 1) {
-      std::string first;
-      for (const auto& [n, d] : bound)
-        if (d && d->kind == lib::ElemKind::Subvector32) {
-          if (first.empty()) first = n;
-          else unite(n, first);
-        }
-    }
+    if (!f || f->depth != 1) continue;
+    std::string first;
+    for (const auto& [n, d] : bound(c, f))
+      if (d && d->kind == lib::ElemKind::Subvector32) {
+        if (first.empty()) first = n;
+        else unite(n, first);
+      }
   }
+  std::map<std::string, char> rootrole;
   for (const auto& c : s.calls) {
     const lib::ElementaryFunction* f = L.find(c.function);
     if (!f || f->depth != 2) continue;
-    auto fix = [&](const std::string& n, const lib::ElementDecl* d) {
-      if (!d || d->kind != lib::ElemKind::Subvector32) return;
-      len.emplace(root(n), d->varies.y ? rows : cols);
-    };
-    for (size_t i = 0; i < c.arguments.size() && i < f->args.size(); ++i)
-      if (!f->args[i].is_scalar) fix(c.arguments[i], f->element(f->args[i].name));
-    for (size_t i = 0; i < c.results.size() && i < f->results.size(); ++i)
-      fix(c.results[i], f->element(f->results[i]));
+    for (const auto& [n, d] : bound(c, f))
+      if (d && d->kind == lib::ElemKind::Subvector32) rootrole.emplace(root(n), d->varies.y ? 'r' : 'c');
   }
-  std::map<std::string, std::pair<int, int>> dims;
+  std::map<std::string, char> roles;
   for (const auto& [n, spec] : s.declarations) {
-    switch (spec.kind) {
-      case lib::ElemKind::Tile32x32: dims[n] = {rows, cols}; break;
-      case lib::ElemKind::Scalar: dims[n] = {1, 1}; break;
-      default: {
-        auto it = len.find(root(n));
-        dims[n] = {1, it == len.end() ? cols : it->second};
-      }
+    if (spec.kind == lib::ElemKind::Tile32x32) roles[n] = 't';
+    else if (spec.kind == lib::ElemKind::Scalar) roles[n] = 's';
+    else {
+      auto it = rootrole.find(root(n));
+      roles[n] = it == rootrole.end() ? 'c' : it->second;
+    }
+  }
+  return roles;
+}
+
+std::map<std::string, std::pair<int, int>> infer_shapes(const script::Script& s,
+                                                        const lib::Library& L, int rows, int cols) {
+  std::map<std::string, std::pair<int, int>> dims;
+  for (const auto& [n, role] : vector_roles(s, L)) {
+    switch (role) {
+      case 't': dims[n] = {rows, cols}; break;
+      case 's': dims[n] = {1, 1}; break;
+      case 'r': dims[n] = {1, rows}; break;
+      default: dims[n] = {1, cols};
     }
   }
   return dims;

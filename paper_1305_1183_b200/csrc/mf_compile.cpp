@@ -1,24 +1,98 @@
-// mf_compile.cpp -- TEMPORARY: routes to the hand-derived plans until the
-// planner / codegen / lowering stack lands.
+// mf_compile.cpp -- script / KernelIR text -> NativePlan (C-ABI side).
 #include "mf_compile.hpp"
 
 #include <stdexcept>
 
+#include "mapfuse/blas.hpp"
+#include "mapfuse/kernel.hpp"
+#include "mapfuse/planner.hpp"
 #include "mapfuse_b200.h"
-#include "mf_builtin.hpp"
 #include "mf_exec.hpp"
 
 namespace mapfuse::b200 {
 
-NativePlan compile_script(const std::string&, const std::string&, int, int, int) {
-  throw Invalid("mf_compile: planner not built yet");
+namespace {
+template <typename F>
+NativePlan as_invalid(F&& f) {
+  try {
+    return f();
+  } catch (const Fault&) {
+    throw;
+  } catch (const Invalid&) {
+    throw;
+  } catch (const std::exception& e) {  // parse / validation / planning errors
+    throw Invalid(e.what());
+  }
 }
+}  // namespace
+
+NativePlan compile_script(const std::string& script_text, const std::string& manifest, int rows,
+                          int cols, int mode) {
+  return as_invalid([&] {
+    if (mode != MF_MODE_FUSED && mode != MF_MODE_UNFUSED) throw Invalid("unknown planner mode");
+    if (manifest.empty()) return plan::compile(script_text, blas::default_library(), rows, cols, mode);
+    const lib::Library L = lib::load_library(manifest);
+    return plan::compile(script_text, L, rows, cols, mode);
+  });
+}
+
 NativePlan compile_sequence(const std::string& sequence, int rows, int cols, int mode) {
-  return builtin_plan(sequence, rows, cols, mode == MF_MODE_FUSED);
+  return as_invalid([&] {
+    const blas::SequenceCase c = blas::build_sequence(sequence);
+    NativePlan p = compile_script(c.script_text, std::string(), rows, cols, mode);
+    p.sequence = c.name;
+    return p;
+  });
 }
-NativePlan plan_from_kernel_text(const std::string&, int, int) {
-  throw Invalid("mf_plan_create: lowering not built yet");
+
+NativePlan plan_from_kernel_text(const std::string& text, int rows, int cols) {
+  return as_invalid([&] {
+    const kernel::KernelIR k = kernel::parse_kernel_text(text);
+    NativePlan p;
+    p.rows = (rows + 31) / 32 * 32;
+    p.cols = (cols + 31) / 32 * 32;
+    p.sequence = k.name;
+    NativeKernel nk = plan::lower_kernel(k);
+    nk.name = k.name;
+    plan::CostModel::defaults().predict_us(nk, p.rows, p.cols);
+    auto add = [&](const std::string& n, int r, int c, Role role, bool rowix) {
+      if (p.find(n)) return;
+      BufferSpec b;
+      b.name = n;
+      b.rows = r;
+      b.cols = c;
+      b.role = role;
+      b.row_indexed = rowix;
+      p.buffers.push_back(b);
+    };
+    if (nk.kind == NativeKernel::Kind::Matrix) {
+      const MatrixOp& op = nk.matrix;
+      for (const auto& m : op.mats) add(m, p.rows, p.cols, Role::Input, false);
+      for (const auto& [u, v] : op.rank) {
+        add(u, 1, p.rows, Role::Input, true);
+        add(v, 1, p.cols, Role::Input, false);
+      }
+      for (const auto& r : op.rows) add(r.x, 1, p.cols, Role::Input, false);
+      for (const auto& c : op.cols) add(c.x, 1, p.rows, Role::Input, true);
+      if (!op.store.empty()) add(op.store, p.rows, p.cols, Role::Output, false);
+      for (const auto& r : op.rows) add(r.y, 1, p.rows, Role::Output, true);
+      for (const auto& c : op.cols) add(c.y, 1, p.cols, Role::Output, false);
+    } else {
+      const bool tiles = k.depth == 2;
+      for (const auto& i : nk.stream.inputs) add(i, tiles ? p.rows : 1, p.cols, Role::Input, false);
+      for (const auto& o : nk.stream.outs) add(o.name, tiles ? p.rows : 1, p.cols, Role::Output, false);
+      if (nk.stream.has_dot) {
+        add(nk.stream.dot_out, 1, 1, Role::Output, false);
+        p.buffers.back().scalar = true;
+      }
+    }
+    for (const auto& b : p.buffers) (void)b;
+    p.kernels.push_back(std::move(nk));
+    p.kernel_ir.push_back(text);
+    return p;
+  });
 }
+
 int classify_exception(const std::exception&) { return MF_ERR_FAULT; }
 
 }  // namespace mapfuse::b200

@@ -220,8 +220,13 @@ void run_matrix(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc, 
   // reduction shapes reach roofline from registers alone (measured on B200,
   // profiles/r01_variants.txt).  tma = -1 auto, 0 register-fed, 1 TMA.
   const bool heavy = sh.nrank > 0 || sh.store;
-  t.tma = eo.tma < 0 ? heavy : eo.tma != 0;
-  if (t.tma && eo.tma < 0 && eo.matrix_k == 2) t.K = 4;
+  if (eo.tma < 0 && k.variant_tma >= 0) {  // the cost model's choice
+    t.tma = k.variant_tma == 1;
+    if (k.variant_k == 2 || k.variant_k == 4) t.K = k.variant_k;
+  } else {
+    t.tma = eo.tma < 0 ? heavy : eo.tma != 0;
+    if (t.tma && eo.tma < 0 && eo.matrix_k == 2) t.K = 4;
+  }
   if (t.tma && !tma_supported(sh, t)) t.tma = false;
   int grid = 0;
   if (t.tma)

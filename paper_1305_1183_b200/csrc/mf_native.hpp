@@ -74,6 +74,10 @@ struct NativeKernel {
   std::vector<int> calls;  // script call ids covered
   StreamOp stream;
   MatrixOp matrix;
+  // implementation variant chosen by the cost model (matrix kernels):
+  // tma -1 = engine default, 0 register-fed, 1 TMA ring; k = float4 slots/thread
+  int variant_tma = -1;
+  int variant_k = 0;
 
   // Algorithmic traffic: every distinct input read once, every
   // output written once.  Evaluated for a concrete m x n.

@@ -182,3 +182,44 @@ def test_host_launch_matches_device(env):
     dev = run_plan(torch, plan, vals, out_shapes(plan))
     for k in outs:
         assert np.array_equal(outs[k], dev[k])
+
+
+def test_user_manifest_function_on_gpu(env):
+    torch, mf, co = env
+    import os
+    text = open(os.path.join(os.path.dirname(__file__), "golden", "axpby3.mf")).read()
+    p = mf.Plan.compile("subvector32 a, b, c, o;\nfloat k;\ninput a, b, c, k;\n"
+                        "o = axpby3(k, a, b, c);\nreturn o;\n", 1, 4096, manifest=text)
+    rng = np.random.default_rng(5)
+    a, b, c = (rng.uniform(-1, 1, 4096).astype(np.float32) for _ in range(3))
+    k = np.float32(0.625)
+    got = run_plan(torch, p, {"a": a, "b": b, "c": c, "k": float(k)}, {"o": (4096,)})["o"]
+    want = ((np.float64(k) * a.astype(np.float64) + b) - 2.0 * c.astype(np.float64)).astype(np.float32)
+    assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("seq", ["BICGK", "GEMVER", "GESUMMV", "AXPYDOT", "VADD"])
+def test_kernel_text_boundary_on_gpu(env, seq):
+    """vm::launch boundary: each emitted KernelIR re-enters via mf_plan_create
+    and produces the same results as the compiled plan."""
+    torch, mf, co = env
+    m, n = (1, 8192) if seq in ("AXPYDOT", "VADD") else (512, 768)
+    vals = rand_inputs(seq, m, n, 21)
+    plan = mf.Plan.sequence(seq, m, n, "fused")
+    full = run_plan(torch, plan, vals, out_shapes(plan))
+    # replay kernel by kernel through the text boundary, intermediates included
+    d = plan.describe()
+    bufs = {}
+    for b in d["buffers"]:
+        shp = (b["rows"], b["cols"]) if b["rows"] > 1 else (b["cols"],)
+        v = vals.get(b["name"])
+        bufs[b["name"]] = (torch.from_numpy(np.ascontiguousarray(v, np.float32)).cuda()
+                           if isinstance(v, np.ndarray) else torch.zeros(shp, device="cuda"))
+    sc = {k: v for k, v in vals.items() if not isinstance(v, np.ndarray)}
+    for k in range(plan.num_kernels):
+        q = mf.Plan.from_kernel_text(plan.kernel_text(k), m, n)
+        names = set(q.describe()["kernels"][0]["inputs"]) | set(q.describe()["kernels"][0]["outputs"])
+        q.launch({nm: bufs[nm] for nm in names}, sc)
+    torch.cuda.synchronize()
+    for name, v in full.items():
+        assert np.array_equal(bufs[name].cpu().numpy().ravel(), v.ravel()), name

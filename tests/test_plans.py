@@ -1,0 +1,112 @@
+"""CPU tests of the compile pipeline through the C-ABI (no GPU needed).
+
+* every Table-1 sequence compiles (fused and unfused) to exactly the plan
+  SURVEY.md Appendix A derives (cross-checked against the hand-derived
+  builtin plans: same kernels, calls, fusion shapes, algorithmic bytes,
+  buffer roles);
+* each emitted KernelIR text re-enters through mf_plan_create (the
+  vm::launch boundary) and lowers to the same kernel;
+* the shared library exports every entry point include/mapfuse_b200.h declares;
+* errors map to the reference's exception classes.
+"""
+import os
+import re
+
+import pytest
+
+import paper_1305_1183_b200 as mf
+from paper_1305_1183_b200 import runtime
+
+SEQS = ["AXPYDOT", "VADD", "WAXPBY", "BICGK", "ATAX", "GEMVER", "GESUMMV", "SGEMV", "SGEMVT",
+        "SSCAL", "MADD"]
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def summary(d):
+    ks = [(tuple(k["calls"]), k["kind"], tuple(sorted(k["shape"].items())), tuple(k["inputs"]),
+           tuple(k["outputs"])) for k in d["kernels"]]
+    bufs = sorted((b["name"], b["rows"], b["cols"], b["role"]) for b in d["buffers"])
+    return ks, bufs, d["bytes_loaded"], d["bytes_stored"]
+
+
+@pytest.mark.parametrize("mode", ["fused", "unfused"])
+@pytest.mark.parametrize("seq", SEQS)
+def test_pipeline_matches_appendix_a(seq, mode):
+    m, n = (1, 4096) if seq in ("AXPYDOT", "VADD", "WAXPBY", "SSCAL") else (256, 256)
+    got = mf.Plan.sequence(seq, m, n, mode).describe()
+    want = mf.Plan.sequence(seq, m, n, "builtin_" + mode).describe()
+    gk, gb, gl, gs = summary(got)
+    wk, wb, wl, ws = summary(want)
+    assert [k[:3] for k in gk] == [k[:3] for k in wk]
+    assert (gl, gs) == (wl, ws)
+    assert [(b[0], b[3]) for b in gb] == [(b[0], b[3]) for b in wb]
+
+
+@pytest.mark.parametrize("seq", SEQS)
+def test_kernel_text_boundary_round_trip(seq):
+    p = mf.Plan.sequence(seq, 128, 128, "fused")
+    d = p.describe()
+    for k in range(p.num_kernels):
+        text = p.kernel_text(k)
+        assert text.startswith("kernel ")
+        q = mf.Plan.from_kernel_text(text, 128, 128)
+        qd = q.describe()["kernels"][0]
+        assert qd["kind"] == d["kernels"][k]["kind"]
+        assert qd["shape"] == d["kernels"][k]["shape"]
+        assert qd["inputs"] == d["kernels"][k]["inputs"]
+        assert qd["outputs"] == d["kernels"][k]["outputs"]
+
+
+def test_fusion_bytes_saved_ratios():
+    # bytes-saved ratios of the BASELINE configs
+    def ratio(seq, m, n):
+        f = mf.Plan.sequence(seq, m, n, "fused").describe()
+        u = mf.Plan.sequence(seq, m, n, "unfused").describe()
+        return (u["bytes_loaded"] + u["bytes_stored"]) / (f["bytes_loaded"] + f["bytes_stored"])
+    assert abs(ratio("AXPYDOT", 1, 1 << 24) - 1.25) < 1e-6
+    assert ratio("VADD", 1, 1 << 20) == 1.5
+    assert abs(ratio("WAXPBY", 1, 1 << 20) - 5 / 3) < 1e-9
+    assert abs(ratio("BICGK", 16384, 16384) - 2.147745792 / 1.074003968) < 1e-9
+    assert abs(ratio("GEMVER", 32768, 32768) - 17181310976 / 12886343680) < 1e-9
+    assert ratio("ATAX", 1024, 1024) == 1.0
+
+
+def test_c_abi_exports_every_declared_symbol():
+    hdr = open(os.path.join(ROOT, "include", "mapfuse_b200.h")).read()
+    declared = sorted(set(re.findall(r"\b(mf_[a-z_]+)\s*\(", hdr)))
+    assert len(declared) >= 16
+    L = mf.lib()
+    for name in declared:
+        assert hasattr(L, name), name
+    assert set(runtime.EXPORTS) <= set(declared)
+
+
+def test_errors_map_to_reference_classes():
+    with pytest.raises(mf.ParseError, match="'t'"):
+        mf.Plan.compile("subvector32 x;\ninput x;\nreturn t;\n", 1, 64)
+    with pytest.raises(mf.ParseError, match="type-mismatch"):
+        mf.Plan.compile("subvector32 A, x, y;\ninput A, x;\ny = sgemv(A, x);\nreturn y;\n", 64, 64)
+    with pytest.raises(mf.ParseError, match="kind-violation"):
+        mf.Plan.compile("subvector32 x, y;\ninput x;\ny = f(x);\nreturn y;\n", 1, 64,
+                        manifest="function f {\n kind map\n depth 1\n parallelism 32 1\n"
+                                 " max_instances 1\n arg a subvector32 varies x\n"
+                                 " out b subvector32 varies x\n routine load a {\n"
+                                 "  map a: tx = w, ty = 0\n  body {\n"
+                                 "   onchip a[tx] = global a[ex*32 + tx]\n  }\n }\n"
+                                 " routine compute {\n  map a: tx = w, ty = 0\n"
+                                 "  map b: tx = w, ty = 0\n  body {\n"
+                                 "   onchip b[tx] = global a[ex*32 + tx]\n  }\n }\n"
+                                 " routine store b {\n  map b: tx = w, ty = 0\n  body {\n"
+                                 "   global b[ex*32 + tx] = onchip b[tx]\n  }\n }\n}\n")
+    with pytest.raises(mf.ParseError):
+        mf.Plan.from_kernel_text("kernel x {\n  bogus 1\n}\n", 64, 64)
+
+
+def test_user_manifest_function_gets_a_kernel():
+    # a new elementary function written only in the routine IR (not one of the
+    # shipped ten) is understood from its compute body and lowered
+    text = open(os.path.join(ROOT, "tests", "golden", "axpby3.mf")).read()
+    p = mf.Plan.compile("subvector32 a, b, c, o;\nfloat k;\ninput a, b, c, k;\n"
+                        "o = axpby3(k, a, b, c);\nreturn o;\n", 1, 4096, manifest=text)
+    k = p.describe()["kernels"][0]
+    assert k["kind"] == "stream" and k["shape"]["inputs"] == 3

@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cmath>
 #include <set>
+#include <iomanip>
 #include <sstream>
 #include <stdexcept>
 
@@ -168,6 +169,7 @@ static std::string jstr(const std::string& s) {
 
 std::string NativePlan::describe_json() const {
   std::ostringstream os;
+  os << std::setprecision(17);
   os << "{\"sequence\":" << jstr(sequence) << ",\"rows\":" << rows << ",\"cols\":" << cols
      << ",\"bytes_loaded\":" << bytes_loaded() << ",\"bytes_stored\":" << bytes_stored()
      << ",\"kernels\":[";
@@ -187,6 +189,49 @@ std::string NativePlan::describe_json() const {
     auto co = k.column_outputs();
     for (size_t j = 0; j < co.size(); ++j) os << (j ? "," : "") << jstr(co[j]);
     os << "]";
+    auto coef = [&](const Coef& c) {
+      std::ostringstream o;
+      o << std::setprecision(17) << "[";
+      for (size_t t = 0; t < c.terms.size(); ++t) {
+        o << (t ? "," : "") << "[" << c.terms[t].c << ",[";
+        for (size_t q = 0; q < c.terms[t].syms.size(); ++q) o << (q ? "," : "") << jstr(c.terms[t].syms[q]);
+        o << "]]";
+      }
+      return o.str() + "]";
+    };
+    auto coefs = [&](const std::vector<Coef>& v) {
+      std::string o = "[";
+      for (size_t t = 0; t < v.size(); ++t) o += (t ? "," : "") + coef(v[t]);
+      return o + "]";
+    };
+    auto reds = [&](const std::vector<MatrixOp::Red>& v) {
+      std::string o = "[";
+      for (size_t t = 0; t < v.size(); ++t)
+        o += std::string(t ? "," : "") + "{\"mat\":" + std::to_string(v[t].mat) + ",\"x\":" + jstr(v[t].x) +
+             ",\"y\":" + jstr(v[t].y) + ",\"coef\":" + coef(v[t].coef) + "}";
+      return o + "]";
+    };
+    if (k.kind == NativeKernel::Kind::Matrix) {
+      const MatrixOp& m = k.matrix;
+      os << ",\"op\":{\"mats\":[";
+      for (size_t t = 0; t < m.mats.size(); ++t) os << (t ? "," : "") << jstr(m.mats[t]);
+      os << "],\"rank\":[";
+      for (size_t t = 0; t < m.rank.size(); ++t)
+        os << (t ? "," : "") << "[" << jstr(m.rank[t].first) << "," << jstr(m.rank[t].second) << "]";
+      os << "],\"store\":" << jstr(m.store) << ",\"rows\":" << reds(m.rows) << ",\"cols\":" << reds(m.cols)
+         << "},\"variant\":{\"tma\":" << k.variant_tma << ",\"k\":" << k.variant_k << "}";
+    } else {
+      const StreamOp& st = k.stream;
+      os << ",\"op\":{\"inputs\":[";
+      for (size_t t = 0; t < st.inputs.size(); ++t) os << (t ? "," : "") << jstr(st.inputs[t]);
+      os << "],\"outs\":[";
+      for (size_t t = 0; t < st.outs.size(); ++t)
+        os << (t ? "," : "") << "{\"name\":" << jstr(st.outs[t].name) << ",\"coef\":" << coefs(st.outs[t].coef) << "}";
+      os << "]";
+      if (st.has_dot)
+        os << ",\"dot\":{\"out\":" << jstr(st.dot_out) << ",\"a\":" << coefs(st.dot_a) << ",\"b\":" << coefs(st.dot_b) << "}";
+      os << "}";
+    }
     if (k.kind == NativeKernel::Kind::Matrix) {
       os << ",\"shape\":{\"mats\":" << k.matrix.mats.size() << ",\"rank\":" << k.matrix.rank.size()
          << ",\"store\":" << (k.matrix.store.empty() ? 0 : 1) << ",\"rows\":" << k.matrix.rows.size()

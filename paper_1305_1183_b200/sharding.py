@@ -1,0 +1,111 @@
+"""Row-sharded execution of a compiled plan over torch.distributed ranks
+(the reference has no multi-device path).
+
+Partition:
+  * plans with a depth-2 (matrix) kernel: every tile is split into P
+    contiguous row panels A_k (rows rounded to multiples of 32); vectors
+    indexed by rows are split the same way; vectors indexed by columns are
+    replicated on input;
+  * pure depth-1 plans: every vector is split into P contiguous slices.
+Each rank runs the SAME planner-selected kernels on its local problem.  Row
+reductions (A p) and row-local maps need no communication.  Column
+reductions (A^T r) and dot products produce per-rank partial sums: they are
+all-reduced (NCCL over NVLink on GPUs) right after the kernel that produced
+them, before any later kernel consumes them -- the plan reports exactly
+which names those are (mf_plan_kernel_column_outputs).  No other exchange
+exists in any Table-1 sequence.
+
+`executor` is injectable so the host-side orchestration can be exercised on
+CPU with the gloo backend (tests/test_sharding_gloo.py); the default
+executor launches the sm_100a kernels through the C-ABI.
+"""
+from __future__ import annotations
+
+from typing import Callable, Dict, Mapping, Optional, Tuple
+
+from .runtime import Plan
+
+
+def split(total: int, parts: int, rank: int, align: int = 32) -> Tuple[int, int]:
+    """Contiguous [begin, end) block of `total` for `rank`, boundaries aligned."""
+    units = (total + align - 1) // align
+    b = units * rank // parts
+    e = units * (rank + 1) // parts
+    return min(total, b * align), min(total, e * align)
+
+
+class ShardedPlan:
+    def __init__(self, sequence: Optional[str] = None, rows: int = 0, cols: int = 0,
+                 mode: str = "fused", script: Optional[str] = None, world: Optional[int] = None,
+                 rank: Optional[int] = None, group=None,
+                 executor: Optional[Callable] = None, allreduce: Optional[Callable] = None):
+        import torch.distributed as dist
+        if world is None:
+            world = dist.get_world_size(group) if dist.is_initialized() else 1
+        if rank is None:
+            rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.world, self.rank, self.group = world, rank, group
+        self.rows_g, self.cols_g = (rows + 31) // 32 * 32, (cols + 31) // 32 * 32
+        probe = (Plan.compile(script, rows, cols, mode) if script else
+                 Plan.sequence(sequence, rows, cols, mode))
+        d = probe.describe()
+        self.matrix_plan = any(k["kind"] == "matrix" for k in d["kernels"]) or any(
+            b["rows"] > 1 for b in d["buffers"])
+        if self.matrix_plan:
+            self.r0, self.r1 = split(self.rows_g, world, rank)
+            lrows, lcols = self.r1 - self.r0, self.cols_g
+        else:
+            self.r0, self.r1 = split(self.cols_g, world, rank)
+            lrows, lcols = 1, self.r1 - self.r0
+        if lrows <= 0 or lcols <= 0:
+            raise ValueError("problem too small for %d ranks" % world)
+        self.plan = (Plan.compile(script, lrows, lcols, mode) if script else
+                     Plan.sequence(sequence, lrows, lcols, mode))
+        self.desc = self.plan.describe()
+        self.global_desc = d
+        self.collective_after = [self.plan.column_outputs(k) for k in range(self.plan.num_kernels)]
+        self.executor = executor
+        self.allreduce = allreduce
+
+    # -- partition of one buffer -------------------------------------------------
+    def local_slice(self, name: str):
+        """(axis, begin, end) of the global buffer this rank holds, or None if
+        the buffer is replicated."""
+        b = next(x for x in self.global_desc["buffers"] if x["name"] == name)
+        if b.get("scalar"):
+            return None
+        if self.matrix_plan:
+            if b["rows"] > 1:
+                return (0, self.r0, self.r1)
+            if b["row_indexed"]:
+                return (1, self.r0, self.r1)
+            return None
+        return (1, self.r0, self.r1)
+
+    def local_shape(self, name: str):
+        b = next(x for x in self.desc["buffers"] if x["name"] == name)
+        return (b["rows"], b["cols"]) if b["rows"] > 1 else (b["cols"],)
+
+    # -- execution -----------------------------------------------------------------
+    def _allreduce(self, t):
+        if self.allreduce is not None:
+            return self.allreduce(t)
+        if self.world == 1:
+            return
+        import torch.distributed as dist
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+
+    def launch(self, buffers: Mapping[str, object], scalars: Mapping[str, float] = {},
+               stream=None) -> Dict[str, int]:
+        """Runs every kernel on the local shard; all-reduces partial column /
+        dot results right after the kernel that produced them."""
+        collectives = 0
+        for k in range(self.plan.num_kernels):
+            if self.executor is not None:
+                self.executor(self.desc["kernels"][k], buffers, scalars)
+            else:
+                self.plan.launch_kernel(k, buffers, scalars, stream)
+            for name in self.collective_after[k]:
+                self._allreduce(buffers[name])
+                collectives += 1
+        return {"kernels": self.plan.num_kernels, "collectives": collectives}

@@ -70,7 +70,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.idx), "--query-gpu=" + self.FIELDS,
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "25"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -117,13 +117,17 @@ def measured_peak():
 
 
 def ncu_traffic(kernel_key: str):
+    """DRAM bytes per launch of the kernel whose template name contains
+    kernel_key, from the committed ncu capture (profiles/ncu_traffic.json)."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(p):
         return None
     with open(p) as f:
         d = json.load(f)
-    v = d.get(kernel_key)
-    return v.get("dram_bytes_per_launch") if isinstance(v, dict) else v
+    for k, v in d.items():
+        if kernel_key in k:
+            return v.get("dram_bytes_per_launch") if isinstance(v, dict) else v
+    return None
 
 
 # ---------------------------------------------------------------------------
@@ -296,6 +300,61 @@ def run_e2e(args, torch, mf, steps):
             "path": "C-ABI mf_launch_host (pinned host buffers, H2D + fused kernels + D2H)"}
 
 
+def run_sharded(args, torch, mf, rank, world, seq):
+    """BiCGK / ATAX at 131072^2 row-sharded over the ranks (BASELINE configs[4]).
+    Each rank generates its row panel on the device (counter-based, global
+    row offset), runs the planner's fused kernels on it, and all-reduces the
+    column partials (NCCL) after the kernel that produced them."""
+    from paper_1305_1183_b200.sharding import ShardedPlan
+    m = n = args.n_matrix
+    sp = ShardedPlan(seq, m, n, "fused")
+    d = sp.desc
+    bufs = {}
+    for i, b in enumerate(d["buffers"]):
+        if b["role"] == "intermediate":
+            continue
+        shp = (b["rows"], b["cols"]) if b["rows"] > 1 else (b["cols"],)
+        t = torch.empty(shp, device="cuda", dtype=torch.float32)
+        if b["role"] == "input":
+            sl = sp.local_slice(b["name"])
+            if b["rows"] > 1:  # tile row panel: global element index (r0 + i) * n + j
+                mf.generate(t, seed=11 + i, row0=sp.r0, ncols_global=n)
+            elif sl is not None:  # row-indexed vector slice
+                mf.runtime._check(mf.lib().mf_generate(mf.runtime.C.c_void_p(t.data_ptr()),
+                                                       t.numel(), 1, 1, 11 + i, sp.r0, 1, None))
+            else:
+                mf.generate(t, seed=11 + i)
+        bufs[b["name"]] = t
+    local_bytes = d["bytes_loaded"] + d["bytes_stored"]
+    for _ in range(args.warmup):
+        sp.launch(bufs, {})
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    gpu_index = int(os.environ.get("LOCAL_RANK", "0"))
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(gpu_index) as clk:
+        start.record()
+        for _ in range(args.steps):
+            sp.launch(bufs, {})
+        end.record()
+        torch.cuda.synchronize()
+    ms = start.elapsed_time(end)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+        tb = torch.tensor([local_bytes], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(tb)
+        total_bytes = float(tb.item())
+    else:
+        total_bytes = float(local_bytes)
+    return {"ms_per_step": ms / args.steps, "value": total_bytes * args.steps / (ms / 1e3) / 1e9,
+            "clocks": clk.summary(), "launches": args.steps * sp.plan.num_kernels,
+            "kernels": [k["name"] for k in d["kernels"]], "rows_per_rank": sp.r1 - sp.r0,
+            "collectives_per_step": sum(len(c) for c in sp.collective_after)}
+
+
 SUITE = [("AXPYDOT", 1, 1 << 24), ("BICGK", 16384, 16384), ("ATAX", 16384, 16384),
          ("GEMVER", 32768, 32768), ("GESUMMV", 32768, 32768)]
 
@@ -329,13 +388,15 @@ def run_suite(args, torch, mf):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="mapfuse", choices=["mapfuse", "reference"])
     ap.add_argument("--n", type=int, default=N_DEFAULT)
     ap.add_argument("--no-suite", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--workload", default="blas1", choices=["blas1", "bicgk-sharded", "atax-sharded"])
+    ap.add_argument("--n-matrix", type=int, default=131072)
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     rank, local, world = env_rank()
@@ -369,6 +430,30 @@ def main():
     import paper_1305_1183_b200 as mf
     mf.lib()
 
+    if args.workload != "blas1":
+        seq = "BICGK" if args.workload.startswith("bicgk") else "ATAX"
+        r = run_sharded(args, torch, mf, rank, world, seq)
+        peak, peak_kind = measured_peak()
+        if rank == 0:
+            line = {"metric": METRIC, "value": round(r["value"], 1), "unit": "GB/s", "n_gpus": world,
+                    "steps": args.steps, "warmup": args.warmup,
+                    "ms_per_step": round(r["ms_per_step"], 4), "higher_is_better": True,
+                    "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                    "config": {"workload": "%s fp32 %dx%d row-sharded over %d GPU(s), NCCL all-reduce "
+                                           "of the column partials" % (seq, args.n_matrix, args.n_matrix, world),
+                               "rows_per_rank": r["rows_per_rank"], "kernels": r["kernels"],
+                               "collectives_per_step": r["collectives_per_step"],
+                               "l2": "inputs (64 GiB) >> L2; no flush"},
+                    "roofline": {"bound": "hbm", "achieved": round(r["value"] / world, 1), "peak": peak,
+                                 "unit": "GB/s", "frac": round(r["value"] / world / peak, 4),
+                                 "traffic": None, "peak_source": peak_kind + " (per GPU)"},
+                    "clocks": r["clocks"], "gpu_launches": r["launches"]}
+            print(json.dumps(line), flush=True)
+        if world > 1:
+            torch.distributed.barrier()
+            torch.distributed.destroy_process_group()
+        return
+
     res = run_workload(args, torch, mf, rank, world)
     ms_per_step = res["total_ms"] / args.steps
     value = res["step_bytes"] * world * args.steps / (res["total_ms"] / 1e3) / 1e9
@@ -379,7 +464,7 @@ def main():
     peak, peak_kind = measured_peak()
     achieved = vadd_bytes / (kms / 1e3) / 1e9
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": ncu_traffic("VADD"),
+                "frac": round(achieved / peak, 4), "traffic": ncu_traffic("stream_kernel<3, 1, 0>"),
                 "kernel": key[2], "peak_source": peak_kind + " (MEASURED_PEAKS.json hbm_gbs)",
                 "algorithmic_bytes_per_launch": vadd_bytes,
                 "avg_launch_us": round(kms * 1e3, 1)}

@@ -1,0 +1,112 @@
+"""GPU parity at BASELINE sizes through size-independent checks.
+
+Full-size problems exceed what the CPU oracle evaluates in seconds, so the
+matrices are generated on the device by the counter-based generator that
+oracle/mf_oracle.c restates bit for bit, and sampled rows / columns are
+re-derived in fp64 on the CPU.
+"""
+import numpy as np
+import pytest
+
+from gpu_util import TAU
+from oracle import COracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+    import paper_1305_1183_b200 as mf
+    mf.lib()
+    return torch, mf, COracle()
+
+
+def _check(got, ref, absref, what):
+    err = np.abs(got.astype(np.float64) - ref)
+    lim = TAU * absref + np.spacing(np.abs(ref).astype(np.float32)).astype(np.float64)
+    assert np.all(err <= lim), (what, float(np.max(err / lim)))
+
+
+@pytest.mark.parametrize("m,n", [(16384, 16384), (4096, 131072), (131072, 131072)])
+def test_bicgk_sampled_rows_and_columns(env, m, n):
+    torch, mf, co = env
+    plan = mf.Plan.sequence("BICGK", m, n, "fused")
+    A = torch.empty(m, n, device="cuda")
+    mf.generate(A, seed=7)
+    p = torch.empty(n, device="cuda")
+    r = torch.empty(m, device="cuda")
+    mf.generate(p, seed=8)
+    mf.generate(r, seed=9)
+    q = torch.empty(m, device="cuda")
+    s = torch.empty(n, device="cuda")
+    plan.launch({"A": A, "p": p, "r": r, "q": q, "s": s})
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(m + n)
+    rows = np.sort(rng.choice(m, 12, replace=False))
+    cols = np.sort(rng.choice(n, 12, replace=False))
+    pc, rc = p.cpu().numpy(), r.cpu().numpy()
+    qr, qa = co.hash_rows(7, n, rows, pc)
+    _check(q.cpu().numpy()[rows], qr, qa, "q")
+    sr, sa = co.hash_cols(7, n, 0, m, cols, rc)
+    _check(s.cpu().numpy()[cols], sr, sa, "s")
+    del A
+    torch.cuda.empty_cache()
+
+
+def test_gemver_full_size_properties(env):
+    """GEMVER 32768^2: B is exact (fp64 rank update rounded once); x and w
+    checked on sampled entries against fp64 recomputation from B."""
+    torch, mf, co = env
+    m = n = 32768
+    plan = mf.Plan.sequence("GEMVER", m, n, "fused")
+    d = {}
+    for i, name in enumerate(["A", "u1", "v1", "u2", "v2", "y", "z"]):
+        shp = (m, n) if name == "A" else ((m,) if name in ("u1", "u2", "y") else (n,))
+        d[name] = torch.empty(shp, device="cuda")
+        mf.generate(d[name], seed=20 + i)
+    d["B"] = torch.empty(m, n, device="cuda")
+    d["x"] = torch.empty(n, device="cuda")
+    d["w"] = torch.empty(m, device="cuda")
+    al, be = 0.625, 0.375
+    plan.launch(d, {"alpha": al, "beta": be})
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(3)
+    rows = np.sort(rng.choice(m, 8, replace=False))
+    cols = np.sort(rng.choice(n, 8, replace=False))
+    f64 = lambda t: t.cpu().numpy().astype(np.float64)
+    u1, v1, u2, v2, y, z = (f64(d[k]) for k in ("u1", "v1", "u2", "v2", "y", "z"))
+    A_rows = d["A"][torch.from_numpy(rows).cuda()].cpu().numpy().astype(np.float64)
+    B_rows = d["B"][torch.from_numpy(rows).cuda()].cpu().numpy()
+    Bexp = (A_rows + u1[rows, None] * v1[None, :] + u2[rows, None] * v2[None, :]).astype(np.float32)
+    assert np.array_equal(B_rows, Bexp)
+    # x = beta * B^T y + z on sampled columns (B exact in float -> fp64 reference)
+    Bc = d["B"][:, torch.from_numpy(cols).cuda()].cpu().numpy().astype(np.float64)
+    Ac = d["A"][:, torch.from_numpy(cols).cuda()].cpu().numpy().astype(np.float64)
+    B64c = Ac + u1[:, None] * v1[None, cols] + u2[:, None] * v2[None, cols]
+    xref = be * (B64c.T @ y) + z[cols]
+    xabs = abs(be) * (np.abs(B64c).T @ np.abs(y)) + np.abs(z[cols])
+    _check(d["x"].cpu().numpy()[cols], xref, xabs, "x")
+    # w = alpha * B x on sampled rows using the device's x
+    x = f64(d["x"])
+    wref = al * (B_rows.astype(np.float64) @ x)
+    wabs = abs(al) * (np.abs(B_rows.astype(np.float64)) @ np.abs(x))
+    _check(d["w"].cpu().numpy()[rows], wref, wabs, "w")
+
+
+def test_sharded_plan_single_rank_equals_plan(env):
+    torch, mf, co = env
+    from paper_1305_1183_b200.sharding import ShardedPlan
+    sp = ShardedPlan("ATAX", 2048, 3072, "fused", world=1, rank=0)
+    plan = mf.Plan.sequence("ATAX", 2048, 3072, "fused")
+    A = torch.empty(2048, 3072, device="cuda")
+    x = torch.empty(3072, device="cuda")
+    mf.generate(A, seed=1)
+    mf.generate(x, seed=2)
+    y1 = torch.empty(3072, device="cuda")
+    y2 = torch.empty(3072, device="cuda")
+    info = sp.launch({"A": A, "x": x, "y": y1, "t": torch.empty(2048, device="cuda")})
+    plan.launch({"A": A, "x": x, "y": y2})
+    torch.cuda.synchronize()
+    assert info["collectives"] == 1
+    assert torch.equal(y1, y2)

@@ -114,7 +114,10 @@ int mf_launch_kernel(const mf_plan* plan, int k, const mf_buffer* buffers, int n
 
 /* vm::launch's exact contract with host memory: copies inputs host->device,
  * runs the plan, copies every bound output back, synchronizes.  stats->ms is
- * the device time of the kernels alone. */
+ * the device time of the kernels alone -- except for element-wise plans over
+ * PINNED host buffers, which run as a chunked 3-stream pipeline (H2D, kernels
+ * and D2H of different chunks overlap); there stats->ms covers the whole
+ * pipeline. */
 int mf_launch_host(const mf_plan* plan, const mf_buffer* host_buffers, int nbuf,
                    const mf_scalar* scalars, int nscalars, mf_stats* stats);
 

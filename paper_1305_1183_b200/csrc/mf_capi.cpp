@@ -1,6 +1,7 @@
 // mf_capi.cpp -- extern "C" surface declared in include/mapfuse_b200.h.
 #include "mapfuse_b200.h"
 
+#include <algorithm>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -96,6 +97,89 @@ void fill_stats(const NativePlan& p, int k0, int k1, const BufMap& b, mf_stats* 
       st->bytes_stored += kern.bytes_stored(1, len);
     }
   }
+}
+
+
+// Element-wise plans (only stream kernels, no cross-element reduction, every
+// buffer the same length) over PINNED host memory are executed as a
+// chunked pipeline: chunk c's H2D copy, kernels and D2H copy are ordered on
+// one of three streams, so transfers in both PCIe directions overlap each
+// other and the kernels.  Results are identical to the one-shot path (the
+// kernels are element-wise).
+bool host_pipeline_ok(const NativePlan& P, const mf_buffer* hb, int nbuf) {
+  if (nbuf == 0) return false;
+  for (const auto& k : P.kernels)
+    if (k.kind != NativeKernel::Kind::Stream || k.stream.has_dot) return false;
+  const int64_t len = (int64_t)hb[0].rows * hb[0].cols;
+  if (len < (int64_t)(8 << 20)) return false;  // small transfers: not worth it
+  for (int i = 0; i < nbuf; ++i) {
+    if ((int64_t)hb[i].rows * hb[i].cols != len) return false;
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, hb[i].data) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    if (at.type != cudaMemoryTypeHost) return false;  // pageable: no async overlap
+  }
+  return true;
+}
+
+double launch_host_pipelined(const mf_plan* plan, const mf_buffer* hb, int nbuf, const BufMap& dev,
+                             const ScalarMap& s) {
+  const NativePlan& P = plan->plan;
+  const int64_t len = (int64_t)hb[0].rows * hb[0].cols;
+  const int64_t chunk = std::max<int64_t>(32, (int64_t)(16 << 20) / 32 * 32);  // 64 MB per buffer
+  BufMap full = complete_bindings(P, dev, plan->ws);
+  constexpr int kStreams = 3;
+  cudaStream_t st[kStreams];
+  for (auto& x : st) check_cuda(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking), "stream");
+  cudaEvent_t start, stop, done[kStreams];
+  check_cuda(cudaEventCreate(&start), "event");
+  check_cuda(cudaEventCreate(&stop), "event");
+  for (auto& e : done) check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+  check_cuda(cudaEventRecord(start, st[0]), "event");
+  for (int i = 1; i < kStreams; ++i) check_cuda(cudaStreamWaitEvent(st[i], start, 0), "wait");
+  int c = 0;
+  for (int64_t off = 0; off < len; off += chunk, ++c) {
+    const int64_t n = std::min(chunk, len - off);
+    cudaStream_t q = st[c % kStreams];
+    BufMap part;
+    for (const auto& [name, d] : full) {
+      DevBuf x = d;
+      x.ptr = d.ptr + off;
+      x.rows = 1;
+      x.cols = n;
+      part[name] = x;
+    }
+    for (int i = 0; i < nbuf; ++i) {
+      const BufferSpec* spec = P.find(hb[i].name);
+      if (spec && spec->role != Role::Input) continue;
+      check_cuda(cudaMemcpyAsync(part[hb[i].name].ptr, hb[i].data + off, sizeof(float) * n,
+                                 cudaMemcpyHostToDevice, q),
+                 "H2D");
+    }
+    for (int k = 0; k < (int)P.kernels.size(); ++k) run_kernel(P, k, part, s, q, plan->ws);
+    for (int i = 0; i < nbuf; ++i) {
+      const BufferSpec* spec = P.find(hb[i].name);
+      if (spec && spec->role == Role::Input) continue;
+      check_cuda(cudaMemcpyAsync(hb[i].data + off, part[hb[i].name].ptr, sizeof(float) * n,
+                                 cudaMemcpyDeviceToHost, q),
+                 "D2H");
+    }
+  }
+  for (int i = 1; i < kStreams; ++i) {
+    check_cuda(cudaEventRecord(done[i], st[i]), "event");
+    check_cuda(cudaStreamWaitEvent(st[0], done[i], 0), "wait");
+  }
+  check_cuda(cudaEventRecord(stop, st[0]), "event");
+  check_cuda(cudaEventSynchronize(stop), "sync");
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, start, stop);
+  cudaEventDestroy(start);
+  cudaEventDestroy(stop);
+  for (auto& e : done) cudaEventDestroy(e);
+  for (auto& x : st) cudaStreamDestroy(x);
+  return ms;
 }
 
 }  // namespace
@@ -199,6 +283,13 @@ int mf_launch_host(const mf_plan* plan, const mf_buffer* host_buffers, int nbuf,
       d.ptr = plan->ws.named(std::string("__host__") + h.name, (int64_t)h.rows * h.cols);
       dev[h.name] = d;
     }
+    ScalarMap s = to_scalars(scalars, nscalars);
+    if (host_pipeline_ok(P, host_buffers, nbuf)) {
+      const double ms = launch_host_pipelined(plan, host_buffers, nbuf, dev, s);
+      fill_stats(P, 0, (int)P.kernels.size(), dev, stats);
+      if (stats) stats->ms = ms;
+      return;
+    }
     cudaStream_t st = nullptr;
     for (int i = 0; i < nbuf; ++i) {
       const mf_buffer& h = host_buffers[i];
@@ -209,7 +300,6 @@ int mf_launch_host(const mf_plan* plan, const mf_buffer* host_buffers, int nbuf,
                  "cudaMemcpy H2D");
     }
     BufMap b = complete_bindings(P, dev, plan->ws);
-    ScalarMap s = to_scalars(scalars, nscalars);
     cudaEvent_t e0, e1;
     check_cuda(cudaEventCreate(&e0), "cudaEventCreate");
     check_cuda(cudaEventCreate(&e1), "cudaEventCreate");
@@ -252,6 +342,12 @@ int mf_set_option(const char* key, int value) {
       options().matrix_k = value;
     } else if (k == "f64acc") {
       options().f64acc = value ? 1 : 0;
+    } else if (k == "stream_unroll") {
+      if (value != 0 && value != 2 && value != 4 && value != 8) throw Invalid("stream_unroll: 0|2|4|8");
+      options().stream_unroll = value;
+    } else if (k == "stream_ctas_per_sm") {
+      if (value < 1 || value > 8) throw Invalid("stream_ctas_per_sm: 1..8");
+      options().stream_ctas_per_sm = value;
     } else if (k == "tma") {
       options().tma = value < 0 ? -1 : (value ? 1 : 0);
     } else if (k == "occupancy") {
@@ -269,6 +365,8 @@ int mf_get_option(const char* key) {
   if (k == "f64acc") return options().f64acc;
   if (k == "occupancy") return options().occupancy;
   if (k == "tma") return options().tma;
+  if (k == "stream_unroll") return options().stream_unroll;
+  if (k == "stream_ctas_per_sm") return options().stream_ctas_per_sm;
   return -1;
 }
 

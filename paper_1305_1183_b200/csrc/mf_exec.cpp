@@ -22,6 +22,8 @@ EngineOptions& options() {
     if (const char* v = std::getenv("MF_F64ACC")) e.f64acc = std::atoi(v);
     if (const char* v = std::getenv("MF_OCCUPANCY")) e.occupancy = std::atoi(v);
     if (const char* v = std::getenv("MF_TMA")) e.tma = std::atoi(v);
+    if (const char* v = std::getenv("MF_STREAM_UNROLL")) e.stream_unroll = std::atoi(v);
+    if (const char* v = std::getenv("MF_STREAM_CTAS")) e.stream_ctas_per_sm = std::atoi(v);
     return e;
   }();
   return o;
@@ -142,7 +144,7 @@ void run_stream(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc, 
     for (int i = 0; i < nin; ++i) a.coef[q][i] = coef(op.outs[q].coef[i], sc, k.name);
   }
   const int sms = device_sm_count();
-  const int grid = stream_grid(a.n4, sms);
+  const int grid = stream_grid(a.n4, sms, options().stream_ctas_per_sm);
   if (op.has_dot) {
     const DevBuf& r = need(bufs, op.dot_out, k.name);
     if (r.size() < 1) throw Fault("kernel " + k.name + ": empty dot output");
@@ -155,7 +157,8 @@ void run_stream(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc, 
     a.ticket = ws.counters(s) + 2;
   }
   if (n == 0) return;
-  check_cuda(launch_stream(nin, nout, op.has_dot, a, grid, s), ("launch " + k.name).c_str());
+  check_cuda(launch_stream(nin, nout, op.has_dot, a, grid, options().stream_unroll, s),
+             ("launch " + k.name).c_str());
 }
 
 void run_matrix(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc, cudaStream_t s,

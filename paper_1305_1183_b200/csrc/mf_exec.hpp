@@ -35,6 +35,8 @@ struct EngineOptions {
   int matrix_k = 2;
   int f64acc = 0;
   int occupancy = 2;
+  int stream_unroll = 0;       // 0 = default (by input count), else 2 / 4 / 8
+  int stream_ctas_per_sm = 4;
   int tma = -1;  // matrix kernels: -1 auto (by shape), 1 = TMA ring, 0 = register-fed
 };
 EngineOptions& options();

@@ -69,9 +69,9 @@ struct StreamBody {
   }
 };
 
-template <int NIN, int NOUT, bool DOT>
+template <int NIN, int NOUT, bool DOT, int U>
 __global__ void __launch_bounds__(kThreads) stream_kernel(StreamArgs a) {
-  constexpr int U = (NIN <= 2) ? 4 : 2;  // float4 loads in flight per input per thread
+  // U float4 loads in flight per input per thread
   const long long stride = (long long)gridDim.x * kThreads;
   long long i = (long long)blockIdx.x * kThreads + threadIdx.x;
   double acc = 0.0;
@@ -333,24 +333,28 @@ MatrixFn matrix_fn(const MatrixShape& s, const MatrixTuning& t) {
 }
 
 template <int NIN, int NOUT, bool DOT>
-cudaError_t go_stream(const StreamArgs& a, int grid, cudaStream_t s) {
-  stream_kernel<NIN, NOUT, DOT><<<grid, kThreads, 0, s>>>(a);
+cudaError_t go_stream(const StreamArgs& a, int grid, int unroll, cudaStream_t s) {
+  // default: ~8 float4 loads in flight per thread
+  if (unroll <= 0) unroll = NIN <= 2 ? 8 : 2;  // measured best on B200 (tools/sweep.py)
+  if (unroll >= 8) stream_kernel<NIN, NOUT, DOT, 8><<<grid, kThreads, 0, s>>>(a);
+  else if (unroll >= 4) stream_kernel<NIN, NOUT, DOT, 4><<<grid, kThreads, 0, s>>>(a);
+  else stream_kernel<NIN, NOUT, DOT, 2><<<grid, kThreads, 0, s>>>(a);
   return cudaGetLastError();
 }
 
 }  // namespace
 
 // ---------------------------------------------------------------------------
-int stream_grid(long long n4, int sms) {
-  long long want = (long long)sms * 4;
+int stream_grid(long long n4, int sms, int ctas_per_sm) {
+  long long want = (long long)sms * (ctas_per_sm > 0 ? ctas_per_sm : 4);
   long long need = (n4 + kThreads - 1) / kThreads;
   return (int)std::max(1LL, std::min(want, need));
 }
 
-cudaError_t launch_stream(int nin, int nout, bool dot, const StreamArgs& a, int grid,
+cudaError_t launch_stream(int nin, int nout, bool dot, const StreamArgs& a, int grid, int unroll,
                           cudaStream_t s) {
 #define MF_STREAM_CASE(I, O, D) \
-  if (nin == I && nout == O && dot == D) return go_stream<I, O, D>(a, grid, s);
+  if (nin == I && nout == O && dot == D) return go_stream<I, O, D>(a, grid, unroll, s);
   MF_STREAM_CASE(1, 1, false)
   MF_STREAM_CASE(2, 1, false)
   MF_STREAM_CASE(3, 1, false)

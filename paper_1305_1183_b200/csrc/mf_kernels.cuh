@@ -62,9 +62,9 @@ struct MatrixTuning {
 };
 
 // Launchers; return cudaSuccess or the launch error.  `sms` = SM count.
-cudaError_t launch_stream(int nin, int nout, bool dot, const StreamArgs& a, int grid,
+cudaError_t launch_stream(int nin, int nout, bool dot, const StreamArgs& a, int grid, int unroll,
                           cudaStream_t s);
-int stream_grid(long long n4, int sms);
+int stream_grid(long long n4, int sms, int ctas_per_sm);
 
 // Fills CB/RB/tiles and returns the grid size (co-resident for the barrier).
 cudaError_t matrix_config(const MatrixShape& sh, const MatrixTuning& t, long long m, long long n,

@@ -223,3 +223,29 @@ def test_kernel_text_boundary_on_gpu(env, seq):
     torch.cuda.synchronize()
     for name, v in full.items():
         assert np.array_equal(bufs[name].cpu().numpy().ravel(), v.ravel()), name
+
+
+@pytest.mark.parametrize("seq", ["VADD", "WAXPBY"])
+def test_host_launch_pipelined_pinned(env, seq):
+    """Element-wise plans over pinned host memory run as an overlapped
+    chunked pipeline; results must equal the device path bit for bit."""
+    torch, mf, co = env
+    n = (1 << 24) + 4096  # several chunks + a ragged tail
+    vals = rand_inputs(seq, 1, n, 17)
+    plan = mf.Plan.sequence(seq, 1, n, "fused")
+    host = {}
+    keep = []
+    for k, v in vals.items():
+        if isinstance(v, np.ndarray):
+            t = torch.from_numpy(v).pin_memory()
+            keep.append(t)
+            host[k] = t.numpy()
+    outname = {"VADD": "x", "WAXPBY": "w"}[seq]
+    to = torch.zeros(n, dtype=torch.float32).pin_memory()
+    keep.append(to)
+    host[outname] = to.numpy()
+    sc = {k: v for k, v in vals.items() if not isinstance(v, np.ndarray)}
+    st = plan.launch_host(host, sc)
+    assert st["ms"] > 0
+    want = co.execute(seq, 1, n, vals)[outname]
+    assert np.array_equal(host[outname], want)

@@ -202,7 +202,8 @@ def time_kernels(torch, plans, steps, warmup, flush=None):
     e = 0
     for s in range(steps):
         if flush is not None:
-            flush.zero_()
+            flush[0].zero_()
+            flush[1].sum()
         evs[e].record()
         first = e
         for plan, bufs, sc in plans:
@@ -360,7 +361,10 @@ SUITE = [("AXPYDOT", 1, 1 << 24), ("BICGK", 16384, 16384), ("ATAX", 16384, 16384
 
 
 def run_suite(args, torch, mf):
-    flush = torch.empty(256 << 20, dtype=torch.float32, device="cuda")  # 1 GiB > L2
+    # L2 flush between timed launches: write 1 GiB, then read another 1 GiB so
+    # the L2 holds clean lines (no write-backs land inside the timed kernel)
+    flush = (torch.empty(256 << 20, dtype=torch.float32, device="cuda"),
+             torch.empty(256 << 20, dtype=torch.float32, device="cuda"))
     sc = {"alpha": 0.5, "beta": 0.75}
     peak, _ = measured_peak()
     out = {}
@@ -388,7 +392,7 @@ def run_suite(args, torch, mf):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="mapfuse", choices=["mapfuse", "reference"])
     ap.add_argument("--n", type=int, default=N_DEFAULT)

@@ -121,6 +121,24 @@ int mf_launch_kernel(const mf_plan* plan, int k, const mf_buffer* buffers, int n
 int mf_launch_host(const mf_plan* plan, const mf_buffer* host_buffers, int nbuf,
                    const mf_scalar* scalars, int nscalars, mf_stats* stats);
 
+/* Row-sharded runs with the column reduction fused into the kernel: every
+ * rank (one process per GPU) creates a peer group sized for n columns,
+ * exports its IPC handle bytes, opens every peer's handle, then launches
+ * kernels through mf_launch_kernel_peers.  Kernels with column outputs
+ * (A^T r, B^T y) then finish with an in-kernel reduce-scatter + all-gather
+ * over NVLink peer memory instead of a separate collective.  Ranks must
+ * issue the same launch sequence.  mf_peer_group_connect_local links groups
+ * living in one process (virtual ranks sharing a GPU; tests). */
+typedef struct mf_peer_group mf_peer_group;
+int mf_peer_group_create(int nranks, int rank, int64_t n_capacity, mf_peer_group** out);
+int mf_peer_group_handle(const mf_peer_group* g, void* out, int cap); /* returns bytes needed */
+int mf_peer_group_open(mf_peer_group* g, int peer, const void* handle, int len);
+int mf_peer_group_connect_local(mf_peer_group* g, int peer, const mf_peer_group* other);
+void mf_peer_group_destroy(mf_peer_group* g);
+int mf_launch_kernel_peers(const mf_plan* plan, int k, mf_peer_group* g, const mf_buffer* buffers,
+                           int nbuf, const mf_scalar* scalars, int nscalars, void* stream,
+                           mf_stats* stats);
+
 /* Counter-based synthetic data on the device, identical to the CPU checker's
  * generator: out[r*ld + c] = U(seed, (row0 + r) * ncols_global + c). */
 int mf_generate(float* dev, int64_t rows, int64_t cols, int64_t ld, uint64_t seed, int64_t row0,

@@ -18,6 +18,10 @@ struct mf_plan {
   mutable Workspace ws;
 };
 
+struct mf_peer_group {
+  PeerGroup g;
+};
+
 namespace {
 
 thread_local std::string g_error;
@@ -324,6 +328,83 @@ int mf_launch_host(const mf_plan* plan, const mf_buffer* host_buffers, int nbuf,
   });
 }
 
+int mf_peer_group_create(int nranks, int rank, int64_t n_capacity, mf_peer_group** out) {
+  return guarded([&] {
+    if (!out || nranks < 1 || nranks > 8 || rank < 0 || rank >= nranks || n_capacity <= 0)
+      throw Invalid("peer group: bad arguments");
+    auto p = std::make_unique<mf_peer_group>();
+    PeerGroup& g = p->g;
+    g.nranks = nranks;
+    g.rank = rank;
+    g.n_cap = (n_capacity + 31) / 32 * 32;
+    check_cuda(cudaMalloc(&g.inbox, sizeof(float) * 2 * (size_t)nranks * g.n_cap), "cudaMalloc inbox");
+    check_cuda(cudaMalloc(&g.outbox, sizeof(float) * 2 * (size_t)g.n_cap), "cudaMalloc outbox");
+    check_cuda(cudaMalloc(&g.flags, 64 * sizeof(unsigned)), "cudaMalloc flags");
+    check_cuda(cudaMemset(g.flags, 0, 64 * sizeof(unsigned)), "cudaMemset flags");
+    g.peer_inbox[rank] = g.inbox;
+    g.peer_outbox[rank] = g.outbox;
+    g.peer_flags[rank] = g.flags;
+    *out = p.release();
+  });
+}
+
+int mf_peer_group_handle(const mf_peer_group* gp, void* out, int cap) {
+  const int need = 3 * (int)sizeof(cudaIpcMemHandle_t);
+  if (!gp || !out || cap < need) return need;
+  cudaIpcMemHandle_t h[3];
+  if (cudaIpcGetMemHandle(&h[0], gp->g.inbox) != cudaSuccess ||
+      cudaIpcGetMemHandle(&h[1], gp->g.outbox) != cudaSuccess ||
+      cudaIpcGetMemHandle(&h[2], gp->g.flags) != cudaSuccess) {
+    g_error = "cudaIpcGetMemHandle failed";
+    cudaGetLastError();
+    return -1;
+  }
+  std::memcpy(out, h, need);
+  return need;
+}
+
+int mf_peer_group_open(mf_peer_group* gp, int peer, const void* handle, int len) {
+  return guarded([&] {
+    if (!gp || !handle || len != 3 * (int)sizeof(cudaIpcMemHandle_t)) throw Invalid("bad handle");
+    PeerGroup& g = gp->g;
+    if (peer < 0 || peer >= g.nranks || peer == g.rank) throw Invalid("bad peer index");
+    cudaIpcMemHandle_t h[3];
+    std::memcpy(h, handle, sizeof h);
+    void* p[3] = {};
+    for (int i = 0; i < 3; ++i) {
+      check_cuda(cudaIpcOpenMemHandle(&p[i], h[i], cudaIpcMemLazyEnablePeerAccess),
+                 "cudaIpcOpenMemHandle");
+      g.opened.push_back(p[i]);
+    }
+    g.peer_inbox[peer] = static_cast<float*>(p[0]);
+    g.peer_outbox[peer] = static_cast<float*>(p[1]);
+    g.peer_flags[peer] = static_cast<unsigned*>(p[2]);
+  });
+}
+
+int mf_peer_group_connect_local(mf_peer_group* gp, int peer, const mf_peer_group* other) {
+  return guarded([&] {
+    if (!gp || !other || peer < 0 || peer >= gp->g.nranks) throw Invalid("bad peer");
+    gp->g.peer_inbox[peer] = other->g.inbox;
+    gp->g.peer_outbox[peer] = other->g.outbox;
+    gp->g.peer_flags[peer] = other->g.flags;
+  });
+}
+
+void mf_peer_group_destroy(mf_peer_group* g) { delete g; }
+
+int mf_launch_kernel_peers(const mf_plan* plan, int k, mf_peer_group* g, const mf_buffer* buffers,
+                           int nbuf, const mf_scalar* scalars, int nscalars, void* stream,
+                           mf_stats* stats) {
+  return guarded([&] {
+    if (!plan) throw Invalid("null plan");
+    BufMap b = complete_bindings(plan->plan, to_map(buffers, nbuf), plan->ws);
+    run_kernel(plan->plan, k, b, to_scalars(scalars, nscalars), static_cast<cudaStream_t>(stream),
+               plan->ws, g ? &g->g : nullptr);
+    fill_stats(plan->plan, k, k + 1, b, stats);
+  });
+}
+
 int mf_generate(float* dev, int64_t rows, int64_t cols, int64_t ld, uint64_t seed, int64_t row0,
                 int64_t ncols_global, void* stream) {
   return guarded([&] {
@@ -348,6 +429,9 @@ int mf_set_option(const char* key, int value) {
     } else if (k == "stream_ctas_per_sm") {
       if (value < 1 || value > 8) throw Invalid("stream_ctas_per_sm: 1..8");
       options().stream_ctas_per_sm = value;
+    } else if (k == "max_sms") {
+      if (value < 0) throw Invalid("max_sms >= 0");
+      options().max_sms = value;
     } else if (k == "tma") {
       options().tma = value < 0 ? -1 : (value ? 1 : 0);
     } else if (k == "occupancy") {
@@ -365,6 +449,7 @@ int mf_get_option(const char* key) {
   if (k == "f64acc") return options().f64acc;
   if (k == "occupancy") return options().occupancy;
   if (k == "tma") return options().tma;
+  if (k == "max_sms") return options().max_sms;
   if (k == "stream_unroll") return options().stream_unroll;
   if (k == "stream_ctas_per_sm") return options().stream_ctas_per_sm;
   return -1;

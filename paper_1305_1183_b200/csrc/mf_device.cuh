@@ -146,5 +146,121 @@ __device__ __forceinline__ void finalize(const MatrixArgs& a, int tid, int nthre
   }
 }
 
+// ---------------------------------------------------------------------------
+// Fused cross-rank finalize for column outputs (after the local grid barrier).
+// Phase A: every rank sums its band partials and writes the local column sums
+//          of slice s straight into rank s's inbox (remote stores over NVLink).
+// Phase B: after a system-scope arrival barrier, rank s reduces its slice over
+//          the P sources in fixed rank order (deterministic, identical on every
+//          rank), scales, writes its own y and its outbox.
+// Phase C: after a second barrier, every rank pulls the other slices from the
+//          owners' outboxes into its y.  Traffic per rank = 2(P-1)/P * n
+//          floats, the ring all-reduce volume, with no extra kernel launch.
+__device__ __forceinline__ void peer_signal_wait(const PeerLinks& pl, int which) {
+  // one thread of block 0, after a grid barrier: all CTAs' writes are done
+  __threadfence_system();
+  for (int s = 0; s < pl.nranks; ++s) atomicAdd_system(pl.flags[s] + which, 1u);
+  const unsigned target = pl.epoch * (unsigned)pl.nranks;
+  const long long t0 = clock64();
+  volatile unsigned* mine = pl.flags[pl.rank] + which;
+  while (*mine < target) {
+    __nanosleep(128);
+    if (pl.spin_limit > 0 && clock64() - t0 > pl.spin_limit) __trap();  // never hang the GPU
+  }
+  __threadfence_system();
+}
+
+template <int NCOL, typename ACC>
+__device__ __forceinline__ void finalize_columns_peers(const MatrixArgs& a, int tid, int nthreads) {
+  const PeerLinks& pl = a.peer;
+  const ACC* colpart = static_cast<const ACC*>(a.colpart);
+  const long long n4 = a.n / 4, gstride = (long long)gridDim.x * nthreads;
+  const long long slice4 = n4 / pl.nranks;  // n / P is a multiple of 4 (n % 32 == 0, P <= 8)
+  const long long P = pl.nranks;
+  // Phase A: local sums -> owner's inbox[c][rank][j]
+  for (long long s = (long long)blockIdx.x * nthreads + tid; s < (long long)NCOL * n4; s += gstride) {
+    const int c = (int)(s / n4);
+    const long long j4 = s % n4, j = j4 * 4;
+    ACC t[4] = {ACC(0), ACC(0), ACC(0), ACC(0)};
+    for (int b = 0; b < a.RB; ++b) {
+      const ACC* p = colpart + ((long long)c * a.RB + b) * a.n + j;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) t[e] += __ldcg(p + e);
+    }
+    const int owner = (int)min(j4 / slice4, P - 1);
+    float4 v = make_float4((float)t[0], (float)t[1], (float)t[2], (float)t[3]);
+    float* dst = pl.inbox[owner] + ((long long)c * P + pl.rank) * pl.n_cap + j;
+    *reinterpret_cast<float4*>(dst) = v;
+  }
+  grid_barrier(a.bar);
+  if (blockIdx.x == 0 && tid == 0) peer_signal_wait(pl, 0);
+  grid_barrier(a.bar);
+  // Phase B: reduce my slice in fixed source order
+  const long long lo4 = slice4 * pl.rank, hi4 = (pl.rank == P - 1) ? n4 : lo4 + slice4;
+  const float* inbox = pl.inbox[pl.rank];
+  float* outbox = pl.outbox[pl.rank];
+  for (long long s = (long long)blockIdx.x * nthreads + tid; s < (long long)NCOL * (hi4 - lo4);
+       s += gstride) {
+    const int c = (int)(s / (hi4 - lo4));
+    const long long j = (lo4 + s % (hi4 - lo4)) * 4;
+    double t[4] = {0, 0, 0, 0};
+    for (long long r = 0; r < P; ++r) {
+      const float4 v = __ldcg(reinterpret_cast<const float4*>(inbox + ((long long)c * P + r) * pl.n_cap + j));
+      t[0] += v.x;
+      t[1] += v.y;
+      t[2] += v.z;
+      t[3] += v.w;
+    }
+    float4 o = make_float4((float)(a.ac[c] * t[0]), (float)(a.ac[c] * t[1]), (float)(a.ac[c] * t[2]),
+                           (float)(a.ac[c] * t[3]));
+    *reinterpret_cast<float4*>(a.yc[c] + j) = o;
+    *reinterpret_cast<float4*>(outbox + (long long)c * pl.n_cap + j) = o;
+  }
+  grid_barrier(a.bar);
+  if (blockIdx.x == 0 && tid == 0) peer_signal_wait(pl, 1);
+  grid_barrier(a.bar);
+  // Phase C: gather the other slices from their owners
+  for (long long s = (long long)blockIdx.x * nthreads + tid; s < (long long)NCOL * n4; s += gstride) {
+    const int c = (int)(s / n4);
+    const long long j4 = s % n4;
+    const int owner = (int)min(j4 / slice4, P - 1);
+    if (owner == pl.rank) continue;
+    const float4 v = __ldcg(reinterpret_cast<const float4*>(pl.outbox[owner] + (long long)c * pl.n_cap + j4 * 4));
+    *reinterpret_cast<float4*>(a.yc[c] + j4 * 4) = v;
+  }
+}
+
+// Row partials (when a row spans several column chunks) are local to a rank.
+template <int NROW, typename ACC>
+__device__ __forceinline__ void finalize_rows(const MatrixArgs& a, int tid, int nthreads) {
+  if (NROW == 0 || a.CB <= 1) return;
+  const ACC* rowpart = static_cast<const ACC*>(a.rowpart);
+  const long long m4 = a.m / 4;
+  for (long long q = (long long)blockIdx.x * nthreads + tid; q < (long long)NROW * m4;
+       q += (long long)gridDim.x * nthreads) {
+    const int o = (int)(q / m4);
+    const long long i = (q % m4) * 4;
+    ACC t[4] = {ACC(0), ACC(0), ACC(0), ACC(0)};
+    for (int b = 0; b < a.CB; ++b) {
+      const ACC* p = rowpart + ((long long)o * a.CB + b) * a.m + i;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) t[e] += __ldcg(p + e);
+    }
+    float4 r = make_float4((float)(a.ar[o] * (double)t[0]), (float)(a.ar[o] * (double)t[1]),
+                           (float)(a.ar[o] * (double)t[2]), (float)(a.ar[o] * (double)t[3]));
+    *reinterpret_cast<float4*>(a.yr[o] + i) = r;
+  }
+}
+
+template <int NROW, int NCOL, typename ACC>
+__device__ __forceinline__ void finalize_any(const MatrixArgs& a, int tid, int nthreads) {
+  if (NCOL > 0 && a.peer.nranks > 1) {
+    finalize_rows<NROW, ACC>(a, tid, nthreads);
+    finalize_columns_peers<NCOL, ACC>(a, tid, nthreads);
+  } else {
+    finalize<NROW, NCOL, ACC>(a, tid, nthreads);
+  }
+}
+
 }  // namespace dev
 }  // namespace mapfuse::b200

@@ -24,6 +24,7 @@ EngineOptions& options() {
     if (const char* v = std::getenv("MF_TMA")) e.tma = std::atoi(v);
     if (const char* v = std::getenv("MF_STREAM_UNROLL")) e.stream_unroll = std::atoi(v);
     if (const char* v = std::getenv("MF_STREAM_CTAS")) e.stream_ctas_per_sm = std::atoi(v);
+    if (const char* v = std::getenv("MF_MAX_SMS")) e.max_sms = std::atoi(v);
     return e;
   }();
   return o;
@@ -90,6 +91,13 @@ float* Workspace::named(const std::string& key, int64_t words) {
   check_cuda(cudaMalloc(&p, std::max<int64_t>(words, 32) * sizeof(float)), "cudaMalloc(named)");
   named_[key] = {p, words};
   return p;
+}
+
+PeerGroup::~PeerGroup() {
+  for (void* p : opened) cudaIpcCloseMemHandle(p);
+  if (inbox) cudaFree(inbox);
+  if (outbox) cudaFree(outbox);
+  if (flags) cudaFree(flags);
 }
 
 // ---------------------------------------------------------------------------
@@ -162,7 +170,7 @@ void run_stream(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc, 
 }
 
 void run_matrix(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc, cudaStream_t s,
-                Workspace& ws) {
+                Workspace& ws, PeerGroup* peers) {
   const MatrixOp& op = k.matrix;
   MatrixShape sh{(int)op.mats.size(), (int)op.rank.size(), op.store.empty() ? 0 : 1,
                  (int)op.rows.size(), (int)op.cols.size()};
@@ -232,12 +240,26 @@ void run_matrix(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc, 
   }
   if (t.tma && !tma_supported(sh, t)) t.tma = false;
   int grid = 0;
+  const int sms = eo.max_sms > 0 ? std::min(eo.max_sms, device_sm_count()) : device_sm_count();
   if (t.tma)
-    check_cuda(matrix_tma_config(sh, t, m, n, device_sm_count(), &a, &grid),
-               ("configure " + k.name).c_str());
+    check_cuda(matrix_tma_config(sh, t, m, n, sms, &a, &grid), ("configure " + k.name).c_str());
   else
-    check_cuda(matrix_config(sh, t, m, n, device_sm_count(), &a, &grid),
-               ("configure " + k.name).c_str());
+    check_cuda(matrix_config(sh, t, m, n, sms, &a, &grid), ("configure " + k.name).c_str());
+  if (peers && peers->nranks > 1 && sh.ncol > 0) {
+    if (n > peers->n_cap) throw Fault("kernel " + k.name + ": peer group capacity below n");
+    a.peer.nranks = peers->nranks;
+    a.peer.rank = peers->rank;
+    a.peer.n_cap = peers->n_cap;
+    for (int r = 0; r < peers->nranks; ++r) {
+      if (!peers->peer_inbox[r] || !peers->peer_flags[r] || !peers->peer_outbox[r])
+        throw Fault("kernel " + k.name + ": peer " + std::to_string(r) + " not connected");
+      a.peer.inbox[r] = peers->peer_inbox[r];
+      a.peer.outbox[r] = peers->peer_outbox[r];
+      a.peer.flags[r] = peers->peer_flags[r];
+    }
+    a.peer.epoch = ++peers->epoch;
+    a.peer.spin_limit = 20000000000LL;  // ~10 s: trap instead of hanging the GPU
+  }
   const size_t acc = matrix_acc_bytes(t);
   const size_t colb = acc * (size_t)sh.ncol * (size_t)a.RB * (size_t)n;
   const size_t rowb = (a.CB > 1) ? acc * (size_t)sh.nrow * (size_t)a.CB * (size_t)m : 0;
@@ -267,12 +289,12 @@ BufMap complete_bindings(const NativePlan& plan, const BufMap& bufs, Workspace& 
 }
 
 void run_kernel(const NativePlan& plan, int k, const BufMap& bufs, const ScalarMap& scalars,
-                cudaStream_t stream, Workspace& ws) {
+                cudaStream_t stream, Workspace& ws, PeerGroup* peers) {
   if (k < 0 || k >= (int)plan.kernels.size()) throw Invalid("kernel index out of range");
   const NativeKernel& kern = plan.kernels[k];
   std::lock_guard<std::mutex> lk(ws.mu);
   if (kern.kind == NativeKernel::Kind::Stream) run_stream(kern, bufs, scalars, stream, ws);
-  else run_matrix(kern, bufs, scalars, stream, ws);
+  else run_matrix(kern, bufs, scalars, stream, ws, peers);
 }
 
 }  // namespace mapfuse::b200

@@ -38,6 +38,22 @@ struct EngineOptions {
   int stream_unroll = 0;       // 0 = default (by input count), else 2 / 4 / 8
   int stream_ctas_per_sm = 4;
   int tma = -1;  // matrix kernels: -1 auto (by shape), 1 = TMA ring, 0 = register-fed
+  int max_sms = 0;  // > 0: cap the SMs a matrix kernel's grid is sized for
+};
+
+// A row-sharding group's in-kernel exchange buffers (see PeerLinks).
+struct PeerGroup {
+  int nranks = 1, rank = 0;
+  int64_t n_cap = 0;
+  float* inbox = nullptr;     // local: [2][P][n_cap]
+  float* outbox = nullptr;    // local: [2][n_cap]
+  unsigned* flags = nullptr;  // local: 64 counters, zeroed
+  float* peer_inbox[8] = {};
+  float* peer_outbox[8] = {};
+  unsigned* peer_flags[8] = {};
+  std::vector<void*> opened;  // IPC mappings to close
+  unsigned epoch = 0;
+  ~PeerGroup();
 };
 EngineOptions& options();
 
@@ -62,7 +78,7 @@ class Workspace {
 
 // Launches plan.kernels[k]; throws Fault / Invalid.
 void run_kernel(const NativePlan& plan, int k, const BufMap& bufs, const ScalarMap& scalars,
-                cudaStream_t stream, Workspace& ws);
+                cudaStream_t stream, Workspace& ws, PeerGroup* peers = nullptr);
 // Binds any plan intermediates the caller left unbound (workspace-backed).
 BufMap complete_bindings(const NativePlan& plan, const BufMap& bufs, Workspace& ws);
 

@@ -28,6 +28,21 @@ struct StreamArgs {
   unsigned* ticket = nullptr;             // last-CTA-done counter (self-resetting)
 };
 
+// In-kernel cross-GPU reduction of column outputs (row-sharded runs).
+// Every rank owns a group-allocated inbox [2][P][n], outbox [2][n] and two
+// arrival counters; peers' copies are mapped into this process (CUDA IPC over
+// NVLink, or plain pointers for virtual ranks sharing one GPU).
+constexpr int kMaxRanks = 8;
+struct PeerLinks {
+  int nranks = 1, rank = 0;
+  float* inbox[kMaxRanks] = {};
+  float* outbox[kMaxRanks] = {};
+  unsigned* flags[kMaxRanks] = {};
+  unsigned epoch = 0;               // launches so far in this group (1-based)
+  long long n_cap = 0;              // inbox / outbox row capacity (floats)
+  long long spin_limit = 0;         // clock64 cycles before trapping (deadlock guard)
+};
+
 // Depth-2 single-pass matrix kernel (see mf_kernels.cu for the mapping).
 struct MatrixArgs {
   long long m = 0, n = 0, ld = 0;   // rows, cols, row stride (floats)
@@ -45,6 +60,7 @@ struct MatrixArgs {
   void* rowpart = nullptr;          // [NROW][CB][m] accumulator type
   unsigned* bar = nullptr;          // grid barrier {count, generation}
   int CB = 1, RB = 1, tiles = 1;    // column chunks, row bands, CB*RB
+  PeerLinks peer;                   // nranks > 1: fused cross-GPU column reduction
 };
 
 // Shape of a matrix-kernel instantiation.

@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) matrix_tma_kernel(MatrixArgs a
     const bool need_rows = (NROW > 0) && a.CB > 1;
     if (NCOL == 0 && !need_rows) return;
     grid_barrier(a.bar);
-    finalize<NROW, NCOL, ACC>(a, tid, kTmaThreads);
+    finalize_any<NROW, NCOL, ACC>(a, tid, kTmaThreads);
   }
 }
 

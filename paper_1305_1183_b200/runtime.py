@@ -63,6 +63,8 @@ EXPORTS = [
     "mf_plan_num_kernels", "mf_plan_describe", "mf_plan_kernel_text",
     "mf_plan_kernel_column_outputs", "mf_launch", "mf_launch_kernel", "mf_launch_host",
     "mf_generate", "mf_set_option", "mf_get_option", "mf_last_error", "mf_version",
+    "mf_peer_group_create", "mf_peer_group_handle", "mf_peer_group_open",
+    "mf_peer_group_connect_local", "mf_peer_group_destroy", "mf_launch_kernel_peers",
 ]
 
 
@@ -96,6 +98,13 @@ def lib() -> C.CDLL:
                                   C.c_int64, C.c_int64, C.c_void_p]
         L.mf_set_option.argtypes = [C.c_char_p, C.c_int]
         L.mf_get_option.argtypes = [C.c_char_p]
+        L.mf_peer_group_create.argtypes = [C.c_int, C.c_int, C.c_int64, P(C.c_void_p)]
+        L.mf_peer_group_handle.argtypes = [C.c_void_p, C.c_void_p, C.c_int]
+        L.mf_peer_group_open.argtypes = [C.c_void_p, C.c_int, C.c_char_p, C.c_int]
+        L.mf_peer_group_connect_local.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
+        L.mf_peer_group_destroy.argtypes = [C.c_void_p]
+        L.mf_launch_kernel_peers.argtypes = [C.c_void_p, C.c_int, C.c_void_p, P(MfBuffer), C.c_int,
+                                             P(MfScalar), C.c_int, C.c_void_p, P(MfStats)]
         L.mf_last_error.restype = C.c_char_p
         L.mf_version.restype = C.c_char_p
         _lib = L
@@ -232,6 +241,16 @@ class Plan:
                                       C.c_void_p(_stream_ptr(stream)), C.byref(st)))
         return st.as_dict()
 
+    def launch_kernel_peers(self, k: int, group: "PeerGroup", buffers: Mapping[str, object],
+                            scalars: Mapping[str, float] = {}, stream=None) -> Dict[str, float]:
+        """Kernel k with its column reductions finished in-kernel across the
+        group's ranks (reduce-scatter + all-gather over peer memory)."""
+        arr, nb, sc, ns, _keep = self._args(buffers, scalars, host=False)
+        st = MfStats()
+        _check(lib().mf_launch_kernel_peers(self.h, k, group.h, arr, nb, sc, ns,
+                                            C.c_void_p(_stream_ptr(stream)), C.byref(st)))
+        return st.as_dict()
+
     def launch_host(self, buffers: Mapping[str, object],
                     scalars: Mapping[str, float] = {}) -> Dict[str, float]:
         """vm::launch's contract: host arrays in, outputs written back in place."""
@@ -239,6 +258,36 @@ class Plan:
         st = MfStats()
         _check(lib().mf_launch_host(self.h, arr, nb, sc, ns, C.byref(st)))
         return st.as_dict()
+
+
+class PeerGroup:
+    """In-kernel exchange buffers of one rank of a row-sharding group."""
+
+    def __init__(self, nranks: int, rank: int, n_capacity: int):
+        h = C.c_void_p()
+        _check(lib().mf_peer_group_create(nranks, rank, n_capacity, C.byref(h)))
+        self.h, self.nranks, self.rank = h, nranks, rank
+
+    def __del__(self):
+        try:
+            if self.h and _lib is not None:
+                _lib.mf_peer_group_destroy(self.h)
+        except Exception:
+            pass
+
+    def handle(self) -> bytes:
+        need = lib().mf_peer_group_handle(self.h, None, 0)
+        buf = C.create_string_buffer(need)
+        got = lib().mf_peer_group_handle(self.h, buf, need)
+        if got != need:
+            raise MapfuseError(got, lib().mf_last_error().decode())
+        return buf.raw
+
+    def open(self, peer: int, handle: bytes) -> None:
+        _check(lib().mf_peer_group_open(self.h, peer, handle, len(handle)))
+
+    def connect_local(self, peer: int, other: "PeerGroup") -> None:
+        _check(lib().mf_peer_group_connect_local(self.h, peer, other.h))
 
 
 def generate(t, seed: int, row0: int = 0, ncols_global: Optional[int] = None, stream=None) -> None:

@@ -38,7 +38,8 @@ class ShardedPlan:
     def __init__(self, sequence: Optional[str] = None, rows: int = 0, cols: int = 0,
                  mode: str = "fused", script: Optional[str] = None, world: Optional[int] = None,
                  rank: Optional[int] = None, group=None,
-                 executor: Optional[Callable] = None, allreduce: Optional[Callable] = None):
+                 executor: Optional[Callable] = None, allreduce: Optional[Callable] = None,
+                 collective: str = "nccl", peer_group=None):
         import torch.distributed as dist
         if world is None:
             world = dist.get_world_size(group) if dist.is_initialized() else 1
@@ -66,6 +67,30 @@ class ShardedPlan:
         self.collective_after = [self.plan.column_outputs(k) for k in range(self.plan.num_kernels)]
         self.executor = executor
         self.allreduce = allreduce
+        # collective = "fused": column reductions of matrix kernels finish
+        # in-kernel over peer memory (mf_launch_kernel_peers); only dot
+        # scalars still go through the process group.
+        self.collective = collective
+        self.peers = peer_group
+        self.fused_names = [[] for _ in range(self.plan.num_kernels)]
+        if collective == "fused":
+            for k, kern in enumerate(self.desc["kernels"]):
+                if kern["kind"] == "matrix":
+                    self.fused_names[k] = list(self.collective_after[k])
+            if self.peers is None and world > 1 and executor is None:
+                self.peers = self._connect_peers()
+
+    def _connect_peers(self):
+        """One PeerGroup per rank; IPC handles exchanged over the process group."""
+        import torch.distributed as dist
+        from .runtime import PeerGroup
+        g = PeerGroup(self.world, self.rank, self.cols_g)
+        handles = [None] * self.world
+        dist.all_gather_object(handles, g.handle(), group=self.group)
+        for r, h in enumerate(handles):
+            if r != self.rank:
+                g.open(r, h)
+        return g
 
     # -- partition of one buffer -------------------------------------------------
     def local_slice(self, name: str):
@@ -100,12 +125,19 @@ class ShardedPlan:
         """Runs every kernel on the local shard; all-reduces partial column /
         dot results right after the kernel that produced them."""
         collectives = 0
+        fused = 0
         for k in range(self.plan.num_kernels):
             if self.executor is not None:
                 self.executor(self.desc["kernels"][k], buffers, scalars)
+            elif self.fused_names[k] and self.peers is not None:
+                self.plan.launch_kernel_peers(k, self.peers, buffers, scalars, stream)
+                fused += len(self.fused_names[k])
             else:
                 self.plan.launch_kernel(k, buffers, scalars, stream)
             for name in self.collective_after[k]:
+                if name in self.fused_names[k] and self.peers is not None and self.executor is None:
+                    continue  # reduced inside the kernel
                 self._allreduce(buffers[name])
                 collectives += 1
-        return {"kernels": self.plan.num_kernels, "collectives": collectives}
+        return {"kernels": self.plan.num_kernels, "collectives": collectives,
+                "fused_collectives": fused}

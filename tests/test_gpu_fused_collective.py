@@ -1,0 +1,89 @@
+"""GPU: the in-kernel cross-rank column reduction (fused compute + collective).
+
+This run has one GPU, so P "virtual ranks" share it: each rank is its own
+plan (own workspace, own grid barrier) whose cooperative grid is sized for
+148/P SMs, launched on its own stream so all ranks' kernels are co-resident;
+peer pointers are the other ranks' group buffers (same code path as CUDA-IPC
+mapped NVLink peers).  Every rank must end with the same, correct column
+vector; row outputs stay local.
+"""
+import numpy as np
+import pytest
+
+from gpu_util import TAU
+from oracle import COracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("seq,m,n,P", [("BICGK", 2048, 4096, 2), ("BICGK", 4096, 2048, 4),
+                                       ("ATAX", 1024, 3072, 2), ("GEMVER", 1024, 2048, 2)])
+@pytest.mark.parametrize("tma", [0, 1])
+def test_virtual_ranks_fused_column_reduction(seq, m, n, P, tma):
+    import torch
+    import paper_1305_1183_b200 as mf
+    co = COracle()
+    mf.set_option("max_sms", 148 // P)
+    mf.set_option("tma", tma)
+    try:
+        rng = np.random.default_rng(m + n + P)
+        full_plan = mf.Plan.sequence(seq, m, n, "fused")
+        gd = full_plan.describe()
+        vals = {}
+        for b in gd["buffers"]:
+            if b["role"] == "input":
+                shp = (b["rows"], b["cols"]) if b["rows"] > 1 else (b["cols"],)
+                vals[b["name"]] = rng.uniform(-1, 1, shp).astype(np.float32)
+        sc = {s: 0.5 + 0.25 * i for i, s in enumerate(gd["scalars"])}
+        rows_of = {b["name"]: b for b in gd["buffers"]}
+        mloc = m // P
+        plans = [mf.Plan.sequence(seq, mloc, n, "fused") for _ in range(P)]
+        groups = [mf.PeerGroup(P, r, n) for r in range(P)]
+        for r in range(P):
+            for q in range(P):
+                if q != r:
+                    groups[r].connect_local(q, groups[q])
+        streams = [torch.cuda.Stream() for _ in range(P)]
+        bufs = []
+        for r in range(P):
+            d = {}
+            for b in plans[r].describe()["buffers"]:
+                g = rows_of[b["name"]]
+                shp = (b["rows"], b["cols"]) if b["rows"] > 1 else (b["cols"],)
+                if b["name"] in vals:
+                    v = vals[b["name"]]
+                    if g["rows"] > 1:
+                        v = v[r * mloc:(r + 1) * mloc]
+                    elif g["row_indexed"]:
+                        v = v[r * mloc:(r + 1) * mloc]
+                    d[b["name"]] = torch.from_numpy(np.ascontiguousarray(v)).cuda()
+                else:
+                    d[b["name"]] = torch.full(shp, float("nan"), device="cuda")
+            bufs.append(d)
+        torch.cuda.synchronize()
+        for k in range(plans[0].num_kernels):
+            kind = plans[0].describe()["kernels"][k]["kind"]
+            for r in range(P):
+                with torch.cuda.stream(streams[r]):
+                    if kind == "matrix":
+                        plans[r].launch_kernel_peers(k, groups[r], bufs[r], sc, streams[r])
+                    else:
+                        plans[r].launch_kernel(k, bufs[r], sc, streams[r])
+            torch.cuda.synchronize()
+        want = co.execute(seq, m, n, {**vals, **sc})
+        absvals = {k: (np.abs(v) if isinstance(v, np.ndarray) else v) for k, v in vals.items()}
+        S = co.execute(seq, m, n, {**absvals, **{k: abs(v) for k, v in sc.items()}})
+        for name, w in want.items():
+            g = rows_of[name]
+            if g["rows"] > 1 or g["row_indexed"]:
+                got = np.concatenate([bufs[r][name].cpu().numpy() for r in range(P)], axis=0)
+            else:
+                got = bufs[0][name].cpu().numpy()
+                for r in range(1, P):  # replicated outputs: identical on every rank
+                    assert np.array_equal(got, bufs[r][name].cpu().numpy()), name
+            err = np.abs(got.astype(np.float64).ravel() - w.astype(np.float64).ravel())
+            lim = TAU * S[name].astype(np.float64).ravel() + np.spacing(np.abs(w.ravel()))
+            assert np.all(err <= lim), (name, float(np.max(err / lim)))
+    finally:
+        mf.set_option("max_sms", 0)
+        mf.set_option("tma", -1)

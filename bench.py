@@ -308,7 +308,7 @@ def run_sharded(args, torch, mf, rank, world, seq):
     column partials (NCCL) after the kernel that produced them."""
     from paper_1305_1183_b200.sharding import ShardedPlan
     m = n = args.n_matrix
-    sp = ShardedPlan(seq, m, n, "fused")
+    sp = ShardedPlan(seq, m, n, "fused", collective=args.collective)
     d = sp.desc
     bufs = {}
     for i, b in enumerate(d["buffers"]):
@@ -401,6 +401,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--workload", default="blas1", choices=["blas1", "bicgk-sharded", "atax-sharded"])
     ap.add_argument("--n-matrix", type=int, default=131072)
+    ap.add_argument("--collective", default="fused", choices=["fused", "nccl"],
+                    help="sharded workloads: in-kernel peer-memory reduction or NCCL all-reduce")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     rank, local, world = env_rank()
@@ -443,8 +445,11 @@ def main():
                     "steps": args.steps, "warmup": args.warmup,
                     "ms_per_step": round(r["ms_per_step"], 4), "higher_is_better": True,
                     "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                    "config": {"workload": "%s fp32 %dx%d row-sharded over %d GPU(s), NCCL all-reduce "
-                                           "of the column partials" % (seq, args.n_matrix, args.n_matrix, world),
+                    "config": {"workload": "%s fp32 %dx%d row-sharded over %d GPU(s), column partials "
+                                           "reduced %s" % (seq, args.n_matrix, args.n_matrix, world,
+                                                           "in-kernel over NVLink peer memory"
+                                                           if args.collective == "fused" else
+                                                           "by NCCL all-reduce"),
                                "rows_per_rank": r["rows_per_rank"], "kernels": r["kernels"],
                                "collectives_per_step": r["collectives_per_step"],
                                "l2": "inputs (64 GiB) >> L2; no flush"},

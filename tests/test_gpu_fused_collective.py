@@ -60,6 +60,11 @@ def test_virtual_ranks_fused_column_reduction(seq, m, n, P, tma):
                 else:
                     d[b["name"]] = torch.full(shp, float("nan"), device="cuda")
             bufs.append(d)
+        # size every rank's workspace first: a workspace reallocation calls
+        # cudaFree, which synchronizes the whole device -- with virtual ranks
+        # sharing one GPU that would serialize ranks that must be co-resident
+        for r in range(P):
+            plans[r].launch(bufs[r], sc)
         torch.cuda.synchronize()
         for k in range(plans[0].num_kernels):
             kind = plans[0].describe()["kernels"][k]["kind"]

@@ -129,5 +129,15 @@ uint64_t count_combinations(const script::Script& s, const script::DataDependenc
 // mode: 0 fused (planner's choice), 1 unfused (one kernel per call).
 b200::NativePlan compile(const std::string& script_text, const lib::Library& L, int rows, int cols,
                          int mode);
+// The rank-th best combination (0 = the selector's choice) -- empirical
+// top-k search (SPEC.md:677-693 cmd_search) times these on the device.
+b200::NativePlan compile_ranked(const std::string& script_text, const lib::Library& L, int rows,
+                                int cols, int mode, int rank);
+int64_t count_covers(const std::string& script_text, const lib::Library& L, int rows, int cols);
+
+// Plan files: a compiled plan as re-runnable text -- header,
+// buffer table, and each kernel's KernelIR (re-lowered on load).
+std::string save_plan(const b200::NativePlan& p);
+b200::NativePlan load_plan(const std::string& text);
 
 }  // namespace mapfuse::plan

@@ -85,6 +85,20 @@ int mf_compile(const char* script_text, const char* manifest, int rows, int cols
  * (blas::build_sequence, proj/include/mapfuse/blas.hpp:27). */
 int mf_compile_sequence(const char* sequence, int rows, int cols, int mode, mf_plan** out);
 
+/* Empirical search support: the rank-th best combination
+ * (0 = the selector's choice) and the number of combinations. */
+int mf_compile_ranked(const char* script_text, const char* manifest, int rows, int cols, int mode,
+                      int rank, mf_plan** out);
+int64_t mf_count_combinations(const char* script_text, const char* manifest, int rows, int cols);
+/* The shipped script text of a Table-1 sequence (blas::build_sequence). */
+int mf_sequence_script(const char* name, char* buf, int cap);
+/* Cost-model prediction of the plan's time in microseconds. */
+double mf_plan_predicted_us(const mf_plan* plan);
+/* Plan files: compile once, run many.  save: size convention as
+ * mf_plan_describe; load re-lowers every KernelIR in the file. */
+int mf_plan_save(const mf_plan* plan, char* buf, int cap);
+int mf_plan_load(const char* text, mf_plan** out);
+
 /* One kernel given as KernelIR text (kernel::emit_pseudo_source format,
  * proj/src/kernel.cpp:33-65) -> single-kernel plan.  This is the exact
  * vm::launch(KernelIR, ...) boundary.  rows/cols: the padded domain. */

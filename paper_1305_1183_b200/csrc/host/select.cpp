@@ -181,25 +181,14 @@ uint64_t count_combinations(const script::Script& s, const script::DataDependenc
   return n;
 }
 
-b200::NativePlan compile(const std::string& script_text, const lib::Library& L, int rows, int cols,
-                         int mode) {
-  script::Script s = script::parse_script(script_text);
-  script::DataDependencyGraph g = script::build_dependency_graph(s, L);
-  auto diags = script::validate(s, g, L);
-  if (!diags.empty()) {
-    std::string msg = "script validation failed:";
-    for (const auto& d : diags) msg += "\n  [" + d.rule + "] " + d.where + ": " + d.message;
-    throw std::invalid_argument(msg);
-  }
-  const int m = (rows + 31) / 32 * 32, n = (cols + 31) / 32 * 32;
-  const CostModel cm = CostModel::defaults();
-  auto combos = enumerate_combinations(s, g, L, Sizes{m, n}, cm, 1, mode == 0);
-  if (combos.empty()) throw std::invalid_argument("no executable combination for this script");
-  const Combination& best = combos.front();
+namespace {
 
+b200::NativePlan plan_from_combination(const script::Script& s, const lib::Library& L, int m, int n,
+                                       const Combination& best) {
   b200::NativePlan plan;
   plan.rows = m;
   plan.cols = n;
+  plan.predicted_us = best.predicted_us;
   for (size_t i = 0; i < best.kernels.size(); ++i) {
     b200::NativeKernel nk = best.kernels[i].native;
     std::string label = "k" + std::to_string(i) + "[";
@@ -217,11 +206,9 @@ b200::NativePlan compile(const std::string& script_text, const lib::Library& L, 
   for (const auto& [name, spec] : s.declarations) {
     const bool input = std::find(s.inputs.begin(), s.inputs.end(), name) != s.inputs.end();
     const bool output = std::find(s.outputs.begin(), s.outputs.end(), name) != s.outputs.end();
-    if (spec.kind == lib::ElemKind::Scalar) {
-      if (input) {
-        plan.scalars.push_back(name);
-        continue;
-      }
+    if (spec.kind == lib::ElemKind::Scalar && input) {
+      plan.scalars.push_back(name);
+      continue;
     }
     bool used = input || output;
     for (const auto& k : plan.kernels) {
@@ -240,6 +227,51 @@ b200::NativePlan compile(const std::string& script_text, const lib::Library& L, 
     plan.buffers.push_back(b);
   }
   return plan;
+}
+
+struct Parsed {
+  script::Script s;
+  script::DataDependencyGraph g;
+};
+
+Parsed parse_checked(const std::string& script_text, const lib::Library& L) {
+  Parsed p;
+  p.s = script::parse_script(script_text);
+  p.g = script::build_dependency_graph(p.s, L);
+  auto diags = script::validate(p.s, p.g, L);
+  if (!diags.empty()) {
+    std::string msg = "script validation failed:";
+    for (const auto& d : diags) msg += "\n  [" + d.rule + "] " + d.where + ": " + d.message;
+    throw std::invalid_argument(msg);
+  }
+  return p;
+}
+
+}  // namespace
+
+b200::NativePlan compile(const std::string& script_text, const lib::Library& L, int rows, int cols,
+                         int mode) {
+  return compile_ranked(script_text, L, rows, cols, mode, 0);
+}
+
+b200::NativePlan compile_ranked(const std::string& script_text, const lib::Library& L, int rows,
+                                int cols, int mode, int rank) {
+  Parsed p = parse_checked(script_text, L);
+  const int m = (rows + 31) / 32 * 32, n = (cols + 31) / 32 * 32;
+  const CostModel cm = CostModel::defaults();
+  auto combos = enumerate_combinations(p.s, p.g, L, Sizes{m, n}, cm, rank + 1, mode == 0);
+  if (combos.empty()) throw std::invalid_argument("no executable combination for this script");
+  if (rank < 0 || rank >= static_cast<int>(combos.size()))
+    throw std::invalid_argument("combination rank " + std::to_string(rank) + " out of range (" +
+                                std::to_string(combos.size()) + " combinations)");
+  return plan_from_combination(p.s, L, m, n, combos[static_cast<size_t>(rank)]);
+}
+
+int64_t count_covers(const std::string& script_text, const lib::Library& L, int rows, int cols) {
+  Parsed p = parse_checked(script_text, L);
+  const int m = (rows + 31) / 32 * 32, n = (cols + 31) / 32 * 32;
+  return static_cast<int64_t>(
+      enumerate_combinations(p.s, p.g, L, Sizes{m, n}, CostModel::defaults(), 0).size());
 }
 
 }  // namespace mapfuse::plan

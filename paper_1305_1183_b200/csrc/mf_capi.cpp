@@ -204,6 +204,55 @@ int mf_compile(const char* script_text, const char* manifest, int rows, int cols
   });
 }
 
+int mf_compile_ranked(const char* script_text, const char* manifest, int rows, int cols, int mode,
+                      int rank, mf_plan** out) {
+  return guarded([&] {
+    if (!script_text || !out) throw Invalid("null argument");
+    auto p = std::make_unique<mf_plan>();
+    p->plan = compile_script_ranked(script_text, manifest ? std::string(manifest) : std::string(),
+                                    rows, cols, mode, rank);
+    *out = p.release();
+  });
+}
+
+int64_t mf_count_combinations(const char* script_text, const char* manifest, int rows, int cols) {
+  int64_t n = -1;
+  const int rc = guarded([&] {
+    if (!script_text) throw Invalid("null argument");
+    n = count_script_covers(script_text, manifest ? std::string(manifest) : std::string(), rows, cols);
+  });
+  return rc == MF_OK ? n : -1;
+}
+
+int mf_sequence_script(const char* name, char* buf, int cap) {
+  std::string s;
+  const int rc = guarded([&] {
+    if (!name) throw Invalid("null name");
+    s = sequence_script_text(name);
+  });
+  if (rc != MF_OK) return -1;
+  return copy_out(s, buf, cap);
+}
+
+double mf_plan_predicted_us(const mf_plan* plan) { return plan ? plan->plan.predicted_us : -1.0; }
+
+int mf_plan_save(const mf_plan* plan, char* buf, int cap) {
+  if (!plan) return -1;
+  std::string s;
+  const int rc = guarded([&] { s = save_plan_text(plan->plan); });
+  if (rc != MF_OK) return -1;
+  return copy_out(s, buf, cap);
+}
+
+int mf_plan_load(const char* text, mf_plan** out) {
+  return guarded([&] {
+    if (!text || !out) throw Invalid("null argument");
+    auto p = std::make_unique<mf_plan>();
+    p->plan = load_plan_text(text);
+    *out = p.release();
+  });
+}
+
 int mf_compile_sequence(const char* sequence, int rows, int cols, int mode, mf_plan** out) {
   return guarded([&] {
     if (!sequence || !out) throw Invalid("null argument");

@@ -36,6 +36,49 @@ NativePlan compile_script(const std::string& script_text, const std::string& man
   });
 }
 
+NativePlan compile_script_ranked(const std::string& script_text, const std::string& manifest,
+                                 int rows, int cols, int mode, int rank) {
+  return as_invalid([&] {
+    if (mode != MF_MODE_FUSED && mode != MF_MODE_UNFUSED) throw Invalid("unknown planner mode");
+    if (manifest.empty())
+      return plan::compile_ranked(script_text, blas::default_library(), rows, cols, mode, rank);
+    const lib::Library L = lib::load_library(manifest);
+    return plan::compile_ranked(script_text, L, rows, cols, mode, rank);
+  });
+}
+
+int64_t count_script_covers(const std::string& script_text, const std::string& manifest, int rows,
+                            int cols) {
+  int64_t n = 0;
+  as_invalid([&] {
+    if (manifest.empty()) n = plan::count_covers(script_text, blas::default_library(), rows, cols);
+    else n = plan::count_covers(script_text, lib::load_library(manifest), rows, cols);
+    return NativePlan{};
+  });
+  return n;
+}
+
+std::string save_plan_text(const NativePlan& p) {
+  std::string s;
+  as_invalid([&] {
+    s = plan::save_plan(p);
+    return NativePlan{};
+  });
+  return s;
+}
+
+std::string sequence_script_text(const std::string& name) {
+  try {
+    return blas::build_sequence(name).script_text;
+  } catch (const std::exception& e) {
+    throw Invalid(e.what());
+  }
+}
+
+NativePlan load_plan_text(const std::string& text) {
+  return as_invalid([&] { return plan::load_plan(text); });
+}
+
 NativePlan compile_sequence(const std::string& sequence, int rows, int cols, int mode) {
   return as_invalid([&] {
     const blas::SequenceCase c = blas::build_sequence(sequence);

@@ -107,6 +107,7 @@ struct NativePlan {
   std::vector<BufferSpec> buffers;
   std::vector<std::string> scalars;   // script scalar names the plan needs
   std::vector<std::string> kernel_ir;  // emitted KernelIR text per kernel (may be empty)
+  double predicted_us = 0.0;           // cost-model prediction (0 if not planned)
   const BufferSpec* find(const std::string& n) const {
     for (const auto& b : buffers)
       if (b.name == n) return &b;

@@ -65,6 +65,8 @@ EXPORTS = [
     "mf_generate", "mf_set_option", "mf_get_option", "mf_last_error", "mf_version",
     "mf_peer_group_create", "mf_peer_group_handle", "mf_peer_group_open",
     "mf_peer_group_connect_local", "mf_peer_group_destroy", "mf_launch_kernel_peers",
+    "mf_compile_ranked", "mf_count_combinations", "mf_plan_predicted_us", "mf_plan_save",
+    "mf_plan_load", "mf_sequence_script",
 ]
 
 
@@ -105,6 +107,15 @@ def lib() -> C.CDLL:
         L.mf_peer_group_destroy.argtypes = [C.c_void_p]
         L.mf_launch_kernel_peers.argtypes = [C.c_void_p, C.c_int, C.c_void_p, P(MfBuffer), C.c_int,
                                              P(MfScalar), C.c_int, C.c_void_p, P(MfStats)]
+        L.mf_compile_ranked.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_int,
+                                        P(C.c_void_p)]
+        L.mf_count_combinations.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_int]
+        L.mf_count_combinations.restype = C.c_int64
+        L.mf_plan_predicted_us.argtypes = [C.c_void_p]
+        L.mf_plan_predicted_us.restype = C.c_double
+        L.mf_plan_save.argtypes = [C.c_void_p, C.c_char_p, C.c_int]
+        L.mf_plan_load.argtypes = [C.c_char_p, P(C.c_void_p)]
+        L.mf_sequence_script.argtypes = [C.c_char_p, C.c_char_p, C.c_int]
         L.mf_last_error.restype = C.c_char_p
         L.mf_version.restype = C.c_char_p
         _lib = L
@@ -177,6 +188,38 @@ class Plan:
         h = C.c_void_p()
         _check(lib().mf_compile_sequence(name.encode(), rows, cols, MODES[mode], C.byref(h)))
         return cls(h.value)
+
+    @classmethod
+    def compile_ranked(cls, script: str, rows: int, cols: int, rank: int, mode: str = "fused",
+                       manifest: Optional[str] = None) -> "Plan":
+        """The rank-th best combination the selector enumerates (0 = its choice)."""
+        h = C.c_void_p()
+        _check(lib().mf_compile_ranked(script.encode(), manifest.encode() if manifest else None,
+                                       rows, cols, MODES[mode], rank, C.byref(h)))
+        return cls(h.value)
+
+    @staticmethod
+    def count_combinations(script: str, rows: int, cols: int,
+                           manifest: Optional[str] = None) -> int:
+        n = lib().mf_count_combinations(script.encode(), manifest.encode() if manifest else None,
+                                        rows, cols)
+        if n < 0:
+            raise ParseError(MF_ERR_INVALID, lib().mf_last_error().decode())
+        return int(n)
+
+    @classmethod
+    def load(cls, text: str) -> "Plan":
+        """Re-runnable plan file (see save())."""
+        h = C.c_void_p()
+        _check(lib().mf_plan_load(text.encode(), C.byref(h)))
+        return cls(h.value)
+
+    def save(self) -> str:
+        return _string(lib().mf_plan_save, self.h)
+
+    @property
+    def predicted_us(self) -> float:
+        return float(lib().mf_plan_predicted_us(self.h))
 
     @classmethod
     def from_kernel_text(cls, text: str, rows: int, cols: int) -> "Plan":
@@ -296,6 +339,16 @@ def generate(t, seed: int, row0: int = 0, ncols_global: Optional[int] = None, st
     _check(lib().mf_generate(C.c_void_p(t.data_ptr()), r, c, c, seed, row0,
                              ncols_global if ncols_global is not None else c,
                              C.c_void_p(_stream_ptr(stream))))
+
+
+def sequence_script(name: str) -> str:
+    """The shipped script text of a Table-1 sequence."""
+    need = lib().mf_sequence_script(name.encode(), None, 0)
+    if need < 0:
+        raise ParseError(MF_ERR_INVALID, lib().mf_last_error().decode())
+    buf = C.create_string_buffer(need)
+    lib().mf_sequence_script(name.encode(), buf, need)
+    return buf.value.decode()
 
 
 def set_option(key: str, value: int) -> None:

@@ -110,3 +110,48 @@ def test_user_manifest_function_gets_a_kernel():
                         "o = axpby3(k, a, b, c);\nreturn o;\n", 1, 4096, manifest=text)
     k = p.describe()["kernels"][0]
     assert k["kind"] == "stream" and k["shape"]["inputs"] == 3
+
+
+# -- empirical-search support and plan files -------------
+def test_ranked_combinations_and_counts():
+    text = mf.runtime.sequence_script("GEMVER")
+    assert mf.Plan.count_combinations(text, 256, 256) == 2
+    best = mf.Plan.compile_ranked(text, 256, 256, 0)
+    second = mf.Plan.compile_ranked(text, 256, 256, 1)
+    assert best.num_kernels == 3 and second.num_kernels == 4
+    assert best.predicted_us <= second.predicted_us
+    with pytest.raises(mf.ParseError, match="out of range"):
+        mf.Plan.compile_ranked(text, 256, 256, 2)
+    assert mf.Plan.count_combinations(mf.runtime.sequence_script("ATAX"), 256, 256) == 1
+    assert mf.Plan.count_combinations(mf.runtime.sequence_script("BICGK"), 256, 256) == 2
+
+
+@pytest.mark.parametrize("seq", SEQS)
+def test_plan_file_round_trip(seq):
+    p = mf.Plan.sequence(seq, 96, 160, "fused")
+    text = p.save()
+    assert text.startswith("mapfuse-plan 1\n")
+    q = mf.Plan.load(text)
+    assert q.describe() == p.describe()
+    assert q.save() == text
+
+
+def test_plan_file_errors():
+    with pytest.raises(mf.ParseError, match="not a mapfuse plan file"):
+        mf.Plan.load("hello\n")
+    good = mf.Plan.sequence("VADD", 1, 64).save()
+    with pytest.raises(mf.ParseError, match="not terminated"):
+        mf.Plan.load(good.replace("\nend\n", "\n"))
+
+
+def test_cli_compile_and_usage_errors(tmp_path):
+    from paper_1305_1183_b200 import cli
+    out = tmp_path / "bicgk.mfp"
+    assert cli.main(["compile", "--sequence", "BICGK", "--rows", "512", "--cols", "512",
+                     "-o", str(out), "--emit-source", str(tmp_path / "src")]) == 0
+    assert mf.Plan.load(out.read_text()).num_kernels == 1
+    assert (tmp_path / "src" / "kernel0.kir").read_text().startswith("kernel ")
+    assert cli.main(["compile", "--sequence", "NOPE", "-o", str(out)]) == 2
+    bad = tmp_path / "bad.mfs"
+    bad.write_text("subvector32 x;\ninput x;\nreturn q;\n")
+    assert cli.main(["compile", "--script", str(bad), "-o", str(out)]) == 2

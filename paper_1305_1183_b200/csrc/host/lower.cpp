@@ -26,9 +26,8 @@ namespace mapfuse::plan {
 using b200::Coef;
 
 bool stream_template_exists(int nin, int nout, bool dot) {
-  if (nin < 1 || nin > 4 || nout < 0 || nout > 2) return false;
-  if (!dot) return nout >= 1 && !(nin == 1 && nout == 2);
-  return (nout == 0 && (nin == 2 || nin == 3)) || (nout == 1 && nin >= 2) || (nout == 2 && nin == 4);
+  // every (inputs 1..4) x (stored outputs 0..2) x (dot) with something to write
+  return nin >= 1 && nin <= 4 && nout >= 0 && nout <= 2 && (nout > 0 || dot);
 }
 
 bool matrix_template_exists(int nmat, int nrank, int store, int nrow, int ncol) {

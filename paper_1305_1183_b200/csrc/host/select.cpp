@@ -244,6 +244,23 @@ Parsed parse_checked(const std::string& script_text, const lib::Library& L) {
     for (const auto& d : diags) msg += "\n  [" + d.rule + "] " + d.where + ": " + d.message;
     throw std::invalid_argument(msg);
   }
+  // Dead-call elimination: a call none of whose results is returned or
+  // (transitively) consumed has no observable effect; it is not planned.
+  // Call ids are kept, so graph edges and kernel labels stay stable.
+  std::set<std::string> needed(p.s.outputs.begin(), p.s.outputs.end());
+  std::vector<script::CallStatement> live;
+  for (auto it = p.s.calls.rbegin(); it != p.s.calls.rend(); ++it) {
+    const bool used = std::any_of(it->results.begin(), it->results.end(),
+                                  [&](const std::string& r) { return needed.count(r) > 0; });
+    if (!used) continue;
+    for (const auto& a : it->arguments) needed.insert(a);
+    live.push_back(*it);
+  }
+  if (live.size() != p.s.calls.size()) {
+    std::reverse(live.begin(), live.end());
+    p.s.calls = std::move(live);
+    p.g = script::build_dependency_graph(p.s, L);
+  }
   return p;
 }
 

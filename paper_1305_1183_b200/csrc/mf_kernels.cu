@@ -355,18 +355,25 @@ cudaError_t launch_stream(int nin, int nout, bool dot, const StreamArgs& a, int 
                           cudaStream_t s) {
 #define MF_STREAM_CASE(I, O, D) \
   if (nin == I && nout == O && dot == D) return go_stream<I, O, D>(a, grid, unroll, s);
+  MF_STREAM_CASE(1, 0, true)
   MF_STREAM_CASE(1, 1, false)
-  MF_STREAM_CASE(2, 1, false)
-  MF_STREAM_CASE(3, 1, false)
-  MF_STREAM_CASE(4, 1, false)
-  MF_STREAM_CASE(2, 2, false)
-  MF_STREAM_CASE(3, 2, false)
-  MF_STREAM_CASE(4, 2, false)
+  MF_STREAM_CASE(1, 1, true)
+  MF_STREAM_CASE(1, 2, false)
+  MF_STREAM_CASE(1, 2, true)
   MF_STREAM_CASE(2, 0, true)
-  MF_STREAM_CASE(3, 0, true)
+  MF_STREAM_CASE(2, 1, false)
   MF_STREAM_CASE(2, 1, true)
+  MF_STREAM_CASE(2, 2, false)
+  MF_STREAM_CASE(2, 2, true)
+  MF_STREAM_CASE(3, 0, true)
+  MF_STREAM_CASE(3, 1, false)
   MF_STREAM_CASE(3, 1, true)
+  MF_STREAM_CASE(3, 2, false)
+  MF_STREAM_CASE(3, 2, true)
+  MF_STREAM_CASE(4, 0, true)
+  MF_STREAM_CASE(4, 1, false)
   MF_STREAM_CASE(4, 1, true)
+  MF_STREAM_CASE(4, 2, false)
   MF_STREAM_CASE(4, 2, true)
 #undef MF_STREAM_CASE
   return cudaErrorNotSupported;

@@ -1,0 +1,118 @@
+"""GPU: random straight-line scripts through planner + codegen + lowering.
+
+Scripts mix depth-1 maps (add / scal / waxpby / axpydot_stage), dot, and
+depth-2 calls (sgemv / sgemvs / sgemtv / ger2) over one matrix, so every
+planner path (fusions, shared inputs, unfused chains, mixed-depth plans) is
+exercised on code the Table-1 suite does not cover.  Results are compared
+with the per-call fp64 oracle chain (reference_call semantics,
+proj/src/blas.cpp:275-342) within the tau*S bound.
+"""
+import numpy as np
+import pytest
+
+from gpu_util import TAU
+from oracle import COracle
+
+pytestmark = pytest.mark.gpu
+
+
+def make_script(rng, ncalls):
+    decl_vec, decl_tile, decl_sc = ["xa", "xb", "ra"], ["A"], ["k"]
+    col_vecs, row_vecs = ["xa", "xb"], ["ra"]  # n-length / m-length inputs
+    tiles = ["A"]
+    lines, calls = [], []
+    i = 0
+    for _ in range(ncalls):
+        kind = rng.choice(["add", "scal", "waxpby", "sgemv", "sgemvs", "sgemtv", "dotc", "ger2"])
+        out = "v%d" % i
+        i += 1
+        if kind in ("add", "waxpby"):
+            pool = col_vecs if rng.random() < 0.6 or len(row_vecs) < 2 else row_vecs
+            a, b = rng.choice(pool), rng.choice(pool)
+            if kind == "add":
+                calls.append(("add", [a, b], out))
+            else:
+                calls.append(("waxpby", ["k", a, "2.0", b], out))
+            (col_vecs if pool is col_vecs else row_vecs).append(out)
+        elif kind == "scal":
+            pool = col_vecs if rng.random() < 0.5 else row_vecs
+            calls.append(("scal", ["k", rng.choice(pool)], out))
+            (col_vecs if pool is col_vecs else row_vecs).append(out)
+        elif kind in ("sgemv", "sgemvs"):
+            args = [rng.choice(tiles), rng.choice(col_vecs)]
+            calls.append((kind, (["k"] if kind == "sgemvs" else []) + args, out))
+            row_vecs.append(out)
+        elif kind == "sgemtv":
+            calls.append(("sgemtv", [rng.choice(tiles), rng.choice(row_vecs)], out))
+            col_vecs.append(out)
+        elif kind == "ger2":
+            if len(row_vecs) < 2:
+                continue
+            calls.append(("ger2", [rng.choice(tiles), rng.choice(row_vecs), rng.choice(col_vecs),
+                                   rng.choice(row_vecs), rng.choice(col_vecs)], out))
+            tiles.append(out)
+        else:  # dot over two column vectors -> scalar output
+            calls.append(("dot", [rng.choice(col_vecs), rng.choice(col_vecs)], "s%d" % i))
+    vecs = [c[2] for c in calls if c[0] not in ("ger2", "dot")]
+    outs_t = [c[2] for c in calls if c[0] == "ger2"]
+    outs_s = [c[2] for c in calls if c[0] == "dot"]
+    text = "TILE32x32 %s;\n" % ", ".join(["A"] + outs_t)
+    text += "subvector32 %s;\n" % ", ".join(decl_vec + vecs)
+    text += "float %s;\n" % ", ".join(decl_sc + outs_s)
+    text += "input A, xa, xb, ra, k;\n"
+    for f, args, out in calls:
+        text += "%s = %s(%s);\n" % (out, f, ", ".join(args))
+    returns = [c[2] for c in calls][-3:]
+    text += "return %s;\n" % ", ".join(returns)
+    return text, calls, returns
+
+
+def reference_chain(co, calls, env, m, n):
+    for f, args, out in calls:
+        vals = [float(a) if a[0].isdigit() else (env[a] if a != "k" else env["k"]) for a in args]
+        if f == "dot":
+            env[out] = co.call("dot", m, n, vals)
+        else:
+            env[out] = co.call(f, m, n, vals)
+    return env
+
+
+def abs_chain(co, calls, env, m, n):
+    """S-bound: the same chain on |inputs| (all coefficients positive here)."""
+    envs = {k: (np.abs(v) if isinstance(v, np.ndarray) else abs(v)) for k, v in env.items()}
+    return reference_chain(co, calls, envs, m, n)
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_random_script(seed):
+    import torch
+    import paper_1305_1183_b200 as mf
+    co = COracle()
+    rng = np.random.default_rng(seed)
+    text, calls, returns = make_script(rng, 3 + seed % 5)
+    m, n = 96 + 32 * (seed % 3), 128 + 64 * (seed % 4)
+    plan = mf.Plan.compile(text, m, n, "fused")
+    d = plan.describe()
+    env = {"A": rng.uniform(-1, 1, (m, n)).astype(np.float32),
+           "xa": rng.uniform(-1, 1, n).astype(np.float32),
+           "xb": rng.uniform(-1, 1, n).astype(np.float32),
+           "ra": rng.uniform(-1, 1, m).astype(np.float32), "k": 0.625}
+    bufs = {}
+    for b in d["buffers"]:
+        shp = (b["rows"], b["cols"]) if b["rows"] > 1 else (b["cols"],)
+        v = env.get(b["name"])
+        bufs[b["name"]] = (torch.from_numpy(v).cuda() if isinstance(v, np.ndarray)
+                           else torch.full(shp, float("nan"), device="cuda"))
+    plan.launch(bufs, {"k": env["k"]})
+    torch.cuda.synchronize()
+    want = reference_chain(co, calls, dict(env), m, n)
+    S = abs_chain(co, calls, dict(env), m, n)
+    for name in returns:
+        got = bufs[name].cpu().numpy().astype(np.float64).ravel()
+        w = np.asarray(want[name], np.float64).ravel()
+        s = np.asarray(S[name], np.float64).ravel()
+        # per-call rounding in the reference chain vs fp64-fused maps on the GPU:
+        # allow a few ulps of every intermediate on top of tau*S
+        lim = 4 * TAU * s + 4 * np.spacing(np.abs(w).astype(np.float32)).astype(np.float64)
+        err = np.abs(got - w)
+        assert np.all(err <= lim), (text, name, float(np.max(err / np.maximum(lim, 1e-300))))

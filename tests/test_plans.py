@@ -155,3 +155,16 @@ def test_cli_compile_and_usage_errors(tmp_path):
     bad = tmp_path / "bad.mfs"
     bad.write_text("subvector32 x;\ninput x;\nreturn q;\n")
     assert cli.main(["compile", "--script", str(bad), "-o", str(out)]) == 2
+
+
+def test_random_scripts_always_compile():
+    """Every random mixed-depth script compiles (dead calls eliminated, every
+    live call lowerable onto a template) -- the GPU side runs them in
+    tests/test_gpu_random_scripts.py."""
+    import numpy as np
+    from test_gpu_random_scripts import make_script
+    for seed in range(300):
+        rng = np.random.default_rng(seed)
+        text, calls, ret = make_script(rng, 3 + seed % 5)
+        p = mf.Plan.compile(text, 96 + 32 * (seed % 3), 128 + 64 * (seed % 4))
+        assert p.num_kernels >= 1

@@ -98,9 +98,12 @@ int64_t transfer_savings(const Fusion& f, const script::Script& s,
   std::map<std::string, int> readers;
   for (int id : f.calls) {
     std::set<std::string> seen;
-    for (const auto& a : call_of(s, id).arguments)
-      if (!script::is_numeric_literal(a) && !produced_inside.count(a) && seen.insert(a).second)
-        ++readers[a];
+    for (const auto& a : call_of(s, id).arguments) {
+      if (script::is_numeric_literal(a) || produced_inside.count(a)) continue;
+      auto d = s.declarations.find(a);
+      if (d != s.declarations.end() && d->second.kind == lib::ElemKind::Scalar) continue;
+      if (seen.insert(a).second) ++readers[a];
+    }
   }
   for (const auto& [n, k] : readers)
     if (k > 1) saved += (k - 1) * W(n);
@@ -120,6 +123,9 @@ std::vector<Fusion> enumerate_fusions(const script::Script& s, const script::Dat
     adj[pos(e.consumer)].push_back(pos(e.producer));
   }
   for (const auto& si : g.shared_inputs) {
+    // a shared scalar parameter saves nothing and does not make calls fusible
+    auto d = s.declarations.find(si.name);
+    if (d != s.declarations.end() && d->second.kind == lib::ElemKind::Scalar) continue;
     adj[pos(si.a)].push_back(pos(si.b));
     adj[pos(si.b)].push_back(pos(si.a));
   }
@@ -147,10 +153,13 @@ std::vector<Fusion> enumerate_fusions(const script::Script& s, const script::Dat
     if (fusibility(f.calls, s, g, L)) continue;
     for (const auto& e : g.edges)
       if (contains(f.calls, e.producer) && contains(f.calls, e.consumer)) f.internal.push_back(e);
-    for (const auto& si : g.shared_inputs)
+    for (const auto& si : g.shared_inputs) {
+      auto d = s.declarations.find(si.name);
+      if (d != s.declarations.end() && d->second.kind == lib::ElemKind::Scalar) continue;
       if (contains(f.calls, si.a) && contains(f.calls, si.b) &&
           std::find(f.shared.begin(), f.shared.end(), si.name) == f.shared.end())
         f.shared.push_back(si.name);
+    }
     f.saved_words = transfer_savings(f, s, g, L, sz);
     if (f.saved_words <= 0) continue;
     out.push_back(std::move(f));

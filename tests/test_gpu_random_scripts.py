@@ -93,10 +93,13 @@ def test_random_script(seed):
     m, n = 96 + 32 * (seed % 3), 128 + 64 * (seed % 4)
     plan = mf.Plan.compile(text, m, n, "fused")
     d = plan.describe()
-    env = {"A": rng.uniform(-1, 1, (m, n)).astype(np.float32),
-           "xa": rng.uniform(-1, 1, n).astype(np.float32),
-           "xb": rng.uniform(-1, 1, n).astype(np.float32),
-           "ra": rng.uniform(-1, 1, m).astype(np.float32), "k": 0.625}
+    # input lengths follow the plan's shape inference (a vector no depth-2
+    # call pins down is column-length, as in the reference's make_problem)
+    env = {"k": 0.625}
+    for b in d["buffers"]:
+        if b["role"] == "input":
+            shp = (b["rows"], b["cols"]) if b["rows"] > 1 else (b["cols"],)
+            env[b["name"]] = rng.uniform(-1, 1, shp).astype(np.float32)
     bufs = {}
     for b in d["buffers"]:
         shp = (b["rows"], b["cols"]) if b["rows"] > 1 else (b["cols"],)

@@ -45,13 +45,26 @@ struct ConstraintViolation {
   std::string explanation;
 };
 
+// Planner rule set.  reference: SPEC.md's rules (+ convexity).  row_resident
+// (mode "b200"): additionally a row reduction may feed a column reduction of
+// the SAME matrix inside one kernel when a whole row fits one CTA's ring
+// (cols <= row_resident_max_cols): the CTA completes t_i itself, no global
+// barrier is needed (mf_rowres.cu).  Beyond the paper; off by default.
+struct PlannerOptions {
+  bool row_resident = false;
+  int64_t row_resident_max_cols = 16384;
+  int64_t cols = 0;  // padded problem cols (row-resident feasibility)
+};
+
 std::optional<ConstraintViolation> fusibility(const std::vector<int>& nodes,
                                               const script::Script& s,
                                               const script::DataDependencyGraph& g,
-                                              const lib::Library& L);
+                                              const lib::Library& L,
+                                              const PlannerOptions& opt = {});
 inline bool is_fusible(const std::vector<int>& nodes, const script::Script& s,
-                       const script::DataDependencyGraph& g, const lib::Library& L) {
-  return !fusibility(nodes, s, g, L).has_value();
+                       const script::DataDependencyGraph& g, const lib::Library& L,
+                       const PlannerOptions& opt = {}) {
+  return !fusibility(nodes, s, g, L, opt).has_value();
 }
 
 // Words each script name occupies at the padded size (tiles m*n, vectors m
@@ -66,7 +79,8 @@ int64_t transfer_savings(const Fusion& f, const script::Script& s,
 // All connected (edges + shared inputs), fusible subsets of size 2..max_size
 // with positive savings, sorted by call ids.
 std::vector<Fusion> enumerate_fusions(const script::Script& s, const script::DataDependencyGraph& g,
-                                      const lib::Library& L, Sizes sz, int max_size = 6);
+                                      const lib::Library& L, Sizes sz, int max_size = 6,
+                                      const PlannerOptions& opt = {});
 
 // ---------------------------------------------------------------- codegen
 struct CodegenParams {
@@ -120,13 +134,15 @@ std::vector<Combination> enumerate_combinations(const script::Script& s,
                                                 const script::DataDependencyGraph& g,
                                                 const lib::Library& L, Sizes sz,
                                                 const CostModel& cm, int k,
-                                                bool allow_fusion = true);
+                                                bool allow_fusion = true,
+                                                const PlannerOptions& opt = {});
 uint64_t count_combinations(const script::Script& s, const script::DataDependencyGraph& g,
                             const lib::Library& L, Sizes sz);
 
 // ---------------------------------------------------------------- pipeline
 // parse -> graph -> validate -> plan -> select -> codegen -> lower.
-// mode: 0 fused (planner's choice), 1 unfused (one kernel per call).
+// mode: 0 fused (the paper's rules), 1 unfused (one kernel per call),
+//       2 b200 (fused + row-resident chains, beyond the paper).
 b200::NativePlan compile(const std::string& script_text, const lib::Library& L, int rows, int cols,
                          int mode);
 // The rank-th best combination (0 = the selector's choice) -- empirical

@@ -44,6 +44,7 @@ extern "C" {
 /* Planner modes for mf_compile. */
 #define MF_MODE_FUSED 0   /* planner-selected fusion partition (reference mode) */
 #define MF_MODE_UNFUSED 1 /* one kernel per elementary call (the baseline chain) */
+#define MF_MODE_B200 2    /* fused + row-resident chains (ATAX in one pass; beyond the paper) */
 
 typedef struct mf_plan mf_plan;
 

@@ -222,6 +222,15 @@ b200::NativeKernel lower_kernel(const kernel::KernelIR& k) {
     if (auto st = stores.find(key); st != stores.end()) m.stored = st->second;
     return m;
   };
+  // row-resident chains: a column reduction whose vector is a row reduction
+  // of the same matrix computed in this kernel (planner mode "b200")
+  std::set<std::string> chained_rows;
+  for (const auto& [key, cs] : computed) {
+    if (cs.kind != K::ColReduce) continue;
+    auto src = computed.find(cs.b);
+    if (src != computed.end() && src->second.kind == K::RowReduce && src->second.a == cs.a)
+      chained_rows.insert(cs.b);
+  }
   std::vector<Mat> mats;
   auto mat_index = [&](const Mat& m) {
     for (size_t i = 0; i < mats.size(); ++i)
@@ -242,9 +251,18 @@ b200::NativeKernel lower_kernel(const kernel::KernelIR& k) {
     if (cs.kind != K::RowReduce && cs.kind != K::ColReduce)
       throw std::invalid_argument("lowering: depth-2 kernel mixes in a vector map / dot");
     auto st = stores.find(key);
+    const int mi = mat_index(operand(cs.a));
+    if (cs.kind == K::RowReduce && chained_rows.count(key)) {
+      op.chain = true;
+      op.rows.push_back({mi, external_vector(cs.b), st == stores.end() ? "" : st->second, cs.coef});
+      continue;
+    }
     if (st == stores.end())
       throw std::invalid_argument("lowering: reduction '" + key + "' consumed inside the kernel");
-    const int mi = mat_index(operand(cs.a));
+    if (cs.kind == K::ColReduce && chained_rows.count(cs.b)) {
+      op.cols.push_back({mi, cs.b, st->second, cs.coef});
+      continue;
+    }
     b200::MatrixOp::Red red{mi, external_vector(cs.b), st->second, cs.coef};
     (cs.kind == K::RowReduce ? op.rows : op.cols).push_back(red);
   }
@@ -274,6 +292,13 @@ b200::NativeKernel lower_kernel(const kernel::KernelIR& k) {
     for (const auto* list : {&op.rows, &op.cols})
       for (const auto& r : *list)
         if (r.mat != 0) throw std::invalid_argument("lowering: matrix index");
+  }
+  if (op.chain) {
+    if (op.mats.size() != 1 || !op.rank.empty() || !op.store.empty() || op.rows.size() != 1 ||
+        op.cols.size() != 1)
+      throw std::invalid_argument("lowering: row-resident chain must be one row + one column "
+                                  "reduction of one matrix");
+    return nk;
   }
   if (!matrix_template_exists(static_cast<int>(op.mats.size()), static_cast<int>(op.rank.size()),
                               op.store.empty() ? 0 : 1, static_cast<int>(op.rows.size()),

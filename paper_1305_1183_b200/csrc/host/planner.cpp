@@ -21,10 +21,47 @@ bool contains(const std::vector<int>& v, int x) { return std::find(v.begin(), v.
 
 }  // namespace
 
+namespace {
+// Row-resident exception (PlannerOptions::row_resident): e carries a row
+// reduction's result into a column reduction of the same tile.
+bool row_resident_edge(const script::Edge& e, const script::Script& s, const lib::Library& L,
+                       const PlannerOptions& opt) {
+  if (!opt.row_resident || opt.cols <= 0 || opt.cols > opt.row_resident_max_cols) return false;
+  const auto& pc = call_of(s, e.producer);
+  const auto& cc = call_of(s, e.consumer);
+  const lib::ElementaryFunction* pf = L.find(pc.function);
+  const lib::ElementaryFunction* cf = L.find(cc.function);
+  if (!pf || !cf || pf->depth != 2 || cf->depth != 2) return false;
+  // producer: accumulable row-indexed output (varies y)
+  const lib::ElementDecl* po = nullptr;
+  for (size_t i = 0; i < pc.results.size(); ++i)
+    if (pc.results[i] == e.name) po = pf->element(pf->results[i]);
+  if (!po || !po->accumulable || !po->varies.y || po->varies.x) return false;
+  // consumer: reads it as a row-indexed vector, and produces a column output
+  const lib::ElementDecl* ci = nullptr;
+  std::string ptile, ctile;
+  for (size_t i = 0; i < pc.arguments.size(); ++i)
+    if (!pf->args[i].is_scalar && pf->element(pf->args[i].name)->kind == lib::ElemKind::Tile32x32)
+      ptile = pc.arguments[i];
+  for (size_t i = 0; i < cc.arguments.size(); ++i) {
+    if (cf->args[i].is_scalar) continue;
+    const lib::ElementDecl* d = cf->element(cf->args[i].name);
+    if (cc.arguments[i] == e.name) ci = d;
+    if (d->kind == lib::ElemKind::Tile32x32) ctile = cc.arguments[i];
+  }
+  if (!ci || !ci->varies.y || ci->varies.x || ptile.empty() || ptile != ctile) return false;
+  for (const auto& r : cf->results) {
+    const lib::ElementDecl* d = cf->element(r);
+    if (!d || !d->accumulable || !d->varies.x || d->varies.y) return false;
+  }
+  return true;
+}
+}  // namespace
+
 std::optional<ConstraintViolation> fusibility(const std::vector<int>& nodes_in,
                                               const script::Script& s,
                                               const script::DataDependencyGraph& g,
-                                              const lib::Library& L) {
+                                              const lib::Library& L, const PlannerOptions& opt) {
   std::vector<int> nodes = nodes_in;
   std::sort(nodes.begin(), nodes.end());
   if (nodes.size() < 2) return ConstraintViolation{"no-savings", nodes, "a fusion needs two calls"};
@@ -43,7 +80,7 @@ std::optional<ConstraintViolation> fusibility(const std::vector<int>& nodes_in,
   for (const auto& e : g.edges)
     if (contains(nodes, e.producer) && contains(nodes, e.consumer)) {
       const lib::ElementaryFunction* f = L.find(call_of(s, e.producer).function);
-      if (f->is_reduction())
+      if (f->is_reduction() && !row_resident_edge(e, s, L, opt))
         return ConstraintViolation{"global-barrier-required", {e.producer, e.consumer},
                                    "'" + e.name + "' is a reduction result consumed inside the fusion"};
     }
@@ -111,7 +148,8 @@ int64_t transfer_savings(const Fusion& f, const script::Script& s,
 }
 
 std::vector<Fusion> enumerate_fusions(const script::Script& s, const script::DataDependencyGraph& g,
-                                      const lib::Library& L, Sizes sz, int max_size) {
+                                      const lib::Library& L, Sizes sz, int max_size,
+                                      const PlannerOptions& opt) {
   const std::vector<int> ids = g.nodes;
   const int n = static_cast<int>(ids.size());
   if (n > 24) throw std::invalid_argument("enumerate_fusions: script too long (> 24 calls)");
@@ -150,7 +188,7 @@ std::vector<Fusion> enumerate_fusions(const script::Script& s, const script::Dat
     Fusion f;
     for (int i = 0; i < n; ++i)
       if (mask >> i & 1u) f.calls.push_back(ids[i]);
-    if (fusibility(f.calls, s, g, L)) continue;
+    if (fusibility(f.calls, s, g, L, opt)) continue;
     for (const auto& e : g.edges)
       if (contains(f.calls, e.producer) && contains(f.calls, e.consumer)) f.internal.push_back(e);
     for (const auto& si : g.shared_inputs) {

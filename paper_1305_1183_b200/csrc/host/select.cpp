@@ -30,6 +30,7 @@ CostModel CostModel::defaults() {
       {"matrix.tma.read", 0.95},   // BiCGK 0.92-0.97
       {"matrix.ldg.rank", 0.62},   // GEMVER ger2+sgemtv, register-fed
       {"matrix.tma.rank", 0.95},   // GEMVER ger2+sgemtv, TMA ring
+      {"matrix.rowres", 0.90},     // row-resident chain (ATAX one pass), estimate
   };
   if (const char* f = std::getenv("MF_COST_DB")) {
     std::ifstream in(f);
@@ -48,6 +49,7 @@ double CostModel::predict_us(b200::NativeKernel& k, int64_t m, int64_t n) const 
     return bytes / ((it == eta.end() ? 0.9 : it->second) * bw) + dev.launch_us;
   };
   if (k.kind == b200::NativeKernel::Kind::Stream) return t("stream");
+  if (k.matrix.chain) return t("matrix.rowres");
   const bool heavy = !k.matrix.rank.empty() || !k.matrix.store.empty();
   const double ldg = t(heavy ? "matrix.ldg.rank" : "matrix.ldg.read");
   const double tma = t(heavy ? "matrix.tma.rank" : "matrix.tma.read");
@@ -70,7 +72,7 @@ struct Candidate {
 
 std::vector<Candidate> candidates(const script::Script& s, const script::DataDependencyGraph& g,
                                   const lib::Library& L, Sizes sz, const CostModel& cm,
-                                  bool allow_fusion) {
+                                  bool allow_fusion, const PlannerOptions& opt) {
   std::vector<Candidate> out;
   auto add = [&](const std::vector<int>& calls, bool must) {
     Candidate c;
@@ -88,7 +90,7 @@ std::vector<Candidate> candidates(const script::Script& s, const script::DataDep
   };
   for (int id : g.nodes) add({id}, true);
   if (allow_fusion)
-    for (const auto& f : enumerate_fusions(s, g, L, sz)) add(f.calls, false);
+    for (const auto& f : enumerate_fusions(s, g, L, sz, 6, opt)) add(f.calls, false);
   return out;
 }
 
@@ -127,8 +129,9 @@ bool launch_order(const script::DataDependencyGraph& g, std::vector<Item>& items
 std::vector<Combination> enumerate_combinations(const script::Script& s,
                                                 const script::DataDependencyGraph& g,
                                                 const lib::Library& L, Sizes sz,
-                                                const CostModel& cm, int k, bool allow_fusion) {
-  const auto cands = candidates(s, g, L, sz, cm, allow_fusion);
+                                                const CostModel& cm, int k, bool allow_fusion,
+                                                const PlannerOptions& opt) {
+  const auto cands = candidates(s, g, L, sz, cm, allow_fusion, opt);
   std::vector<Combination> covers;
   std::set<int> covered;
   std::vector<const Candidate*> chosen;
@@ -276,7 +279,10 @@ b200::NativePlan compile_ranked(const std::string& script_text, const lib::Libra
   Parsed p = parse_checked(script_text, L);
   const int m = (rows + 31) / 32 * 32, n = (cols + 31) / 32 * 32;
   const CostModel cm = CostModel::defaults();
-  auto combos = enumerate_combinations(p.s, p.g, L, Sizes{m, n}, cm, rank + 1, mode == 0);
+  PlannerOptions opt;
+  opt.row_resident = mode == 2;
+  opt.cols = n;
+  auto combos = enumerate_combinations(p.s, p.g, L, Sizes{m, n}, cm, rank + 1, mode != 1, opt);
   if (combos.empty()) throw std::invalid_argument("no executable combination for this script");
   if (rank < 0 || rank >= static_cast<int>(combos.size()))
     throw std::invalid_argument("combination rank " + std::to_string(rank) + " out of range (" +

@@ -29,7 +29,8 @@ NativePlan as_invalid(F&& f) {
 NativePlan compile_script(const std::string& script_text, const std::string& manifest, int rows,
                           int cols, int mode) {
   return as_invalid([&] {
-    if (mode != MF_MODE_FUSED && mode != MF_MODE_UNFUSED) throw Invalid("unknown planner mode");
+    if (mode != MF_MODE_FUSED && mode != MF_MODE_UNFUSED && mode != MF_MODE_B200)
+      throw Invalid("unknown planner mode");
     if (manifest.empty()) return plan::compile(script_text, blas::default_library(), rows, cols, mode);
     const lib::Library L = lib::load_library(manifest);
     return plan::compile(script_text, L, rows, cols, mode);
@@ -39,7 +40,8 @@ NativePlan compile_script(const std::string& script_text, const std::string& man
 NativePlan compile_script_ranked(const std::string& script_text, const std::string& manifest,
                                  int rows, int cols, int mode, int rank) {
   return as_invalid([&] {
-    if (mode != MF_MODE_FUSED && mode != MF_MODE_UNFUSED) throw Invalid("unknown planner mode");
+    if (mode != MF_MODE_FUSED && mode != MF_MODE_UNFUSED && mode != MF_MODE_B200)
+      throw Invalid("unknown planner mode");
     if (manifest.empty())
       return plan::compile_ranked(script_text, blas::default_library(), rows, cols, mode, rank);
     const lib::Library L = lib::load_library(manifest);

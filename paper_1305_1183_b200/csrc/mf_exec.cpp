@@ -169,9 +169,67 @@ void run_stream(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc, 
              ("launch " + k.name).c_str());
 }
 
+void fill_peers(MatrixArgs& a, PeerGroup* peers, int64_t n, const std::string& kname) {
+  if (!peers || peers->nranks <= 1) return;
+  if (n > peers->n_cap) throw Fault("kernel " + kname + ": peer group capacity below n");
+  a.peer.nranks = peers->nranks;
+  a.peer.rank = peers->rank;
+  a.peer.n_cap = peers->n_cap;
+  for (int r = 0; r < peers->nranks; ++r) {
+    if (!peers->peer_inbox[r] || !peers->peer_flags[r] || !peers->peer_outbox[r])
+      throw Fault("kernel " + kname + ": peer " + std::to_string(r) + " not connected");
+    a.peer.inbox[r] = peers->peer_inbox[r];
+    a.peer.outbox[r] = peers->peer_outbox[r];
+    a.peer.flags[r] = peers->peer_flags[r];
+  }
+  a.peer.epoch = ++peers->epoch;
+  a.peer.spin_limit = 20000000000LL;  // ~10 s: trap instead of hanging the GPU
+}
+
+// Row-resident chain: t = a*A x (optionally stored), y = b*A^T t, one pass.
+void run_rowres(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc, cudaStream_t s,
+                Workspace& ws, PeerGroup* peers) {
+  const MatrixOp& op = k.matrix;
+  if (op.mats.size() != 1 || op.rows.size() != 1 || op.cols.size() != 1 || !op.rank.empty())
+    throw Invalid("kernel " + k.name + ": malformed row-resident chain");
+  const DevBuf& M = need(bufs, op.mats[0], k.name);
+  const int64_t m = M.rows, n = M.cols;
+  if (n > rowres_max_cols())
+    throw Fault("kernel " + k.name + ": row-resident chain needs n <= " +
+                std::to_string(rowres_max_cols()) + " (got " + std::to_string(n) + ")");
+  MatrixArgs a;
+  a.m = m;
+  a.n = n;
+  a.ld = n;
+  a.M[0] = M.ptr;
+  const DevBuf& x = need(bufs, op.rows[0].x, k.name);
+  need_len(x, n, op.rows[0].x, k.name);
+  a.xr[0] = x.ptr;
+  a.ar[0] = coef(op.rows[0].coef, sc, k.name);
+  if (!op.rows[0].y.empty()) {
+    const DevBuf& t = need(bufs, op.rows[0].y, k.name);
+    need_len(t, m, op.rows[0].y, k.name);
+    a.yr[0] = t.ptr;
+  }
+  const DevBuf& y = need(bufs, op.cols[0].y, k.name);
+  need_len(y, n, op.cols[0].y, k.name);
+  a.yc[0] = y.ptr;
+  a.ac[0] = coef(op.cols[0].coef, sc, k.name);
+  if (m == 0 || n == 0) return;
+  const EngineOptions& eo = options();
+  const int sms = eo.max_sms > 0 ? std::min(eo.max_sms, device_sm_count()) : device_sm_count();
+  int grid = 0;
+  check_cuda(rowres_config(m, n, sms, &a, &grid), ("configure " + k.name).c_str());
+  a.colpart = ws.scratch(sizeof(float) * (size_t)a.RB * (size_t)n + 256, s);
+  a.bar = ws.counters(s);
+  fill_peers(a, peers, n, k.name);
+  check_cuda(launch_rowres(a, grid, s), ("launch " + k.name).c_str());
+}
+
 void run_matrix(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc, cudaStream_t s,
                 Workspace& ws, PeerGroup* peers) {
   const MatrixOp& op = k.matrix;
+  if (op.chain) return run_rowres(k, bufs, sc, s, ws, peers);
   MatrixShape sh{(int)op.mats.size(), (int)op.rank.size(), op.store.empty() ? 0 : 1,
                  (int)op.rows.size(), (int)op.cols.size()};
   if (!matrix_shape_supported(sh))
@@ -245,21 +303,7 @@ void run_matrix(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc, 
     check_cuda(matrix_tma_config(sh, t, m, n, sms, &a, &grid), ("configure " + k.name).c_str());
   else
     check_cuda(matrix_config(sh, t, m, n, sms, &a, &grid), ("configure " + k.name).c_str());
-  if (peers && peers->nranks > 1 && sh.ncol > 0) {
-    if (n > peers->n_cap) throw Fault("kernel " + k.name + ": peer group capacity below n");
-    a.peer.nranks = peers->nranks;
-    a.peer.rank = peers->rank;
-    a.peer.n_cap = peers->n_cap;
-    for (int r = 0; r < peers->nranks; ++r) {
-      if (!peers->peer_inbox[r] || !peers->peer_flags[r] || !peers->peer_outbox[r])
-        throw Fault("kernel " + k.name + ": peer " + std::to_string(r) + " not connected");
-      a.peer.inbox[r] = peers->peer_inbox[r];
-      a.peer.outbox[r] = peers->peer_outbox[r];
-      a.peer.flags[r] = peers->peer_flags[r];
-    }
-    a.peer.epoch = ++peers->epoch;
-    a.peer.spin_limit = 20000000000LL;  // ~10 s: trap instead of hanging the GPU
-  }
+  if (sh.ncol > 0) fill_peers(a, peers, n, k.name);
   const size_t acc = matrix_acc_bytes(t);
   const size_t colb = acc * (size_t)sh.ncol * (size_t)a.RB * (size_t)n;
   const size_t rowb = (a.CB > 1) ? acc * (size_t)sh.nrow * (size_t)a.CB * (size_t)m : 0;

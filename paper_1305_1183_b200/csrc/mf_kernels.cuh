@@ -95,6 +95,11 @@ cudaError_t matrix_tma_config(const MatrixShape& sh, const MatrixTuning& t, long
 cudaError_t launch_matrix_tma(const MatrixShape& sh, const MatrixTuning& t, const MatrixArgs& a,
                               int grid, cudaStream_t s);
 int tma_stages(const MatrixShape& sh, const MatrixTuning& t);
+
+// Row-resident chained reduction t = a*A x ; y = b*A^T t, one pass (mf_rowres.cu).
+long long rowres_max_cols();
+cudaError_t rowres_config(long long m, long long n, int sms, MatrixArgs* a, int* grid);
+cudaError_t launch_rowres(const MatrixArgs& a, int grid, cudaStream_t s);
 bool tma_supported(const MatrixShape& sh, const MatrixTuning& t);  // fits a >= 2-stage ring
 size_t matrix_acc_bytes(const MatrixTuning& t);
 

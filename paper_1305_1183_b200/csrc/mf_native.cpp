@@ -81,7 +81,8 @@ std::vector<std::string> NativeKernel::inputs() const {
       add(w);
     }
     for (const auto& r : matrix.rows) add(r.x);
-    for (const auto& c : matrix.cols) add(c.x);
+    if (!matrix.chain)
+      for (const auto& c : matrix.cols) add(c.x);
   }
   return v;
 }
@@ -93,7 +94,8 @@ std::vector<std::string> NativeKernel::outputs() const {
     if (stream.has_dot) v.push_back(stream.dot_out);
   } else {
     if (!matrix.store.empty()) v.push_back(matrix.store);
-    for (const auto& r : matrix.rows) v.push_back(r.y);
+    for (const auto& r : matrix.rows)
+      if (!r.y.empty()) v.push_back(r.y);
     for (const auto& c : matrix.cols) v.push_back(c.y);
   }
   return v;
@@ -120,7 +122,7 @@ uint64_t NativeKernel::bytes_loaded(int64_t m, int64_t n) const {
   for (const auto& r : matrix.rows)
     if (seen.insert(r.x).second) b += 4ull * n;
   for (const auto& c : matrix.cols)
-    if (seen.insert(c.x).second) b += 4ull * m;
+    if (!matrix.chain && seen.insert(c.x).second) b += 4ull * m;
   return b;
 }
 
@@ -128,7 +130,9 @@ uint64_t NativeKernel::bytes_stored(int64_t m, int64_t n) const {
   if (kind == Kind::Stream)
     return 4ull * (uint64_t)stream.outs.size() * (uint64_t)n + (stream.has_dot ? 4ull : 0ull);
   uint64_t b = matrix.store.empty() ? 0 : 4ull * (uint64_t)(m * n);
-  b += 4ull * m * matrix.rows.size() + 4ull * n * matrix.cols.size();
+  for (const auto& r : matrix.rows)
+    if (!r.y.empty()) b += 4ull * m;
+  b += 4ull * n * matrix.cols.size();
   return b;
 }
 
@@ -218,7 +222,8 @@ std::string NativePlan::describe_json() const {
       os << "],\"rank\":[";
       for (size_t t = 0; t < m.rank.size(); ++t)
         os << (t ? "," : "") << "[" << jstr(m.rank[t].first) << "," << jstr(m.rank[t].second) << "]";
-      os << "],\"store\":" << jstr(m.store) << ",\"rows\":" << reds(m.rows) << ",\"cols\":" << reds(m.cols)
+      os << "],\"store\":" << jstr(m.store) << ",\"chain\":" << (m.chain ? "true" : "false")
+         << ",\"rows\":" << reds(m.rows) << ",\"cols\":" << reds(m.cols)
          << "},\"variant\":{\"tma\":" << k.variant_tma << ",\"k\":" << k.variant_k << "}";
     } else {
       const StreamOp& st = k.stream;
@@ -235,7 +240,7 @@ std::string NativePlan::describe_json() const {
     if (k.kind == NativeKernel::Kind::Matrix) {
       os << ",\"shape\":{\"mats\":" << k.matrix.mats.size() << ",\"rank\":" << k.matrix.rank.size()
          << ",\"store\":" << (k.matrix.store.empty() ? 0 : 1) << ",\"rows\":" << k.matrix.rows.size()
-         << ",\"cols\":" << k.matrix.cols.size() << "}";
+         << ",\"cols\":" << k.matrix.cols.size() << ",\"chain\":" << (k.matrix.chain ? 1 : 0) << "}";
     } else {
       os << ",\"shape\":{\"inputs\":" << k.stream.inputs.size() << ",\"outs\":"
          << k.stream.outs.size() << ",\"dot\":" << (k.stream.has_dot ? 1 : 0) << "}";

@@ -66,6 +66,9 @@ struct MatrixOp {
   };
   std::vector<Red> rows;  // y[i] = coef * sum_j E[i][j] x[j]     (<= 2)
   std::vector<Red> cols;  // y[j] = coef * sum_i E[i][j] x[i]     (<= 2)
+  // row-resident chain (planner mode "b200"): cols[0].x is rows[0]'s result,
+  // computed in the same pass; rows[0].y may be "" (t never stored)
+  bool chain = false;
 };
 
 struct NativeKernel {

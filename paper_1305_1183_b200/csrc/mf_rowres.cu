@@ -1,0 +1,206 @@
+// mf_rowres.cu -- row-resident chained reduction: t = a*A x ; y = b*A^T t
+// in ONE pass over A (ATAX in a single read).
+//
+// The paper (and SPEC.md:190) forbid fusing a reduction with the consumer of
+// its result: on the paper's 32x32-tile kernels t_i is only complete after a
+// global barrier, so ATAX reads A twice.  On B200 a whole row
+// of a matrix with n <= 16384 fp32 columns (64 KB) fits in one stage of a
+// shared-memory ring, so a CTA that owns entire rows completes t_i itself:
+//   producer warp: cp.async.bulk of row i (up to 64 KB) into a 3-stage ring;
+//   16 consumer warps: each thread holds K float4 column slots of the row in
+//     registers, reduces A_i . x across the CTA (warp butterfly + 16-way
+//     shared-memory combine, fixed order), and immediately accumulates
+//     A_i^T t_i into its register column accumulators;
+//   column partials of every CTA's row band are combined after one grid
+//   barrier (or across GPUs in-kernel, see mf_device.cuh finalize_any).
+// Traffic: mn + 2n words instead of 2mn + m + 2n.  Planner mode "b200" only.
+#include <algorithm>
+
+#include "mf_device.cuh"
+#include "mf_kernels.cuh"
+
+namespace mapfuse::b200 {
+namespace {
+
+using namespace dev;
+
+constexpr int kRrConsumers = 512;
+constexpr int kRrWarps = kRrConsumers / 32;
+constexpr int kRrThreads = kRrConsumers + 32;
+constexpr int kRrStages = 3;
+
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void rr_mbar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(count));
+}
+__device__ __forceinline__ void rr_expect_tx(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void rr_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(b)) : "memory");
+}
+__device__ __forceinline__ void rr_wait(unsigned long long* b, unsigned parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nRR_WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra RR_WAIT_%=;\n}\n" ::"r"(smem_addr(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void rr_bulk(void* dst, const void* src, unsigned bytes,
+                                        unsigned long long* bar, unsigned long long pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(pol)
+      : "memory");
+}
+
+template <int K>
+__global__ void __launch_bounds__(kRrThreads, 1) rowres_kernel(MatrixArgs a) {
+  constexpr int C = 4 * kRrConsumers * K;  // columns covered by one CTA
+  extern __shared__ __align__(128) unsigned char smem[];
+  float* ring = reinterpret_cast<float*>(smem);
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(ring + (size_t)kRrStages * C);
+  unsigned long long* empty = full + kRrStages;
+  __shared__ float red[2][kRrWarps];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const long long r0 = (long long)blockIdx.x * a.m / gridDim.x;
+  const long long r1 = (long long)(blockIdx.x + 1) * a.m / gridDim.x;
+  if (tid == 0) {
+    for (int s = 0; s < kRrStages; ++s) {
+      rr_mbar_init(&full[s], 1);
+      rr_mbar_init(&empty[s], kRrWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == kRrWarps) {
+    if (lane == 0) {  // producer: one row (n floats) per stage
+      const unsigned long long pol = evict_first_policy();
+      const unsigned bytes = (unsigned)(a.n * 4);
+      int stage = 0;
+      unsigned phase = 0;
+      for (long long i = r0; i < r1; ++i) {
+        rr_wait(&empty[stage], phase ^ 1u);
+        rr_expect_tx(&full[stage], bytes);
+        rr_bulk(ring + (size_t)stage * C, a.M[0] + i * a.ld, bytes, &full[stage], pol);
+        if (++stage == kRrStages) {
+          stage = 0;
+          phase ^= 1u;
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    int lcol[K];
+    bool ok[K];
+    float4 xs[K];
+    float cacc[K][4];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      lcol[k] = 4 * (tid + kRrConsumers * k);
+      ok[k] = lcol[k] < a.n;
+      xs[k] = ok[k] ? __ldg(reinterpret_cast<const float4*>(a.xr[0] + lcol[k]))
+                    : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) cacc[k][e] = 0.f;
+    }
+    int stage = 0, buf = 0;
+    unsigned phase = 0;
+    for (long long i = r0; i < r1; ++i) {
+      rr_wait(&full[stage], phase);
+      const float* row = ring + (size_t)stage * C;
+      float4 av[K];
+      float part = 0.f;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        av[k] = ok[k] ? *reinterpret_cast<const float4*>(row + lcol[k]) : make_float4(0.f, 0.f, 0.f, 0.f);
+        part = fmaf(av[k].x, xs[k].x, part);
+        part = fmaf(av[k].y, xs[k].y, part);
+        part = fmaf(av[k].z, xs[k].z, part);
+        part = fmaf(av[k].w, xs[k].w, part);
+      }
+      __syncwarp();
+      if (lane == 0) rr_arrive(&empty[stage]);  // row now lives in registers
+      if (++stage == kRrStages) {
+        stage = 0;
+        phase ^= 1u;
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
+      if (lane == 0) red[buf][warp] = part;
+      asm volatile("bar.sync 1, %0;" ::"n"(kRrConsumers) : "memory");
+      float s = red[buf][0];
+#pragma unroll
+      for (int w = 1; w < kRrWarps; ++w) s += red[buf][w];
+      buf ^= 1;
+      // t_i rounded to fp32 exactly as the unfused plan stores it
+      const float ti = (float)(a.ar[0] * (double)s);
+      if (tid == 0 && a.yr[0]) a.yr[0][i] = ti;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        cacc[k][0] = fmaf(av[k].x, ti, cacc[k][0]);
+        cacc[k][1] = fmaf(av[k].y, ti, cacc[k][1]);
+        cacc[k][2] = fmaf(av[k].z, ti, cacc[k][2]);
+        cacc[k][3] = fmaf(av[k].w, ti, cacc[k][3]);
+      }
+    }
+    float* colpart = static_cast<float*>(a.colpart);
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      if (ok[k]) {
+        float* dst = colpart + (long long)blockIdx.x * a.n + lcol[k];
+        *reinterpret_cast<float4*>(dst) = make_float4(cacc[k][0], cacc[k][1], cacc[k][2], cacc[k][3]);
+      }
+  }
+  grid_barrier(a.bar);
+  finalize_any<0, 1, float>(a, tid, kRrThreads);
+}
+
+using RrFn = void (*)(MatrixArgs);
+
+RrFn rowres_fn(long long n) {
+  if (n <= 4LL * kRrConsumers * 2) return rowres_kernel<2>;
+  if (n <= 4LL * kRrConsumers * 4) return rowres_kernel<4>;
+  if (n <= 4LL * kRrConsumers * 8) return rowres_kernel<8>;
+  return nullptr;
+}
+
+size_t rowres_smem(long long n) {
+  const long long C = n <= 4096 ? 4096 : (n <= 8192 ? 8192 : 16384);
+  return (size_t)kRrStages * C * 4 + 2 * kRrStages * 8 + 128;
+}
+
+}  // namespace
+
+long long rowres_max_cols() { return 4LL * kRrConsumers * 8; }
+
+cudaError_t rowres_config(long long m, long long n, int sms, MatrixArgs* a, int* grid) {
+  RrFn fn = rowres_fn(n);
+  if (!fn) return cudaErrorNotSupported;
+  const size_t smem = rowres_smem(n);
+  cudaError_t e = cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  const long long g = std::max(1LL, std::min<long long>(sms, m));
+  a->CB = 1;
+  a->RB = (int)g;  // one row band per CTA: colpart is [grid][n]
+  a->tiles = (int)g;
+  *grid = (int)g;
+  return cudaSuccess;
+}
+
+cudaError_t launch_rowres(const MatrixArgs& a, int grid, cudaStream_t s) {
+  RrFn fn = rowres_fn(a.n);
+  if (!fn) return cudaErrorNotSupported;
+  MatrixArgs copy = a;
+  void* args[] = {&copy};
+  return cudaLaunchCooperativeKernel((const void*)fn, dim3(grid), dim3(kRrThreads), args,
+                                     rowres_smem(a.n), s);
+}
+
+}  // namespace mapfuse::b200

@@ -19,7 +19,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG, "libmapfuse_b200.so")
 
 MF_OK, MF_ERR_FAULT, MF_ERR_INVALID = 0, 1, 2
-MODES = {"fused": 0, "unfused": 1, "builtin_fused": 10, "builtin_unfused": 11}
+MODES = {"fused": 0, "unfused": 1, "b200": 2, "builtin_fused": 10, "builtin_unfused": 11}
 
 
 class MapfuseError(RuntimeError):

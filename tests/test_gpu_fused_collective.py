@@ -92,3 +92,42 @@ def test_virtual_ranks_fused_column_reduction(seq, m, n, P, tma):
     finally:
         mf.set_option("max_sms", 0)
         mf.set_option("tma", -1)
+
+
+def test_virtual_ranks_row_resident_chain():
+    """Row-resident ATAX kernel + in-kernel cross-rank column reduction."""
+    import torch
+    import paper_1305_1183_b200 as mf
+    co = COracle()
+    P, m, n = 2, 2048, 8192
+    mf.set_option("max_sms", 148 // P)
+    try:
+        rng = np.random.default_rng(5)
+        A = rng.uniform(-1, 1, (m, n)).astype(np.float32)
+        x = rng.uniform(-1, 1, n).astype(np.float32)
+        mloc = m // P
+        plans = [mf.Plan.sequence("ATAX", mloc, n, "b200") for _ in range(P)]
+        assert plans[0].describe()["kernels"][0]["shape"]["chain"] == 1
+        groups = [mf.PeerGroup(P, r, n) for r in range(P)]
+        for r in range(P):
+            for q in range(P):
+                if q != r:
+                    groups[r].connect_local(q, groups[q])
+        bufs = [{"A": torch.from_numpy(A[r * mloc:(r + 1) * mloc].copy()).cuda(),
+                 "x": torch.from_numpy(x).cuda(), "y": torch.zeros(n, device="cuda")}
+                for r in range(P)]
+        for r in range(P):
+            plans[r].launch(bufs[r])
+        torch.cuda.synchronize()
+        streams = [torch.cuda.Stream() for _ in range(P)]
+        for r in range(P):
+            plans[r].launch_kernel_peers(0, groups[r], bufs[r], {}, streams[r])
+        torch.cuda.synchronize()
+        want = co.execute("ATAX", m, n, {"A": A, "x": x})["y"]
+        S = co.execute("ATAX", m, n, {"A": np.abs(A), "x": np.abs(x)})["y"]
+        for r in range(P):
+            got = bufs[r]["y"].cpu().numpy().astype(np.float64)
+            assert np.all(np.abs(got - want) <= TAU * S + np.spacing(np.abs(want)))
+        assert np.array_equal(bufs[0]["y"].cpu().numpy(), bufs[1]["y"].cpu().numpy())
+    finally:
+        mf.set_option("max_sms", 0)

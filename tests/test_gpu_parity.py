@@ -249,3 +249,24 @@ def test_host_launch_pipelined_pinned(env, seq):
     assert st["ms"] > 0
     want = co.execute(seq, 1, n, vals)[outname]
     assert np.array_equal(host[outname], want)
+
+
+@pytest.mark.parametrize("m,n", [(64, 64), (96, 160), (1024, 4096), (3000, 8192), (2048, 16384),
+                                 (16384, 16384), (256, 4000)])
+def test_b200_mode_row_resident_atax(env, m, n):
+    """Planner mode "b200": ATAX as ONE row-resident pass over A."""
+    torch, mf, co = env
+    vals = rand_inputs("ATAX", m, n, 77 + m)
+    plan = mf.Plan.sequence("ATAX", m, n, "b200")
+    ks = plan.describe()["kernels"]
+    assert len(ks) == 1 and ks[0]["shape"]["chain"] == 1
+    mp, np_ = (m + 31) // 32 * 32, (n + 31) // 32 * 32
+    vals = rand_inputs("ATAX", mp, np_, 77 + m)
+    got = run_plan(torch, plan, vals, out_shapes(plan))
+    want = co.execute("ATAX", mp, np_, vals)
+    S = scale_bound(co, "ATAX", mp, np_, vals)
+    check_output("ATAX", "y", got["y"], want["y"], S["y"])
+    # identical rounding of t to the two-kernel plan: same result as the fused-mode plan
+    ref = run_plan(torch, mf.Plan.sequence("ATAX", m, n, "fused"), vals, out_shapes(plan))
+    err = np.abs(got["y"].astype(np.float64) - ref["y"])
+    assert np.all(err <= 2.0 ** -17 * S["y"] + np.spacing(np.abs(ref["y"])))

@@ -168,3 +168,21 @@ def test_random_scripts_always_compile():
         text, calls, ret = make_script(rng, 3 + seed % 5)
         p = mf.Plan.compile(text, 96 + 32 * (seed % 3), 128 + 64 * (seed % 4))
         assert p.num_kernels >= 1
+
+
+def test_b200_mode_row_resident_plans():
+    """Mode "b200" fuses ATAX's sgemv -> sgemtv through t when a row fits a
+    CTA (n <= 16384), keeps the paper's plan otherwise and elsewhere."""
+    d = mf.Plan.sequence("ATAX", 16384, 16384, "b200").describe()
+    assert [k["calls"] for k in d["kernels"]] == [[0, 1]]
+    assert d["kernels"][0]["op"]["chain"] is True
+    assert d["bytes_loaded"] + d["bytes_stored"] == 4 * (16384 * 16384 + 2 * 16384)
+    assert len(mf.Plan.sequence("ATAX", 16384, 32768, "b200").describe()["kernels"]) == 2
+    for seq in ("BICGK", "GEMVER", "GESUMMV", "SGEMVT", "VADD", "AXPYDOT"):
+        a = mf.Plan.sequence(seq, 2048, 2048, "b200").describe()
+        b = mf.Plan.sequence(seq, 2048, 2048, "fused").describe()
+        assert [k["calls"] for k in a["kernels"]] == [k["calls"] for k in b["kernels"]], seq
+    # the chain kernel survives the KernelIR text boundary
+    p = mf.Plan.sequence("ATAX", 1024, 1024, "b200")
+    q = mf.Plan.from_kernel_text(p.kernel_text(0), 1024, 1024)
+    assert q.describe()["kernels"][0]["op"]["chain"] is True

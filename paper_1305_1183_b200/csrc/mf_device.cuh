@@ -98,52 +98,80 @@ __device__ __forceinline__ double fmacc<double>(double a, double b, double c) {
   return fma(a, b, c);
 }
 
+// Cross-CTA partial sums, parallel and deterministic: 8 lanes cooperate on one
+// float4 slot (lane g of the group sums partials g, g+8, g+16, ... in order;
+// a fixed xor butterfly combines the 8), so a slot with 148 partials costs
+// ~19 dependent L2 loads per lane instead of 148.  Loop trip counts are
+// warp-uniform so every shuffle has all 32 lanes.
+constexpr int kFinGroup = 8;
+
+template <typename ACC>
+__device__ __forceinline__ void group_sum4(const ACC* base, long long stride, int count, bool valid,
+                                           int glane, ACC (&t)[4]) {
+  t[0] = t[1] = t[2] = t[3] = ACC(0);
+  if (valid)
+    for (int b = glane; b < count; b += kFinGroup) {
+      const ACC* q = base + (long long)b * stride;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) t[e] += __ldcg(q + e);
+    }
+#pragma unroll
+  for (int off = kFinGroup / 2; off > 0; off >>= 1)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) t[e] += __shfl_xor_sync(0xffffffffu, t[e], off);
+}
+
+// Visits slots [0, total) in warp-uniform rounds; f(slot, valid, glane, lead).
+template <typename F>
+__device__ __forceinline__ void for_each_slot_grouped(long long total, int tid, int nthreads, F&& f) {
+  const int lane = tid & 31;
+  const int glane = lane % kFinGroup;
+  const long long warps_total = (long long)gridDim.x * (nthreads / 32);
+  const long long gwarp = (long long)blockIdx.x * (nthreads / 32) + tid / 32;
+  constexpr int per_warp = 32 / kFinGroup;
+  for (long long first = gwarp * per_warp; first < total; first += warps_total * per_warp) {
+    const long long slot = first + lane / kFinGroup;
+    f(slot, slot < total, glane, glane == 0 && slot < total);
+  }
+}
+
 // Cross-CTA finalize after the grid barrier: column outputs sum the RB band
 // partials, row outputs (when the row was split over CB column chunks) sum
 // the CB chunk partials -- fixed order, so results are reproducible.
 template <int NROW, int NCOL, typename ACC>
 __device__ __forceinline__ void finalize(const MatrixArgs& a, int tid, int nthreads) {
-  ACC* colpart = static_cast<ACC*>(a.colpart);
-  ACC* rowpart = static_cast<ACC*>(a.rowpart);
+  const ACC* colpart = static_cast<const ACC*>(a.colpart);
+  const ACC* rowpart = static_cast<const ACC*>(a.rowpart);
   const bool need_rows = (NROW > 0) && a.CB > 1;
   const long long n4 = a.n / 4, m4 = a.m / 4;
   const long long col_slots = (long long)NCOL * n4;
   const long long total = col_slots + (need_rows ? (long long)NROW * m4 : 0);
-  for (long long s = (long long)blockIdx.x * nthreads + tid; s < total;
-       s += (long long)gridDim.x * nthreads) {
-    if (s < col_slots) {
-      const int c = (int)(s / n4);
-      const long long j = (s % n4) * 4;
-      ACC t[4] = {ACC(0), ACC(0), ACC(0), ACC(0)};
-      for (int b = 0; b < a.RB; ++b) {
-        const ACC* p = colpart + ((long long)c * a.RB + b) * a.n + j;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) t[e] += __ldcg(p + e);
+  for_each_slot_grouped(total, tid, nthreads, [&](long long s, bool valid, int glane, bool lead) {
+    ACC t[4];
+    // invalid lanes only occur past the last slot: follow that region's branch
+    // so each warp's shuffles stay convergent (col_slots is a multiple of 8)
+    const bool col_branch = valid ? (s < col_slots) : !need_rows;
+    if (col_branch) {
+      const int c = valid ? (int)(s / n4) : 0;
+      const long long j = valid ? (s % n4) * 4 : 0;
+      group_sum4<ACC>(colpart + (long long)c * a.RB * a.n + j, a.n, a.RB, valid && NCOL > 0, glane, t);
+      if (lead && NCOL > 0) {
+        float4 o = make_float4((float)(a.ac[c] * (double)t[0]), (float)(a.ac[c] * (double)t[1]),
+                               (float)(a.ac[c] * (double)t[2]), (float)(a.ac[c] * (double)t[3]));
+        *reinterpret_cast<float4*>(a.yc[c] + j) = o;
       }
-      float4 o;
-      o.x = (float)(a.ac[c] * (double)t[0]);
-      o.y = (float)(a.ac[c] * (double)t[1]);
-      o.z = (float)(a.ac[c] * (double)t[2]);
-      o.w = (float)(a.ac[c] * (double)t[3]);
-      *reinterpret_cast<float4*>(a.yc[c] + j) = o;
     } else {
-      const long long q = s - col_slots;
+      const long long q = valid ? s - col_slots : 0;
       const int o = (int)(q / m4);
       const long long i = (q % m4) * 4;
-      ACC t[4] = {ACC(0), ACC(0), ACC(0), ACC(0)};
-      for (int b = 0; b < a.CB; ++b) {
-        const ACC* p = rowpart + ((long long)o * a.CB + b) * a.m + i;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) t[e] += __ldcg(p + e);
+      group_sum4<ACC>(rowpart + (long long)o * a.CB * a.m + i, a.m, a.CB, valid, glane, t);
+      if (lead) {
+        float4 r = make_float4((float)(a.ar[o] * (double)t[0]), (float)(a.ar[o] * (double)t[1]),
+                               (float)(a.ar[o] * (double)t[2]), (float)(a.ar[o] * (double)t[3]));
+        *reinterpret_cast<float4*>(a.yr[o] + i) = r;
       }
-      float4 r;
-      r.x = (float)(a.ar[o] * (double)t[0]);
-      r.y = (float)(a.ar[o] * (double)t[1]);
-      r.z = (float)(a.ar[o] * (double)t[2]);
-      r.w = (float)(a.ar[o] * (double)t[3]);
-      *reinterpret_cast<float4*>(a.yr[o] + i) = r;
     }
-  }
+  });
 }
 
 // ---------------------------------------------------------------------------
@@ -178,20 +206,18 @@ __device__ __forceinline__ void finalize_columns_peers(const MatrixArgs& a, int 
   const long long slice4 = n4 / pl.nranks;  // n / P is a multiple of 4 (n % 32 == 0, P <= 8)
   const long long P = pl.nranks;
   // Phase A: local sums -> owner's inbox[c][rank][j]
-  for (long long s = (long long)blockIdx.x * nthreads + tid; s < (long long)NCOL * n4; s += gstride) {
-    const int c = (int)(s / n4);
-    const long long j4 = s % n4, j = j4 * 4;
-    ACC t[4] = {ACC(0), ACC(0), ACC(0), ACC(0)};
-    for (int b = 0; b < a.RB; ++b) {
-      const ACC* p = colpart + ((long long)c * a.RB + b) * a.n + j;
-#pragma unroll
-      for (int e = 0; e < 4; ++e) t[e] += __ldcg(p + e);
-    }
+  for_each_slot_grouped((long long)NCOL * n4, tid, nthreads,
+                        [&](long long s, bool valid, int glane, bool lead) {
+    const int c = valid ? (int)(s / n4) : 0;
+    const long long j4 = valid ? s % n4 : 0, j = j4 * 4;
+    ACC t[4];
+    group_sum4<ACC>(colpart + (long long)c * a.RB * a.n + j, a.n, a.RB, valid, glane, t);
+    if (!lead) return;
     const int owner = (int)min(j4 / slice4, P - 1);
     float4 v = make_float4((float)t[0], (float)t[1], (float)t[2], (float)t[3]);
     float* dst = pl.inbox[owner] + ((long long)c * P + pl.rank) * pl.n_cap + j;
     *reinterpret_cast<float4*>(dst) = v;
-  }
+  });
   grid_barrier(a.bar);
   if (blockIdx.x == 0 && tid == 0) peer_signal_wait(pl, 0);
   grid_barrier(a.bar);
@@ -236,20 +262,17 @@ __device__ __forceinline__ void finalize_rows(const MatrixArgs& a, int tid, int 
   if (NROW == 0 || a.CB <= 1) return;
   const ACC* rowpart = static_cast<const ACC*>(a.rowpart);
   const long long m4 = a.m / 4;
-  for (long long q = (long long)blockIdx.x * nthreads + tid; q < (long long)NROW * m4;
-       q += (long long)gridDim.x * nthreads) {
-    const int o = (int)(q / m4);
-    const long long i = (q % m4) * 4;
-    ACC t[4] = {ACC(0), ACC(0), ACC(0), ACC(0)};
-    for (int b = 0; b < a.CB; ++b) {
-      const ACC* p = rowpart + ((long long)o * a.CB + b) * a.m + i;
-#pragma unroll
-      for (int e = 0; e < 4; ++e) t[e] += __ldcg(p + e);
-    }
+  for_each_slot_grouped((long long)NROW * m4, tid, nthreads,
+                        [&](long long q, bool valid, int glane, bool lead) {
+    const int o = valid ? (int)(q / m4) : 0;
+    const long long i = valid ? (q % m4) * 4 : 0;
+    ACC t[4];
+    group_sum4<ACC>(rowpart + (long long)o * a.CB * a.m + i, a.m, a.CB, valid, glane, t);
+    if (!lead) return;
     float4 r = make_float4((float)(a.ar[o] * (double)t[0]), (float)(a.ar[o] * (double)t[1]),
                            (float)(a.ar[o] * (double)t[2]), (float)(a.ar[o] * (double)t[3]));
     *reinterpret_cast<float4*>(a.yr[o] + i) = r;
-  }
+  });
 }
 
 template <int NROW, int NCOL, typename ACC>

@@ -7,10 +7,11 @@
 // of a matrix with n <= 16384 fp32 columns (64 KB) fits in one stage of a
 // shared-memory ring, so a CTA that owns entire rows completes t_i itself:
 //   producer warp: cp.async.bulk of row i (up to 64 KB) into a 3-stage ring;
-//   16 consumer warps: each thread holds K float4 column slots of the row in
-//     registers, reduces A_i . x across the CTA (warp butterfly + 16-way
-//     shared-memory combine, fixed order), and immediately accumulates
-//     A_i^T t_i into its register column accumulators;
+//   16 consumer warps: each thread owns K float4 column slots; pass 1 reads
+//     them from the staged row and reduces A_i . x across the CTA (warp
+//     shuffles + 16-way shared-memory combine, fixed order); pass 2 re-reads
+//     the same slots and accumulates A_i^T t_i into register column
+//     accumulators, then releases the stage;
 //   column partials of every CTA's row band are combined after one grid
 //   barrier (or across GPUs in-kernel, see mf_device.cuh finalize_any).
 // Traffic: mn + 2n words instead of 2mn + m + 2n.  Planner mode "b200" only.
@@ -59,14 +60,14 @@ __device__ __forceinline__ void rr_bulk(void* dst, const void* src, unsigned byt
       : "memory");
 }
 
-template <int K>
+template <int K, int R>
 __global__ void __launch_bounds__(kRrThreads, 1) rowres_kernel(MatrixArgs a) {
   constexpr int C = 4 * kRrConsumers * K;  // columns covered by one CTA
   extern __shared__ __align__(128) unsigned char smem[];
-  float* ring = reinterpret_cast<float*>(smem);
-  unsigned long long* full = reinterpret_cast<unsigned long long*>(ring + (size_t)kRrStages * C);
+  float* ring = reinterpret_cast<float*>(smem);  // stage = R rows of n floats (<= R*C)
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(ring + (size_t)kRrStages * R * C);
   unsigned long long* empty = full + kRrStages;
-  __shared__ float red[2][kRrWarps];
+  __shared__ float red[2][kRrWarps][R];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const long long r0 = (long long)blockIdx.x * a.m / gridDim.x;
   const long long r1 = (long long)(blockIdx.x + 1) * a.m / gridDim.x;
@@ -79,15 +80,22 @@ __global__ void __launch_bounds__(kRrThreads, 1) rowres_kernel(MatrixArgs a) {
   }
   __syncthreads();
   if (warp == kRrWarps) {
-    if (lane == 0) {  // producer: one row (n floats) per stage
+    if (lane == 0) {  // producer: R consecutive rows (contiguous) per stage
       const unsigned long long pol = evict_first_policy();
-      const unsigned bytes = (unsigned)(a.n * 4);
       int stage = 0;
       unsigned phase = 0;
-      for (long long i = r0; i < r1; ++i) {
+      for (long long i = r0; i < r1; i += R) {
+        const long long rows = (r1 - i) < R ? (r1 - i) : R;
+        const long long bytes = rows * a.n * 4;
         rr_wait(&empty[stage], phase ^ 1u);
-        rr_expect_tx(&full[stage], bytes);
-        rr_bulk(ring + (size_t)stage * C, a.M[0] + i * a.ld, bytes, &full[stage], pol);
+        rr_expect_tx(&full[stage], (unsigned)bytes);
+        // 16 KB pieces keep several bulk transfers in flight per stage
+        const char* src = reinterpret_cast<const char*>(a.M[0] + i * a.ld);
+        char* dst = reinterpret_cast<char*>(ring + (size_t)stage * R * C);
+        for (long long off = 0; off < bytes; off += 16384) {
+          const long long piece = (bytes - off) < 16384 ? (bytes - off) : 16384;
+          rr_bulk(dst + off, src + off, (unsigned)piece, &full[stage], pol);
+        }
         if (++stage == kRrStages) {
           stage = 0;
           phase ^= 1u;
@@ -111,42 +119,65 @@ __global__ void __launch_bounds__(kRrThreads, 1) rowres_kernel(MatrixArgs a) {
     }
     int stage = 0, buf = 0;
     unsigned phase = 0;
-    for (long long i = r0; i < r1; ++i) {
+    for (long long i0 = r0; i0 < r1; i0 += R) {
       rr_wait(&full[stage], phase);
-      const float* row = ring + (size_t)stage * C;
-      float4 av[K];
-      float part = 0.f;
+      const float* rows = ring + (size_t)stage * R * C;
+      const int nr = (r1 - i0) < R ? (int)(r1 - i0) : R;
+      // pass 1: A_i . x for the stage's rows (rows stay in shared memory)
+      float part[R];
 #pragma unroll
-      for (int k = 0; k < K; ++k) {
-        av[k] = ok[k] ? *reinterpret_cast<const float4*>(row + lcol[k]) : make_float4(0.f, 0.f, 0.f, 0.f);
-        part = fmaf(av[k].x, xs[k].x, part);
-        part = fmaf(av[k].y, xs[k].y, part);
-        part = fmaf(av[k].z, xs[k].z, part);
-        part = fmaf(av[k].w, xs[k].w, part);
+      for (int rr = 0; rr < R; ++rr) {
+        part[rr] = 0.f;
+        if (rr >= nr) continue;
+        const float* row = rows + (size_t)rr * a.n;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          if (!ok[k]) continue;
+          const float4 v = *reinterpret_cast<const float4*>(row + lcol[k]);
+          part[rr] = fmaf(v.x, xs[k].x, part[rr]);
+          part[rr] = fmaf(v.y, xs[k].y, part[rr]);
+          part[rr] = fmaf(v.z, xs[k].z, part[rr]);
+          part[rr] = fmaf(v.w, xs[k].w, part[rr]);
+        }
+      }
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) part[rr] += __shfl_xor_sync(0xffffffffu, part[rr], off);
+        if (lane == 0) red[buf][warp][rr] = part[rr];
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(kRrConsumers) : "memory");
+      float ti[R];
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) {
+        float s = red[buf][0][rr];
+#pragma unroll
+        for (int w = 1; w < kRrWarps; ++w) s += red[buf][w][rr];
+        // t_i rounded to fp32 exactly as the unfused plan stores it
+        ti[rr] = (float)(a.ar[0] * (double)s);
+        if (tid == 0 && a.yr[0] && rr < nr) a.yr[0][i0 + rr] = ti[rr];
+      }
+      buf ^= 1;
+      // pass 2: accumulate A_i^T t_i into the register column accumulators
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) {
+        if (rr >= nr) continue;
+        const float* row = rows + (size_t)rr * a.n;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          if (!ok[k]) continue;
+          const float4 v = *reinterpret_cast<const float4*>(row + lcol[k]);
+          cacc[k][0] = fmaf(v.x, ti[rr], cacc[k][0]);
+          cacc[k][1] = fmaf(v.y, ti[rr], cacc[k][1]);
+          cacc[k][2] = fmaf(v.z, ti[rr], cacc[k][2]);
+          cacc[k][3] = fmaf(v.w, ti[rr], cacc[k][3]);
+        }
       }
       __syncwarp();
-      if (lane == 0) rr_arrive(&empty[stage]);  // row now lives in registers
+      if (lane == 0) rr_arrive(&empty[stage]);  // this warp is done with the stage
       if (++stage == kRrStages) {
         stage = 0;
         phase ^= 1u;
-      }
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
-      if (lane == 0) red[buf][warp] = part;
-      asm volatile("bar.sync 1, %0;" ::"n"(kRrConsumers) : "memory");
-      float s = red[buf][0];
-#pragma unroll
-      for (int w = 1; w < kRrWarps; ++w) s += red[buf][w];
-      buf ^= 1;
-      // t_i rounded to fp32 exactly as the unfused plan stores it
-      const float ti = (float)(a.ar[0] * (double)s);
-      if (tid == 0 && a.yr[0]) a.yr[0][i] = ti;
-#pragma unroll
-      for (int k = 0; k < K; ++k) {
-        cacc[k][0] = fmaf(av[k].x, ti, cacc[k][0]);
-        cacc[k][1] = fmaf(av[k].y, ti, cacc[k][1]);
-        cacc[k][2] = fmaf(av[k].z, ti, cacc[k][2]);
-        cacc[k][3] = fmaf(av[k].w, ti, cacc[k][3]);
       }
     }
     float* colpart = static_cast<float*>(a.colpart);
@@ -163,16 +194,17 @@ __global__ void __launch_bounds__(kRrThreads, 1) rowres_kernel(MatrixArgs a) {
 
 using RrFn = void (*)(MatrixArgs);
 
+// stage ~64 KB: R rows of the CTA's column span
 RrFn rowres_fn(long long n) {
-  if (n <= 4LL * kRrConsumers * 2) return rowres_kernel<2>;
-  if (n <= 4LL * kRrConsumers * 4) return rowres_kernel<4>;
-  if (n <= 4LL * kRrConsumers * 8) return rowres_kernel<8>;
+  if (n <= 4LL * kRrConsumers * 2) return rowres_kernel<2, 4>;
+  if (n <= 4LL * kRrConsumers * 4) return rowres_kernel<4, 2>;
+  if (n <= 4LL * kRrConsumers * 8) return rowres_kernel<8, 1>;
   return nullptr;
 }
 
 size_t rowres_smem(long long n) {
-  const long long C = n <= 4096 ? 4096 : (n <= 8192 ? 8192 : 16384);
-  return (size_t)kRrStages * C * 4 + 2 * kRrStages * 8 + 128;
+  (void)n;
+  return (size_t)kRrStages * 16384 * 4 + 2 * kRrStages * 8 + 128;  // R*C = 16384 floats
 }
 
 }  // namespace

@@ -48,8 +48,8 @@ def time_plan(plan, bufs, reps=7):
     return statistics.median(ts)
 
 
-def run(seq, m, n, settings):
-    plan = mf.Plan.sequence(seq, m, n, "fused")
+def run(seq, m, n, settings, mode="fused"):
+    plan = mf.Plan.sequence(seq, m, n, mode)
     d = plan.describe()
     byts = d["bytes_loaded"] + d["bytes_stored"]
     bufs = make(plan)
@@ -57,7 +57,7 @@ def run(seq, m, n, settings):
         for k, v in st.items():
             mf.set_option(k, v)
         ms = time_plan(plan, bufs)
-        print("%-8s %-42s %9.1f us %7.0f GB/s  %.3f" % (seq, st, ms * 1e3, byts / ms / 1e6,
+        print("%-8s %-6s %-42s %9.1f us %7.0f GB/s  %.3f" % (seq, mode, st, ms * 1e3, byts / ms / 1e6,
                                                       byts / ms / 1e6 / PEAK), flush=True)
     del bufs
     torch.cuda.empty_cache()
@@ -76,3 +76,7 @@ if which in ("matrix", "all"):
     for seq, m, n in (("BICGK", 16384, 16384), ("ATAX", 16384, 16384), ("GESUMMV", 32768, 32768),
                       ("GEMVER", 32768, 32768), ("BICGK", 4096, 131072)):
         run(seq, m, n, st)
+if which in ("rowres", "all"):
+    for m, n in ((16384, 16384), (8192, 16384), (16384, 8192), (32768, 4096)):
+        for mode in ("fused", "b200"):
+            run("ATAX", m, n, [{"tma": -1}], mode)

@@ -26,11 +26,11 @@ CostModel CostModel::defaults() {
   // measured on B200 (round 1): fraction of the 6545.6 GB/s copy bandwidth
   cm.eta = {
       {"stream", 0.98},            // VADD 0.99, WAXPBY 0.96, AXPYDOT 1.00
-      {"matrix.ldg.read", 1.02},   // BiCGK 1.00, ATAX 1.04, GESUMMV 1.12
+      {"matrix.ldg.read", 1.04},   // BiCGK 1.03, ATAX 1.05, GESUMMV 1.12
       {"matrix.tma.read", 0.95},   // BiCGK 0.92-0.97
       {"matrix.ldg.rank", 0.62},   // GEMVER ger2+sgemtv, register-fed
-      {"matrix.tma.rank", 0.95},   // GEMVER ger2+sgemtv, TMA ring
-      {"matrix.rowres", 0.90},     // row-resident chain (ATAX one pass), estimate
+      {"matrix.tma.rank", 0.97},   // GEMVER ger2+sgemtv, TMA ring, 16 consumer warps
+      {"matrix.rowres", 0.88},     // row-resident chain (ATAX one pass, 16384^2)
   };
   if (const char* f = std::getenv("MF_COST_DB")) {
     std::ifstream in(f);

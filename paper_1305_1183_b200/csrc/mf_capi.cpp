@@ -478,6 +478,9 @@ int mf_set_option(const char* key, int value) {
     } else if (k == "stream_ctas_per_sm") {
       if (value < 1 || value > 8) throw Invalid("stream_ctas_per_sm: 1..8");
       options().stream_ctas_per_sm = value;
+    } else if (k == "tma_consumers") {
+      if (value != 0 && value != 256 && value != 512) throw Invalid("tma_consumers: 0|256|512");
+      options().tma_consumers = value;
     } else if (k == "max_sms") {
       if (value < 0) throw Invalid("max_sms >= 0");
       options().max_sms = value;
@@ -499,6 +502,7 @@ int mf_get_option(const char* key) {
   if (k == "occupancy") return options().occupancy;
   if (k == "tma") return options().tma;
   if (k == "max_sms") return options().max_sms;
+  if (k == "tma_consumers") return options().tma_consumers;
   if (k == "stream_unroll") return options().stream_unroll;
   if (k == "stream_ctas_per_sm") return options().stream_ctas_per_sm;
   return -1;

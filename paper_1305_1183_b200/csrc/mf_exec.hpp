@@ -39,6 +39,7 @@ struct EngineOptions {
   int stream_ctas_per_sm = 4;
   int tma = -1;  // matrix kernels: -1 auto (by shape), 1 = TMA ring, 0 = register-fed
   int max_sms = 0;  // > 0: cap the SMs a matrix kernel's grid is sized for
+  int tma_consumers = 0;  // TMA matrix variant: 0 auto (by shape), 256 or 512 consumer threads
 };
 
 // A row-sharding group's in-kernel exchange buffers (see PeerLinks).

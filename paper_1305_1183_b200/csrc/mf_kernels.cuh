@@ -75,6 +75,7 @@ struct MatrixTuning {
   bool f64acc = false; // accumulate reductions in fp64
   int occupancy = 2;   // CTAs per SM targeted (register-fed variant)
   bool tma = true;     // TMA/mbarrier shared-memory ring (mf_matrix_tma.cu)
+  int consumers = 256; // TMA variant: consumer threads per CTA (256 | 512)
 };
 
 // Launchers; return cudaSuccess or the launch error.  `sms` = SM count.

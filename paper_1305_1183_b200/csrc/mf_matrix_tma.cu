@@ -25,9 +25,7 @@ namespace {
 
 using namespace dev;
 
-constexpr int kConsumers = 256;
-constexpr int kConsumerWarps = kConsumers / 32;
-constexpr int kTmaThreads = kConsumers + 32;  // + 1 producer warp
+// consumer threads per CTA: 256 (8 warps) or 512 (16 warps) + 1 producer warp
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
@@ -62,8 +60,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }
+template <int NC>
 __device__ __forceinline__ void consumers_sync() {
-  asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
+  asm volatile("bar.sync 1, %0;" ::"n"(NC) : "memory");
 }
 
 // Bands start on multiples of R so every per-row vector slice is 16-byte
@@ -75,8 +74,11 @@ __device__ __forceinline__ void band(const MatrixArgs& a, int rb, int R, long lo
   *r1 = (long long)(rb + 1) * units / a.RB * R;
 }
 
-template <int NMAT, int NRANK, bool STORE, int NROW, int NCOL, int K, int R, typename ACC>
-__global__ void __launch_bounds__(kTmaThreads, 1) matrix_tma_kernel(MatrixArgs a, int S) {
+template <int NMAT, int NRANK, bool STORE, int NROW, int NCOL, int K, int R, typename ACC, int NC>
+__global__ void __launch_bounds__(NC + 32, 1) matrix_tma_kernel(MatrixArgs a, int S) {
+  constexpr int kConsumers = NC;
+  constexpr int kConsumerWarps = NC / 32;
+  constexpr int kTmaThreads = NC + 32;
   static_assert(R >= 4, "bulk copies of per-row slices need R >= 4");
   constexpr int NV = (NROW > 0 ? NROW : 1) * R;
   constexpr int C = 4 * kConsumers * K;
@@ -244,7 +246,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) matrix_tma_kernel(MatrixArgs a
           ACC wsum = butterfly<ACC, NV>(rp, lane);
           constexpr int group = 32 / NV;
           if ((lane & (group - 1)) == 0) red[buf][warp][lane / group] = wsum;
-          consumers_sync();
+          consumers_sync<NC>();
           if (tid < NV) {
             ACC s = red[buf][0][tid];
 #pragma unroll
@@ -281,9 +283,10 @@ using TmaFn = void (*)(MatrixArgs, int);
 
 template <int NMAT, int NRANK, bool STORE, int NROW, int NCOL>
 TmaFn pick_tma(const MatrixTuning& t) {
-  if (t.f64acc) return matrix_tma_kernel<NMAT, NRANK, STORE, NROW, NCOL, 2, 4, double>;
-  if (t.K == 4) return matrix_tma_kernel<NMAT, NRANK, STORE, NROW, NCOL, 4, 4, float>;
-  return matrix_tma_kernel<NMAT, NRANK, STORE, NROW, NCOL, 2, 4, float>;
+  if (t.f64acc) return matrix_tma_kernel<NMAT, NRANK, STORE, NROW, NCOL, 2, 4, double, 256>;
+  if (t.consumers == 512) return matrix_tma_kernel<NMAT, NRANK, STORE, NROW, NCOL, 2, 4, float, 512>;
+  if (t.K == 4) return matrix_tma_kernel<NMAT, NRANK, STORE, NROW, NCOL, 4, 4, float, 256>;
+  return matrix_tma_kernel<NMAT, NRANK, STORE, NROW, NCOL, 2, 4, float, 256>;
 }
 
 TmaFn tma_fn(const MatrixShape& s, const MatrixTuning& t) {
@@ -298,8 +301,16 @@ TmaFn tma_fn(const MatrixShape& s, const MatrixTuning& t) {
   return nullptr;
 }
 
-size_t tma_stage_bytes(const MatrixShape& s, int K) {
-  const size_t R = 4, C = 4 * kConsumers * (size_t)K;
+// columns one CTA covers (the chunk width) and threads per CTA
+long long tma_chunk(const MatrixTuning& t) {
+  if (t.f64acc) return 4LL * 256 * 2;
+  if (t.consumers == 512) return 4LL * 512 * 2;
+  return 4LL * 256 * (t.K == 4 ? 4 : 2);
+}
+int tma_threads(const MatrixTuning& t) { return (!t.f64acc && t.consumers == 512 ? 512 : 256) + 32; }
+
+size_t tma_stage_bytes(const MatrixShape& s, const MatrixTuning& t) {
+  const size_t R = 4, C = (size_t)tma_chunk(t);
   return (size_t)s.nmat * R * C * 4 + (size_t)(s.ncol + s.nrank) * R * 4;
 }
 
@@ -307,19 +318,16 @@ size_t tma_stage_bytes(const MatrixShape& s, int K) {
 
 int tma_stages(const MatrixShape& sh, const MatrixTuning& t) {
   const size_t budget = 200 * 1024;
-  const int K = t.f64acc ? 2 : (t.K == 4 ? 4 : 2);
-  return (int)std::max<size_t>(2, std::min<size_t>(8, budget / tma_stage_bytes(sh, K)));
+  return (int)std::max<size_t>(2, std::min<size_t>(8, budget / tma_stage_bytes(sh, t)));
 }
 
 bool tma_supported(const MatrixShape& sh, const MatrixTuning& t) {
-  const int K = t.f64acc ? 2 : (t.K == 4 ? 4 : 2);
-  return tma_fn(sh, t) != nullptr && 2 * tma_stage_bytes(sh, K) <= 200 * 1024;
+  return tma_fn(sh, t) != nullptr && 2 * tma_stage_bytes(sh, t) <= 200 * 1024;
 }
 
 size_t tma_smem_bytes(const MatrixShape& sh, const MatrixTuning& t) {
-  const int K = t.f64acc ? 2 : (t.K == 4 ? 4 : 2);
   const int S = tma_stages(sh, t);
-  return (size_t)S * tma_stage_bytes(sh, K) + 16 + 2 * (size_t)S * 8 + 128;
+  return (size_t)S * tma_stage_bytes(sh, t) + 16 + 2 * (size_t)S * 8 + 128;
 }
 
 cudaError_t matrix_tma_config(const MatrixShape& sh, const MatrixTuning& t, long long m,
@@ -331,11 +339,10 @@ cudaError_t matrix_tma_config(const MatrixShape& sh, const MatrixTuning& t, long
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kTmaThreads, smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, tma_threads(t), smem);
   if (e != cudaSuccess) return e;
   per_sm = std::max(1, per_sm);
-  const int K = t.f64acc ? 2 : (t.K == 4 ? 4 : 2);
-  const long long C = 4LL * kConsumers * K;
+  const long long C = tma_chunk(t);
   const int CB = (int)((n + C - 1) / C);
   const long long G = (long long)sms * per_sm;
   const long long units = m / 4;  // R = 4 row units
@@ -374,9 +381,9 @@ cudaError_t launch_matrix_tma(const MatrixShape& sh, const MatrixTuning& t, cons
   MatrixArgs copy = a;
   void* args[] = {&copy, &S};
   if (needs_barrier)
-    return cudaLaunchCooperativeKernel((const void*)fn, dim3(grid), dim3(kTmaThreads), args, smem,
-                                       s);
-  fn<<<grid, kTmaThreads, smem, s>>>(copy, S);
+    return cudaLaunchCooperativeKernel((const void*)fn, dim3(grid), dim3(tma_threads(t)), args,
+                                       smem, s);
+  fn<<<grid, tma_threads(t), smem, s>>>(copy, S);
   return cudaGetLastError();
 }
 

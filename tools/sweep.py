@@ -71,11 +71,13 @@ if which in ("stream", "all"):
     mf.set_option("stream_unroll", 0)
     mf.set_option("stream_ctas_per_sm", 4)
 if which in ("matrix", "all"):
-    st = [{"tma": -1, "matrix_k": 2}, {"tma": 0, "matrix_k": 2}, {"tma": 0, "matrix_k": 4},
-          {"tma": 1, "matrix_k": 2}, {"tma": 1, "matrix_k": 4}]
+    st = [{"tma": -1, "matrix_k": 2, "tma_consumers": 0}, {"tma": 0, "matrix_k": 2},
+          {"tma": 0, "matrix_k": 4}, {"tma": 1, "matrix_k": 2}, {"tma": 1, "matrix_k": 4},
+          {"tma": 1, "matrix_k": 2, "tma_consumers": 512}, {"tma": -1, "matrix_k": 2, "tma_consumers": 512}]
     for seq, m, n in (("BICGK", 16384, 16384), ("ATAX", 16384, 16384), ("GESUMMV", 32768, 32768),
                       ("GEMVER", 32768, 32768), ("BICGK", 4096, 131072)):
         run(seq, m, n, st)
+    mf.set_option("tma_consumers", 0)
 if which in ("rowres", "all"):
     for m, n in ((16384, 16384), (8192, 16384), (16384, 8192), (32768, 4096)):
         for mode in ("fused", "b200"):

@@ -99,6 +99,23 @@ kernel::KernelIR generate_kernel(const std::vector<int>& calls, const script::Sc
 // KernelIR -> the sm_100a kernel family and its operand roles.  Throws
 // std::invalid_argument when no hand-written template covers the kernel.
 b200::NativeKernel lower_kernel(const kernel::KernelIR& k);
+// Generic path: KernelIR -> CUDA C++ that executes it with
+// the reference VM's semantics (proj/src/vm.cpp:357-445), one CTA per VM
+// block.  Throws std::invalid_argument for a KernelIR the VM would reject
+// statically (unexpanded macro, barrier inside a body, unknown region).
+b200::NativeKernel generic_kernel(const kernel::KernelIR& k);
+// lower_kernel when a hand-written family covers the kernel, else the
+// generic kernel (or always generic with engine option "generic" = 1).
+b200::NativeKernel lower_or_generic(const kernel::KernelIR& k);
+// Engine option "generic" (env MF_GENERIC): route every kernel to the
+// generic path (tests, and the measured cost of the generic emitter).
+void set_force_generic(bool on);
+bool force_generic();
+// Engine option "generic_iterations": 0 = chosen per problem size
+// (generic_params), >= 1 = fixed serial iterations for generic kernels.
+void set_generic_iterations(int n);
+int generic_iterations();
+CodegenParams generic_params(const kernel::KernelIR& k, Sizes sz);
 bool stream_template_exists(int nin, int nout, bool dot);
 bool matrix_template_exists(int nmat, int nrank, int store, int nrow, int ncol);
 

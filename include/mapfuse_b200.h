@@ -127,6 +127,23 @@ int mf_launch(const mf_plan* plan, const mf_buffer* buffers, int nbuf, const mf_
 int mf_launch_kernel(const mf_plan* plan, int k, const mf_buffer* buffers, int nbuf,
                      const mf_scalar* scalars, int nscalars, void* stream, mf_stats* stats);
 
+/* CUDA C++ source of kernel k when it runs on the generic path (the code
+ * generator's output for KernelIRs no hand-written family covers); "" for
+ * hand-written kernels.  Size convention as mf_plan_describe. */
+int mf_plan_kernel_source(const mf_plan* plan, int k, char* buf, int cap);
+/* Compiles every generic kernel of the plan for sm_100a now (NVRTC; needs no
+ * GPU), so the first launch does not pay for it.  Returns MF_OK or the
+ * compiler's diagnostics via mf_last_error(). */
+int mf_plan_prepare(const mf_plan* plan);
+
+/* Synchronizes `stream` and reports (MF_ERR_FAULT) the first device fault a
+ * generic kernel of this plan recorded since the last check: out-of-bounds
+ * global or on-chip index, poisoned on-chip read, division by zero -- the
+ * VM's faults (proj/src/vm.cpp:77-81, :102-109, :184-185).  Hand-written
+ * kernels validate everything before launch and never record faults.
+ * mf_launch_host checks by itself. */
+int mf_plan_check(const mf_plan* plan, void* stream);
+
 /* vm::launch's exact contract with host memory: copies inputs host->device,
  * runs the plan, copies every bound output back, synchronizes.  stats->ms is
  * the device time of the kernels alone -- except for element-wise plans over
@@ -160,7 +177,10 @@ int mf_generate(float* dev, int64_t rows, int64_t cols, int64_t ld, uint64_t see
                 int64_t ncols_global, void* stream);
 
 /* Engine options: "matrix_k" (2|4 float4 slots per thread), "f64acc" (0|1:
- * accumulate matrix reductions in fp64), "occupancy" (CTAs per SM). */
+ * accumulate matrix reductions in fp64), "occupancy" (CTAs per SM),
+ * "generic" (0|1: run every kernel on the generic NVRTC-emitted path, even
+ * where a hand-written family applies), "generic_poison" (0|1: generic
+ * kernels poison on-chip memory and fault on uninitialised reads). */
 int mf_set_option(const char* key, int value);
 int mf_get_option(const char* key);
 

@@ -16,7 +16,10 @@
 #include <vector>
 
 #include "mapfuse/blas.hpp"
+#include "mapfuse/device.hpp"
+#include "mapfuse/kernel.hpp"
 #include "mapfuse/script.hpp"
+#include "mapfuse/vm.hpp"
 
 namespace {
 thread_local std::string g_err;
@@ -142,6 +145,44 @@ int mfr_problem_names(void* h, char* dst, int cap) {
   if (static_cast<int>(s.size()) + 1 > cap) return -static_cast<int>(s.size() + 1);
   std::memcpy(dst, s.c_str(), s.size() + 1);
   return 0;
+}
+
+// Runs the reference's virtual SIMT device, vm::launch (proj/src/vm.cpp:450-479),
+// on a KernelIR given in its text form (kernel::parse_kernel_text,
+// proj/src/kernel.cpp:178-280), with the default device config
+// (blas::default_device_config_text).  Buffers are host arrays updated in
+// place, exactly as LaunchArgs binds them (vm.hpp:25-35).  trace != 0 also
+// runs the race detector; *hazards receives the hazard count.  Returns 0,
+// 1 for a VmFault / parse error (message via mfr_last_error).
+int mfr_vm_launch(const char* kernel_text, int nbuf, const char* const* names, const int* rows,
+                  const int* cols, float* const* data, int nsc, const char* const* sc_names,
+                  const float* sc_values, int poison, int trace, long* hazards,
+                  unsigned long long* words_loaded, unsigned long long* words_stored) {
+  try {
+    namespace vm = mapfuse::vm;
+    const mapfuse::kernel::KernelIR k = mapfuse::kernel::parse_kernel_text(kernel_text);
+    const vm::DeviceConfig dev =
+        vm::parse_device_config(mapfuse::blas::default_device_config_text());
+    std::vector<std::vector<float>> store(static_cast<size_t>(nbuf));
+    vm::LaunchArgs args;
+    for (int i = 0; i < nbuf; ++i) {
+      const size_t n = static_cast<size_t>(rows[i]) * static_cast<size_t>(cols[i]);
+      store[i].assign(data[i], data[i] + n);
+      args.buffers[names[i]] = vm::GlobalBuffer{rows[i], cols[i], &store[i]};
+    }
+    for (int j = 0; j < nsc; ++j) args.scalars[sc_names[j]] = sc_values[j];
+    args.poison_onchip = poison != 0;
+    args.trace = trace != 0;
+    const vm::LaunchResult r = vm::launch(k, dev, args);
+    for (int i = 0; i < nbuf; ++i) std::memcpy(data[i], store[i].data(), sizeof(float) * store[i].size());
+    if (hazards) *hazards = static_cast<long>(r.races.hazards.size());
+    if (words_loaded) *words_loaded = r.stats.global_words_loaded;
+    if (words_stored) *words_stored = r.stats.global_words_stored;
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
 }
 
 const char* mfr_manifest() {

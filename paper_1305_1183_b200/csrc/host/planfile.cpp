@@ -91,7 +91,7 @@ b200::NativePlan load_plan(const std::string& text) {
         body += l + "\n";
       }
       if (!closed) throw std::invalid_argument("plan file: kernel '" + name + "' not terminated");
-      b200::NativeKernel nk = lower_kernel(kernel::parse_kernel_text(body));
+      b200::NativeKernel nk = lower_or_generic(kernel::parse_kernel_text(body));
       nk.name = name;
       nk.variant_tma = tma;
       nk.variant_k = kk;

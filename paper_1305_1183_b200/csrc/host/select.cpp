@@ -31,6 +31,9 @@ CostModel CostModel::defaults() {
       {"matrix.ldg.rank", 0.62},   // GEMVER ger2+sgemtv, register-fed
       {"matrix.tma.rank", 0.97},   // GEMVER ger2+sgemtv, TMA ring, 16 consumer warps
       {"matrix.rowres", 0.88},     // row-resident chain (ATAX one pass, 16384^2)
+      {"generic.d1", 0.45},        // NVRTC-emitted KernelIR (host/cudagen.cpp), depth 1:
+                                   //   VADD 0.55, AXPYDOT 0.34 (profiles/r01_generic_sweep.txt)
+      {"generic.d2", 0.25},        // ... depth 2: BiCGK 0.20, GESUMMV 0.24, ATAX 0.28, GEMVER 0.34
   };
   if (const char* f = std::getenv("MF_COST_DB")) {
     std::ifstream in(f);
@@ -49,6 +52,8 @@ double CostModel::predict_us(b200::NativeKernel& k, int64_t m, int64_t n) const 
     return bytes / ((it == eta.end() ? 0.9 : it->second) * bw) + dev.launch_us;
   };
   if (k.kind == b200::NativeKernel::Kind::Stream) return t("stream");
+  if (k.kind == b200::NativeKernel::Kind::Generic)
+    return t(k.generic.depth == 1 ? "generic.d1" : "generic.d2");
   if (k.matrix.chain) return t("matrix.rowres");
   const bool heavy = !k.matrix.rank.empty() || !k.matrix.store.empty();
   const double ldg = t(heavy ? "matrix.ldg.rank" : "matrix.ldg.read");
@@ -61,6 +66,45 @@ double CostModel::predict_us(b200::NativeKernel& k, int64_t m, int64_t n) const 
   k.variant_tma = 0;
   k.variant_k = 2;
   return ldg;
+}
+
+// Serial iterations for a generic kernel (the paper's ITERS parameter,
+// PAPER.md:259).  Each block loops over `iterations` instances, so
+// accumulators invariant across iterations are cleared once and added to
+// global memory once per block instead of once per tile.  Measured on B200
+// (tools/generic_sweep.py, profiles/r01_generic_sweep.txt): ~4 for depth-2
+// kernels with accumulators, 1 for depth-2 maps, ~16 for depth-1.
+//
+// The iteration count must DIVIDE the iterated grid extent: the epilogue
+// runs with it = iterations-1, and an instance beyond the grid skips every
+// call (vm.cpp:381-399) -- so with a ragged last band the
+// epilogue's stores of the invariant accumulators would be dropped (the
+// reference VM drops them too).  For the same reason depth-1 kernels iterate
+// only when the element count fills every instance of every block.
+// Option "generic_iterations" (>= 1) fixes the count (still made a divisor).
+CodegenParams generic_params(const kernel::KernelIR& k, Sizes sz) {
+  CodegenParams p;
+  bool accumulates = false;
+  for (const auto* sec : {&k.prologue, &k.epilogue})
+    for (const auto& c : *sec) accumulates = accumulates || !c.is_pure_clear() || !c.clear_key.empty();
+  int64_t limit = 1, blocks_per_band = 1;
+  if (k.depth == 2) {
+    limit = std::max<int64_t>(1, sz.rows / 32);  // iterate y
+    blocks_per_band = std::max<int64_t>(1, sz.cols / 32);
+  } else {
+    const int64_t elems = std::max<int64_t>(1, std::max<int64_t>(sz.cols, sz.rows) / 32);
+    const int inst = std::max(1, std::min(4, k.instances));
+    if (elems % inst != 0) return p;
+    limit = elems / inst;
+  }
+  const int forced = generic_iterations();
+  int64_t want = forced >= 1 ? forced : (k.depth == 1 ? 16 : (accumulates ? 4 : 1));
+  // keep >= 4 blocks per SM (148 SMs)
+  while (want > 1 && (limit / want) * blocks_per_band < 148 * 4 && forced < 1) want /= 2;
+  int64_t it = std::max<int64_t>(1, std::min(want, limit));
+  while (limit % it) --it;  // largest divisor of the grid extent <= want
+  p.iterations = static_cast<int>(it);
+  return p;
 }
 
 namespace {
@@ -80,11 +124,20 @@ std::vector<Candidate> candidates(const script::Script& s, const script::DataDep
     try {
       c.item.calls = calls;
       c.item.kir = generate_kernel(calls, s, g, L);
-      c.item.native = lower_kernel(c.item.kir);
+      c.item.native = lower_or_generic(c.item.kir);
+      if (c.item.native.kind == b200::NativeKernel::Kind::Generic) {
+        // generic kernels execute the KernelIR as written: pick the
+        // implementation parameters (serial iterations) for this size
+        const CodegenParams prm = generic_params(c.item.kir, sz);
+        if (prm.iterations != c.item.kir.iterations) {
+          c.item.kir = generate_kernel(calls, s, g, L, prm);
+          c.item.native = generic_kernel(c.item.kir);
+        }
+      }
       c.item.predicted_us = cm.predict_us(c.item.native, sz.rows, sz.cols);
     } catch (const std::invalid_argument& e) {
       if (must) throw std::invalid_argument("call " + std::to_string(calls[0]) + ": " + e.what());
-      return;  // infeasible implementation: no sm_100a template covers it
+      return;  // infeasible implementation (the generic emitter rejected it too)
     }
     out.push_back(std::move(c));
   };

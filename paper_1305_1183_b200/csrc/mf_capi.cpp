@@ -6,9 +6,11 @@
 #include <memory>
 #include <string>
 
+#include "mapfuse/planner.hpp"
 #include "mf_builtin.hpp"
 #include "mf_compile.hpp"
 #include "mf_exec.hpp"
+#include "mf_jit.hpp"
 #include "mf_kernels.cuh"
 
 using namespace mapfuse::b200;
@@ -86,7 +88,15 @@ void fill_stats(const NativePlan& p, int k0, int k1, const BufMap& b, mf_stats* 
   for (int k = k0; k < k1; ++k) {
     const auto& kern = p.kernels[k];
     int64_t m = p.rows, n = p.cols;
-    if (kern.kind == NativeKernel::Kind::Matrix) {
+    if (kern.kind == NativeKernel::Kind::Generic) {
+      auto it = b.find(kern.generic.domain);
+      if (it != b.end()) {
+        m = kern.generic.depth == 2 ? it->second.rows : 1;
+        n = kern.generic.depth == 2 ? it->second.cols : it->second.size();
+      }
+      st->bytes_loaded += kern.bytes_loaded(m, n);
+      st->bytes_stored += kern.bytes_stored(m, n);
+    } else if (kern.kind == NativeKernel::Kind::Matrix) {
       auto it = b.find(kern.matrix.mats[0]);
       if (it != b.end()) {
         m = it->second.rows;
@@ -321,6 +331,36 @@ int mf_launch_kernel(const mf_plan* plan, int k, const mf_buffer* buffers, int n
   });
 }
 
+int mf_plan_kernel_source(const mf_plan* plan, int k, char* buf, int cap) {
+  std::string s;
+  const int rc = guarded([&] {
+    if (!plan) throw Invalid("null plan");
+    if (k < 0 || k >= (int)plan->plan.kernels.size()) throw Invalid("kernel index out of range");
+    const auto& kern = plan->plan.kernels[k];
+    if (kern.kind == NativeKernel::Kind::Generic) s = kern.generic.source;
+  });
+  return rc == MF_OK ? copy_out(s, buf, cap) : -rc;
+}
+
+int mf_plan_prepare(const mf_plan* plan) {
+  return guarded([&] {
+    if (!plan) throw Invalid("null plan");
+    for (const auto& kern : plan->plan.kernels)
+      if (kern.kind == NativeKernel::Kind::Generic) {
+        const bool poison =
+            kern.generic_poison >= 0 ? kern.generic_poison != 0 : options().generic_poison != 0;
+        jit_prepare(kern.generic.source, poison);
+      }
+  });
+}
+
+int mf_plan_check(const mf_plan* plan, void* stream) {
+  return guarded([&] {
+    if (!plan) throw Invalid("null plan");
+    check_jit_faults(plan->ws, static_cast<cudaStream_t>(stream));
+  });
+}
+
 int mf_launch_host(const mf_plan* plan, const mf_buffer* host_buffers, int nbuf,
                    const mf_scalar* scalars, int nscalars, mf_stats* stats) {
   return guarded([&] {
@@ -368,6 +408,7 @@ int mf_launch_host(const mf_plan* plan, const mf_buffer* host_buffers, int nbuf,
                  "cudaMemcpy D2H");
     }
     check_cuda(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+    check_jit_faults(plan->ws, st);
     float ms = 0.f;
     cudaEventElapsedTime(&ms, e0, e1);
     cudaEventDestroy(e0);
@@ -489,6 +530,13 @@ int mf_set_option(const char* key, int value) {
     } else if (k == "occupancy") {
       if (value < 1 || value > 8) throw Invalid("occupancy must be 1..8");
       options().occupancy = value;
+    } else if (k == "generic") {
+      mapfuse::plan::set_force_generic(value != 0);
+    } else if (k == "generic_iterations") {
+      if (value < 0 || value > 4096) throw Invalid("generic_iterations: 0 (auto) .. 4096");
+      mapfuse::plan::set_generic_iterations(value);
+    } else if (k == "generic_poison") {
+      options().generic_poison = value ? 1 : 0;
     } else {
       throw Invalid("unknown option '" + k + "'");
     }
@@ -505,6 +553,9 @@ int mf_get_option(const char* key) {
   if (k == "tma_consumers") return options().tma_consumers;
   if (k == "stream_unroll") return options().stream_unroll;
   if (k == "stream_ctas_per_sm") return options().stream_ctas_per_sm;
+  if (k == "generic") return mapfuse::plan::force_generic() ? 1 : 0;
+  if (k == "generic_poison") return options().generic_poison;
+  if (k == "generic_iterations") return mapfuse::plan::generic_iterations();
   return -1;
 }
 

@@ -1,6 +1,7 @@
 // mf_compile.cpp -- script / KernelIR text -> NativePlan (C-ABI side).
 #include "mf_compile.hpp"
 
+#include <algorithm>
 #include <stdexcept>
 
 #include "mapfuse/blas.hpp"
@@ -97,7 +98,7 @@ NativePlan plan_from_kernel_text(const std::string& text, int rows, int cols) {
     p.rows = (rows + 31) / 32 * 32;
     p.cols = (cols + 31) / 32 * 32;
     p.sequence = k.name;
-    NativeKernel nk = plan::lower_kernel(k);
+    NativeKernel nk = plan::lower_or_generic(k);
     nk.name = k.name;
     plan::CostModel::defaults().predict_us(nk, p.rows, p.cols);
     auto add = [&](const std::string& n, int r, int c, Role role, bool rowix) {
@@ -110,7 +111,21 @@ NativePlan plan_from_kernel_text(const std::string& text, int rows, int cols) {
       b.row_indexed = rowix;
       p.buffers.push_back(b);
     };
-    if (nk.kind == NativeKernel::Kind::Matrix) {
+    if (nk.kind == NativeKernel::Kind::Generic) {
+      // shapes follow the index expressions; the kernel bounds-checks every
+      // access against the bound shapes at run time, as the VM does
+      const GenericOp& g = nk.generic;
+      const bool d2 = g.depth == 2;
+      for (size_t i = 0; i < g.buffers.size(); ++i) {
+        const std::string& b = g.buffers[i];
+        const bool out = std::find(g.outputs.begin(), g.outputs.end(), b) != g.outputs.end();
+        const char e = b == g.domain ? (d2 ? 't' : 'n') : g.extent[i];
+        const int r = e == 't' && d2 ? p.rows : 1;
+        const int c = e == '1' ? 1 : (e == 'm' ? p.rows : p.cols);
+        add(b, r, c, out ? Role::Output : Role::Input, e == 'm');
+        if (e == '1') p.buffers.back().scalar = true;
+      }
+    } else if (nk.kind == NativeKernel::Kind::Matrix) {
       const MatrixOp& op = nk.matrix;
       for (const auto& m : op.mats) add(m, p.rows, p.cols, Role::Input, false);
       for (const auto& [u, v] : op.rank) {

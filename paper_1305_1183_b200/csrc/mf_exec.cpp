@@ -11,6 +11,7 @@
 #include <cstring>
 #include <sstream>
 
+#include "mf_jit.hpp"
 #include "mf_kernels.cuh"
 
 namespace mapfuse::b200 {
@@ -26,6 +27,7 @@ EngineOptions& options() {
     if (const char* v = std::getenv("MF_STREAM_CTAS")) e.stream_ctas_per_sm = std::atoi(v);
     if (const char* v = std::getenv("MF_MAX_SMS")) e.max_sms = std::atoi(v);
     if (const char* v = std::getenv("MF_TMA_CONSUMERS")) e.tma_consumers = std::atoi(v);
+    if (const char* v = std::getenv("MF_GENERIC_POISON")) e.generic_poison = std::atoi(v);
     return e;
   }();
   return o;
@@ -57,6 +59,7 @@ Workspace::~Workspace() {
   // Best effort: the process may be tearing down the CUDA context already.
   if (scratch_) cudaFree(scratch_);
   if (counters_) cudaFree(counters_);
+  if (jit_fault_) cudaFree(jit_fault_);
   for (auto& [k, v] : named_) cudaFree(v.first);
 }
 
@@ -78,6 +81,14 @@ unsigned* Workspace::counters(cudaStream_t s) {
     check_cuda(cudaMemsetAsync(counters_, 0, 64 * sizeof(unsigned), s), "cudaMemset(counters)");
   }
   return counters_;
+}
+
+unsigned* Workspace::jit_fault(cudaStream_t s) {
+  if (!jit_fault_) {
+    check_cuda(cudaMalloc(&jit_fault_, 2 * sizeof(unsigned)), "cudaMalloc(jit fault)");
+    check_cuda(cudaMemsetAsync(jit_fault_, 0, 2 * sizeof(unsigned), s), "cudaMemset(jit fault)");
+  }
+  return jit_fault_;
 }
 
 float* Workspace::named(const std::string& key, int64_t words) {
@@ -319,7 +330,83 @@ void run_matrix(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc, 
   else check_cuda(launch_matrix(sh, t, a, grid, s), ("launch " + k.name).c_str());
 }
 
+// Generic kernel: one CTA per VM block over the grid the domain buffer
+// implies (proj/src/vm.cpp:24-47, :450-466); see host/cudagen.cpp.
+void run_generic(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc, cudaStream_t s,
+                 Workspace& ws) {
+  const GenericOp& g = k.generic;
+  auto dom = bufs.find(g.domain);
+  if (dom == bufs.end() || !dom->second.ptr)
+    throw Fault("launch: no domain buffer '" + g.domain + "'");
+  const int64_t rows = dom->second.rows, cols = dom->second.cols;
+  auto cdiv = [](int64_t a, int64_t b) { return (a + b - 1) / b; };
+  MfjArgs a{};
+  int64_t launch_x = 0, launch_y = 1;
+  if (g.depth == 2) {
+    if (rows % 32 || cols % 32) throw Fault("launch: domain '" + g.domain + "' not padded to 32");
+    a.full_x = cols / 32;
+    a.full_y = rows / 32;
+    launch_x = g.iter_dim == 'x' ? cdiv(a.full_x, g.iterations) : a.full_x;
+    launch_y = g.iter_dim == 'y' ? cdiv(a.full_y, g.iterations) : a.full_y;
+  } else {
+    const int64_t len = rows == 1 ? cols : rows;
+    if (len % 32) throw Fault("launch: domain '" + g.domain + "' not padded to 32");
+    a.n_elems = len / 32;
+    a.full_x = cdiv(a.n_elems, g.instances);
+    a.full_y = 1;
+    launch_x = cdiv(a.full_x, g.iterations);
+  }
+  for (size_t i = 0; i < g.buffers.size(); ++i) {
+    auto it = bufs.find(g.buffers[i]);
+    if (it == bufs.end() || !it->second.ptr)
+      throw Fault("kernel " + k.name + ": unbound buffer '" + g.buffers[i] + "'");
+    a.buf[i] = it->second.ptr;
+    a.rows[i] = it->second.rows;
+    a.cols[i] = it->second.cols;
+  }
+  for (size_t j = 0; j < g.scalars.size(); ++j) {
+    auto it = sc.find(g.scalars[j]);
+    if (it == sc.end()) throw Fault("kernel " + k.name + ": unbound scalar '" + g.scalars[j] + "'");
+    a.scal[j] = static_cast<float>(it->second);
+  }
+  a.fault = ws.jit_fault(s);
+  if (!k.vm_semantics)  // engine contract: outputs are overwritten, not accumulated into
+    for (const auto& name : g.accumulated) {
+      const DevBuf& b = bufs.at(name);
+      check_cuda(cudaMemsetAsync(b.ptr, 0, sizeof(float) * (size_t)b.size(), s), "zero accumulated output");
+    }
+  if (launch_x == 0 || launch_y == 0) return;
+  if (launch_x > 0x7fffffffLL || launch_y > 65535)
+    throw Fault("kernel " + k.name + ": grid exceeds the device's limits");
+  const size_t smem = sizeof(float) * (size_t)g.shared_words_total;
+  if (smem > 227u * 1024u) throw Fault("vm fault: shared allocation exceeds device limit");
+  const bool poison = k.generic_poison >= 0 ? k.generic_poison != 0 : options().generic_poison != 0;
+  jit_launch(g.source, poison, dim3((unsigned)launch_x, (unsigned)launch_y),
+             dim3((unsigned)(g.block_x * g.block_y)), smem, a, s);
+}
+
 }  // namespace
+
+void check_jit_faults(Workspace& ws, cudaStream_t stream) {
+  if (!ws.jit_used()) return;
+  unsigned h[2] = {0, 0};
+  unsigned* d = ws.jit_fault(stream);
+  check_cuda(cudaMemcpyAsync(h, d, sizeof h, cudaMemcpyDeviceToHost, stream), "read jit fault");
+  check_cuda(cudaStreamSynchronize(stream), "generic kernel");
+  if (h[0] == kJitOk) return;
+  check_cuda(cudaMemsetAsync(d, 0, sizeof h, stream), "reset jit fault");
+  check_cuda(cudaStreamSynchronize(stream), "reset jit fault");
+  const char* what = "fault";
+  switch (h[0]) {
+    case kJitGlobalBounds: what = "global access out of bounds"; break;
+    case kJitOnchipBounds: what = "on-chip access out of element bounds"; break;
+    case kJitPoisonRead: what = "read of uninitialized on-chip word"; break;
+    case kJitDivZero: what = "index expression divides by zero"; break;
+    case kJitBadStep: what = "loop with non-positive step"; break;
+    default: break;
+  }
+  throw Fault(std::string("vm fault: ") + what + " (generic kernel, detail " + std::to_string(h[1]) + ")");
+}
 
 BufMap complete_bindings(const NativePlan& plan, const BufMap& bufs, Workspace& ws) {
   std::lock_guard<std::mutex> lk(ws.mu);
@@ -342,6 +429,7 @@ void run_kernel(const NativePlan& plan, int k, const BufMap& bufs, const ScalarM
   const NativeKernel& kern = plan.kernels[k];
   std::lock_guard<std::mutex> lk(ws.mu);
   if (kern.kind == NativeKernel::Kind::Stream) run_stream(kern, bufs, scalars, stream, ws);
+  else if (kern.kind == NativeKernel::Kind::Generic) run_generic(kern, bufs, scalars, stream, ws);
   else run_matrix(kern, bufs, scalars, stream, ws, peers);
 }
 

@@ -40,6 +40,7 @@ struct EngineOptions {
   int tma = -1;  // matrix kernels: -1 auto (by shape), 1 = TMA ring, 0 = register-fed
   int max_sms = 0;  // > 0: cap the SMs a matrix kernel's grid is sized for
   int tma_consumers = 0;  // TMA matrix variant: 0 auto (by shape), 256 or 512 consumer threads
+  int generic_poison = 0;  // 1: generic kernels poison on-chip memory (VM fault on uninitialised reads)
 };
 
 // A row-sharding group's in-kernel exchange buffers (see PeerLinks).
@@ -68,18 +69,25 @@ class Workspace {
   void* scratch(size_t bytes, cudaStream_t s);   // grows on demand
   unsigned* counters(cudaStream_t s);            // zeroed once, self-resetting
   float* named(const std::string& key, int64_t words);  // persistent per key
+  unsigned* jit_fault(cudaStream_t s);           // generic kernels' fault word pair, zeroed once
+  bool jit_used() const { return jit_fault_ != nullptr; }
   std::mutex mu;
 
  private:
   void* scratch_ = nullptr;
   size_t scratch_bytes_ = 0;
   unsigned* counters_ = nullptr;
+  unsigned* jit_fault_ = nullptr;
   std::map<std::string, std::pair<float*, int64_t>> named_;
 };
 
 // Launches plan.kernels[k]; throws Fault / Invalid.
 void run_kernel(const NativePlan& plan, int k, const BufMap& bufs, const ScalarMap& scalars,
                 cudaStream_t stream, Workspace& ws, PeerGroup* peers = nullptr);
+// Synchronizes `stream` and turns a fault recorded by a generic kernel of
+// this workspace (host/cudagen.cpp: bounds, poisoned read, division by zero)
+// into a Fault -- the VM's VmFault (proj/src/vm.cpp:77-81).  Resets it.
+void check_jit_faults(Workspace& ws, cudaStream_t stream);
 // Binds any plan intermediates the caller left unbound (workspace-backed).
 BufMap complete_bindings(const NativePlan& plan, const BufMap& bufs, Workspace& ws);
 

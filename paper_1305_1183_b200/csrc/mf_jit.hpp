@@ -1,0 +1,44 @@
+// mf_jit.hpp -- NVRTC-compiled generic kernels (host/cudagen.cpp emits them).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+namespace mapfuse::b200 {
+
+// Host mirror of the emitted `struct MfjArgs` (host/cudagen.cpp kPrelude):
+// same member types and order, so the layouts agree.
+constexpr int kMfjMaxBuffers = 64;
+constexpr int kMfjMaxScalars = 32;
+struct MfjArgs {
+  float* buf[kMfjMaxBuffers];
+  long long rows[kMfjMaxBuffers];
+  long long cols[kMfjMaxBuffers];
+  float scal[kMfjMaxScalars];
+  long long full_x, full_y, n_elems;
+  unsigned int* fault;
+};
+
+// Device fault codes written by generic kernels (first fault wins).
+enum JitFault : unsigned {
+  kJitOk = 0,
+  kJitGlobalBounds = 1,
+  kJitOnchipBounds = 2,
+  kJitPoisonRead = 3,
+  kJitDivZero = 4,
+  kJitBadStep = 5,
+};
+
+// Compiles (once per process, cached) and launches on `stream`.
+void jit_launch(const std::string& src, bool poison, dim3 grid, dim3 block, size_t smem,
+                const MfjArgs& args, cudaStream_t stream);
+// NVRTC compile only (no GPU needed): returns the sm_100a cubin; log optional.
+std::vector<char> jit_compile_only(const std::string& src, bool poison, std::string* log);
+// Compiles into the process cache (no GPU needed); later launches reuse it.
+void jit_prepare(const std::string& src, bool poison);
+bool jit_available(std::string* why);
+size_t jit_cache_size();
+
+}  // namespace mapfuse::b200

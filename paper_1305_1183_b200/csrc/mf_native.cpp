@@ -68,6 +68,7 @@ std::string Coef::str() const {
 }
 
 std::vector<std::string> NativeKernel::inputs() const {
+  if (kind == Kind::Generic) return generic.inputs;
   std::vector<std::string> v;
   auto add = [&](const std::string& s) {
     if (!s.empty() && std::find(v.begin(), v.end(), s) == v.end()) v.push_back(s);
@@ -88,6 +89,7 @@ std::vector<std::string> NativeKernel::inputs() const {
 }
 
 std::vector<std::string> NativeKernel::outputs() const {
+  if (kind == Kind::Generic) return generic.outputs;
   std::vector<std::string> v;
   if (kind == Kind::Stream) {
     for (const auto& o : stream.outs) v.push_back(o.name);
@@ -103,6 +105,14 @@ std::vector<std::string> NativeKernel::outputs() const {
 
 std::vector<std::string> NativeKernel::column_outputs() const {
   std::vector<std::string> v;
+  if (kind == Kind::Generic) {  // cross-row (or whole-domain) accumulations
+    for (const auto& a : generic.accumulated) {
+      const auto it = std::find(generic.buffers.begin(), generic.buffers.end(), a);
+      const char e = generic.extent[static_cast<size_t>(it - generic.buffers.begin())];
+      if (e == '1' || (generic.depth == 2 && e == 'n')) v.push_back(a);
+    }
+    return v;
+  }
   if (kind == Kind::Stream) {
     if (stream.has_dot) v.push_back(stream.dot_out);
   } else {
@@ -111,7 +121,20 @@ std::vector<std::string> NativeKernel::column_outputs() const {
   return v;
 }
 
+static uint64_t generic_words(const GenericOp& g, const std::vector<std::string>& names, int64_t m,
+                              int64_t n) {
+  uint64_t w = 0;
+  for (const auto& name : names) {
+    const auto it = std::find(g.buffers.begin(), g.buffers.end(), name);
+    const char e = g.extent[static_cast<size_t>(it - g.buffers.begin())];
+    if (g.depth == 1) w += e == '1' ? 1u : (uint64_t)n;
+    else w += e == 't' ? (uint64_t)(m * n) : (e == 'm' ? (uint64_t)m : (e == 'n' ? (uint64_t)n : 1u));
+  }
+  return w;
+}
+
 uint64_t NativeKernel::bytes_loaded(int64_t m, int64_t n) const {
+  if (kind == Kind::Generic) return 4ull * generic_words(generic, generic.inputs, m, n);
   if (kind == Kind::Stream) return 4ull * (uint64_t)stream.inputs.size() * (uint64_t)n;
   uint64_t b = 4ull * (uint64_t)matrix.mats.size() * (uint64_t)(m * n);
   std::set<std::string> seen;
@@ -127,6 +150,7 @@ uint64_t NativeKernel::bytes_loaded(int64_t m, int64_t n) const {
 }
 
 uint64_t NativeKernel::bytes_stored(int64_t m, int64_t n) const {
+  if (kind == Kind::Generic) return 4ull * generic_words(generic, generic.outputs, m, n);
   if (kind == Kind::Stream)
     return 4ull * (uint64_t)stream.outs.size() * (uint64_t)n + (stream.has_dot ? 4ull : 0ull);
   uint64_t b = matrix.store.empty() ? 0 : 4ull * (uint64_t)(m * n);
@@ -137,24 +161,31 @@ uint64_t NativeKernel::bytes_stored(int64_t m, int64_t n) const {
 }
 
 static int64_t stream_len(const NativePlan& p, const NativeKernel& k) {
+  if (k.kind == NativeKernel::Kind::Generic) {
+    const BufferSpec* b = p.find(k.generic.domain);
+    return b ? (int64_t)b->rows * b->cols : p.cols;
+  }
   const std::string& first = k.stream.inputs.empty() ? std::string() : k.stream.inputs[0];
   const BufferSpec* b = p.find(first);
   return b ? (int64_t)b->rows * b->cols : p.cols;
 }
 
+static bool depth1(const NativeKernel& k) {
+  return k.kind == NativeKernel::Kind::Stream ||
+         (k.kind == NativeKernel::Kind::Generic && k.generic.depth == 1);
+}
+
 uint64_t NativePlan::bytes_loaded() const {
   uint64_t b = 0;
   for (const auto& k : kernels)
-    b += k.kind == NativeKernel::Kind::Stream ? k.bytes_loaded(1, stream_len(*this, k))
-                                              : k.bytes_loaded(rows, cols);
+    b += depth1(k) ? k.bytes_loaded(1, stream_len(*this, k)) : k.bytes_loaded(rows, cols);
   return b;
 }
 
 uint64_t NativePlan::bytes_stored() const {
   uint64_t b = 0;
   for (const auto& k : kernels)
-    b += k.kind == NativeKernel::Kind::Stream ? k.bytes_stored(1, stream_len(*this, k))
-                                              : k.bytes_stored(rows, cols);
+    b += depth1(k) ? k.bytes_stored(1, stream_len(*this, k)) : k.bytes_stored(rows, cols);
   return b;
 }
 
@@ -181,7 +212,10 @@ std::string NativePlan::describe_json() const {
     const auto& k = kernels[i];
     if (i) os << ",";
     os << "{\"name\":" << jstr(k.name) << ",\"kind\":"
-       << (k.kind == NativeKernel::Kind::Stream ? "\"stream\"" : "\"matrix\"") << ",\"calls\":[";
+       << (k.kind == NativeKernel::Kind::Stream
+               ? "\"stream\""
+               : (k.kind == NativeKernel::Kind::Matrix ? "\"matrix\"" : "\"generic\""))
+       << ",\"calls\":[";
     for (size_t j = 0; j < k.calls.size(); ++j) os << (j ? "," : "") << k.calls[j];
     os << "],\"inputs\":[";
     auto in = k.inputs();
@@ -225,6 +259,14 @@ std::string NativePlan::describe_json() const {
       os << "],\"store\":" << jstr(m.store) << ",\"chain\":" << (m.chain ? "true" : "false")
          << ",\"rows\":" << reds(m.rows) << ",\"cols\":" << reds(m.cols)
          << "},\"variant\":{\"tma\":" << k.variant_tma << ",\"k\":" << k.variant_k << "}";
+    } else if (k.kind == NativeKernel::Kind::Generic) {
+      const GenericOp& g = k.generic;
+      os << ",\"op\":{\"depth\":" << g.depth << ",\"block\":[" << g.block_x << "," << g.block_y
+         << "],\"instances\":" << g.instances << ",\"iterations\":" << g.iterations
+         << ",\"domain\":" << jstr(g.domain) << ",\"shared_bytes\":" << 4 * g.shared_words_total
+         << ",\"accumulated\":[";
+      for (size_t t = 0; t < g.accumulated.size(); ++t) os << (t ? "," : "") << jstr(g.accumulated[t]);
+      os << "],\"source_bytes\":" << g.source.size() << "}";
     } else {
       const StreamOp& st = k.stream;
       os << ",\"op\":{\"inputs\":[";
@@ -241,7 +283,7 @@ std::string NativePlan::describe_json() const {
       os << ",\"shape\":{\"mats\":" << k.matrix.mats.size() << ",\"rank\":" << k.matrix.rank.size()
          << ",\"store\":" << (k.matrix.store.empty() ? 0 : 1) << ",\"rows\":" << k.matrix.rows.size()
          << ",\"cols\":" << k.matrix.cols.size() << ",\"chain\":" << (k.matrix.chain ? 1 : 0) << "}";
-    } else {
+    } else if (k.kind == NativeKernel::Kind::Stream) {
       os << ",\"shape\":{\"inputs\":" << k.stream.inputs.size() << ",\"outs\":"
          << k.stream.outs.size() << ",\"dot\":" << (k.stream.has_dot ? 1 : 0) << "}";
     }

@@ -71,12 +71,35 @@ struct MatrixOp {
   bool chain = false;
 };
 
+// Generic kernel: any KernelIR, emitted as CUDA C++ by
+// host/cudagen.cpp following the reference VM's execution semantics
+// (proj/src/vm.cpp:357-445) and JIT-compiled for sm_100a with NVRTC
+// (mf_jit.cpp).  Covers every kernel the hand-written families do not.
+struct GenericOp {
+  std::string source;                // CUDA C++ translation unit (NVRTC input)
+  std::vector<std::string> buffers;  // MfjArgs::buf[i] order
+  std::vector<char> extent;          // per buffer: 't' m x n, 'm', 'n', '1' (traffic accounting)
+  std::vector<std::string> scalars;  // MfjArgs::scal[j] order
+  std::vector<std::string> inputs, outputs;  // global loads / stores (+ atomics)
+  std::vector<std::string> accumulated;      // targets of global atomic adds
+  int depth = 1, block_x = 32, block_y = 1, instances = 1, iterations = 1;
+  char iter_dim = 'x';
+  std::string domain;
+  int shared_words_total = 0;
+};
+
 struct NativeKernel {
-  enum class Kind { Stream, Matrix } kind = Kind::Stream;
+  enum class Kind { Stream, Matrix, Generic } kind = Kind::Stream;
   std::string name;  // e.g. "bicgk_k0[sgemv+sgemtv]"
   std::vector<int> calls;  // script call ids covered
   StreamOp stream;
   MatrixOp matrix;
+  GenericOp generic;
+  // Generic kernels only: true = the reference VM's contract (global atomic
+  // outputs accumulate onto what the caller stored, vm.hpp:91-93); false =
+  // this engine's contract (outputs are overwritten: zeroed before launch).
+  bool vm_semantics = false;
+  int generic_poison = -1;  // generic kernels: -1 engine option, 0 / 1 explicit (LaunchArgs::poison_onchip)
   // implementation variant chosen by the cost model (matrix kernels):
   // tma -1 = engine default, 0 register-fed, 1 TMA ring; k = float4 slots/thread
   int variant_tma = -1;

@@ -11,7 +11,12 @@
 namespace mapfuse::vm {
 
 LaunchResult launch(const kernel::KernelIR& k, const DeviceConfig& dev, const LaunchArgs& args) {
-  (void)dev;  // the virtual-device cost parameters do not apply to real hardware
+  // The virtual device's cost parameters do not apply to real hardware; its
+  // static limits still reject what the reference rejects (vm.cpp:457-460).
+  if (k.threads() > dev.max_threads_per_block)
+    throw VmFault("vm fault: block of " + std::to_string(k.threads()) + " threads exceeds device");
+  if (k.shared_bytes_total() > dev.shared_bytes_per_block)
+    throw VmFault("vm fault: shared allocation exceeds device limit");
   auto dom = args.buffers.find(k.domain);
   if (dom == args.buffers.end()) throw VmFault("launch: domain buffer '" + k.domain + "' is unbound");
   b200::NativePlan plan;
@@ -21,6 +26,11 @@ LaunchResult launch(const kernel::KernelIR& k, const DeviceConfig& dev, const La
   } catch (const std::exception& e) {
     throw VmFault(std::string("launch: ") + e.what());
   }
+  // A kernel no hand-written family covers runs on the generic path with the
+  // VM's own contract: atomic outputs accumulate onto the caller's values
+  // (vm.hpp:91-93) and on-chip memory is poisoned as LaunchArgs asks.
+  plan.kernels[0].vm_semantics = true;
+  plan.kernels[0].generic_poison = args.poison_onchip ? 1 : 0;
   LaunchResult res;
   b200::Workspace ws;
   try {
@@ -47,6 +57,7 @@ LaunchResult launch(const kernel::KernelIR& k, const DeviceConfig& dev, const La
     b200::run_kernel(plan, 0, bufs, sc, nullptr, ws);
     cudaEventRecord(e1, nullptr);
     b200::check_cuda(cudaEventSynchronize(e1), "kernel");
+    b200::check_jit_faults(ws, nullptr);
     float ms = 0;
     cudaEventElapsedTime(&ms, e0, e1);
     cudaEventDestroy(e0);
@@ -74,7 +85,9 @@ LaunchResult launch(const kernel::KernelIR& k, const DeviceConfig& dev, const La
       res.stats.per_buffer[n].stored += w;
       res.stats.global_words_stored += w;
     }
-    res.stats.native_kernel = nk.kind == b200::NativeKernel::Kind::Matrix ? "matrix" : "stream";
+    res.stats.native_kernel = nk.kind == b200::NativeKernel::Kind::Matrix
+                                  ? "matrix"
+                                  : (nk.kind == b200::NativeKernel::Kind::Stream ? "stream" : "generic");
   } catch (const b200::Fault& e) {
     throw VmFault(e.what());
   } catch (const b200::Invalid& e) {

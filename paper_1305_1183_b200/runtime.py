@@ -66,7 +66,8 @@ EXPORTS = [
     "mf_peer_group_create", "mf_peer_group_handle", "mf_peer_group_open",
     "mf_peer_group_connect_local", "mf_peer_group_destroy", "mf_launch_kernel_peers",
     "mf_compile_ranked", "mf_count_combinations", "mf_plan_predicted_us", "mf_plan_save",
-    "mf_plan_load", "mf_sequence_script",
+    "mf_plan_load", "mf_sequence_script", "mf_plan_kernel_source", "mf_plan_prepare",
+    "mf_plan_check",
 ]
 
 
@@ -88,7 +89,7 @@ def lib() -> C.CDLL:
         L.mf_plan_num_kernels.argtypes = [C.c_void_p]
         for fn in ("mf_plan_describe",):
             getattr(L, fn).argtypes = [C.c_void_p, C.c_char_p, C.c_int]
-        for fn in ("mf_plan_kernel_text", "mf_plan_kernel_column_outputs"):
+        for fn in ("mf_plan_kernel_text", "mf_plan_kernel_column_outputs", "mf_plan_kernel_source"):
             getattr(L, fn).argtypes = [C.c_void_p, C.c_int, C.c_char_p, C.c_int]
         L.mf_launch.argtypes = [C.c_void_p, P(MfBuffer), C.c_int, P(MfScalar), C.c_int,
                                 C.c_void_p, P(MfStats)]
@@ -116,6 +117,8 @@ def lib() -> C.CDLL:
         L.mf_plan_save.argtypes = [C.c_void_p, C.c_char_p, C.c_int]
         L.mf_plan_load.argtypes = [C.c_char_p, P(C.c_void_p)]
         L.mf_sequence_script.argtypes = [C.c_char_p, C.c_char_p, C.c_int]
+        L.mf_plan_prepare.argtypes = [C.c_void_p]
+        L.mf_plan_check.argtypes = [C.c_void_p, C.c_void_p]
         L.mf_last_error.restype = C.c_char_p
         L.mf_version.restype = C.c_char_p
         _lib = L
@@ -237,6 +240,20 @@ class Plan:
 
     def kernel_text(self, k: int) -> str:
         return _string(lib().mf_plan_kernel_text, self.h, k)
+
+    def kernel_source(self, k: int) -> str:
+        """CUDA C++ the code generator emitted for kernel k when it runs on the
+        generic (NVRTC) path; "" for hand-written kernels."""
+        return _string(lib().mf_plan_kernel_source, self.h, k)
+
+    def prepare(self) -> None:
+        """Compiles every generic kernel for sm_100a now (no GPU needed)."""
+        _check(lib().mf_plan_prepare(self.h))
+
+    def check(self, stream=None) -> None:
+        """Synchronizes and raises VmFault for a device fault a generic kernel
+        recorded (out-of-bounds index, poisoned read, division by zero)."""
+        _check(lib().mf_plan_check(self.h, _stream_ptr(stream)))
 
     def column_outputs(self, k: int):
         s = _string(lib().mf_plan_kernel_column_outputs, self.h, k)

@@ -1,0 +1,130 @@
+"""Generic path, CPU side.
+
+* host/cudagen.cpp emits CUDA C++ for every kernel the planner can produce
+  (all 11 Table-1 sequences, fused and unfused, forced onto the generic path)
+  and NVRTC compiles each one for sm_100a -- no GPU needed.
+* The code generator's KernelIRs execute race-free on the reference's own
+  virtual SIMT device and reproduce the reference oracle within the
+  tolerance of SURVEY.md 8(c): the semantics the generic kernels reproduce
+  on the GPU (tests/test_gpu_generic.py) are the reference's.
+* User functions outside the hand-written algebra plan onto generic kernels.
+"""
+import numpy as np
+import pytest
+
+from generic_util import GENERIC_MF, USER_SCRIPTS, host_buffers, vm_plan
+from golden_util import all_goldens
+from gpu_util import check_output, scale_bound
+from oracle import COracle, RefOracle
+
+SEQS = ["AXPYDOT", "VADD", "WAXPBY", "SSCAL", "MADD", "BICGK", "ATAX", "SGEMV", "SGEMVT",
+        "GEMVER", "GESUMMV"]
+GOLDENS = all_goldens()
+
+
+@pytest.fixture(scope="module")
+def mf():
+    import paper_1305_1183_b200 as mf
+    mf.lib()
+    return mf
+
+
+@pytest.fixture
+def generic(mf):
+    mf.set_option("generic", 1)
+    yield mf
+    mf.set_option("generic", 0)
+
+
+@pytest.mark.parametrize("mode", ["fused", "unfused"])
+@pytest.mark.parametrize("seq", SEQS)
+def test_every_sequence_emits_and_compiles(generic, seq, mode):
+    mf = generic
+    m, n = (1, 4096) if seq in ("AXPYDOT", "VADD", "WAXPBY", "SSCAL") else (96, 160)
+    plan = mf.Plan.sequence(seq, m, n, mode)
+    d = plan.describe()
+    assert all(k["kind"] == "generic" for k in d["kernels"])
+    for k in range(plan.num_kernels):
+        src = plan.kernel_source(k)
+        assert 'extern "C" __global__' in src and "mfj_kernel" in src
+    plan.prepare()  # NVRTC -> sm_100a cubin for every kernel; raises on a compile error
+
+
+def test_hand_written_kernels_have_no_source(mf):
+    plan = mf.Plan.sequence("BICGK", 128, 128, "fused")
+    assert plan.describe()["kernels"][0]["kind"] == "matrix"
+    assert plan.kernel_source(0) == ""
+
+
+def test_generic_traffic_matches_hand_written(mf):
+    """Algorithmic bytes are a property of the plan, not of the kernel family."""
+    for seq, m, n in [("BICGK", 128, 192), ("GEMVER", 96, 160), ("AXPYDOT", 1, 4096),
+                      ("GESUMMV", 64, 96)]:
+        a = mf.Plan.sequence(seq, m, n, "fused").describe()
+        mf.set_option("generic", 1)
+        try:
+            b = mf.Plan.sequence(seq, m, n, "fused").describe()
+        finally:
+            mf.set_option("generic", 0)
+        assert (a["bytes_loaded"], a["bytes_stored"]) == (b["bytes_loaded"], b["bytes_stored"]), seq
+
+
+@pytest.mark.skipif(not RefOracle.available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("mode", ["fused", "unfused"])
+@pytest.mark.parametrize("g", GOLDENS, ids=lambda g: g.name)
+def test_codegen_kernels_on_reference_vm(mf, g, mode):
+    """The planner's KernelIRs, run by the reference's vm::launch, are
+    race-free (vm.cpp:481-521) and match the reference oracle."""
+    ref, co = RefOracle(), COracle()
+    plan = mf.Plan.sequence(g.seq, g.meta["requested"][0], g.meta["requested"][1], mode)
+    host = host_buffers(plan, g.inputs)
+    vm_plan(ref, plan, host, g.scalars)
+    want = g.out
+    S = scale_bound(co, g.seq, g.m, g.n, g.values())
+    for name in want:
+        check_output(g.seq, name, host[name], want[name], S[name], exact=False)
+
+
+def test_user_functions_plan_onto_generic_kernels(mf):
+    lib = open(GENERIC_MF).read()
+    s, m, n = USER_SCRIPTS["mul_add"]
+    fused = mf.Plan.compile(s, m, n, "fused", manifest=lib).describe()
+    assert [k["kind"] for k in fused["kernels"]] == ["generic"]
+    unf = mf.Plan.compile(s, m, n, "unfused", manifest=lib).describe()
+    assert [k["kind"] for k in unf["kernels"]] == ["generic", "stream"]  # add is hand-written
+    assert fused["bytes_loaded"] + fused["bytes_stored"] == 16 * 4096
+    s, m, n = USER_SCRIPTS["rscale_sgemv"]
+    fused = mf.Plan.compile(s, m, n, "fused", manifest=lib)
+    d = fused.describe()
+    assert [k["kind"] for k in d["kernels"]] == ["generic"]
+    assert d["kernels"][0]["op"]["accumulated"] == ["y"]
+    assert d["kernels"][0]["column_outputs"] == []  # y is row-indexed: row-local under sharding
+    fused.prepare()
+
+
+@pytest.mark.skipif(not RefOracle.available(), reason="oracle/_ref not built")
+def test_user_functions_on_reference_vm(mf):
+    ref = RefOracle()
+    lib = open(GENERIC_MF).read()
+    s, m, n = USER_SCRIPTS["rscale_sgemv"]
+    plan = mf.Plan.compile(s, m, n, "fused", manifest=lib)
+    host = host_buffers(plan, {}, np.random.default_rng(3))
+    vm_plan(ref, plan, host, {})
+    A, d, e, x = (host[k].astype(np.float64) for k in ("A", "d", "e", "x"))
+    B = (d.reshape(-1, 1) * A) * e.reshape(1, -1)
+    assert np.allclose(host["B"], B, rtol=1e-6, atol=1e-7)
+    y = B @ x.ravel()
+    assert np.max(np.abs(host["y"].ravel() - y)) <= 1e-5 * np.max(np.abs(y))
+
+
+def test_kernel_text_boundary_falls_back_to_generic(mf):
+    """mf_plan_create accepts any KernelIR text the VM accepts."""
+    lib = open(GENERIC_MF).read()
+    s, m, n = USER_SCRIPTS["mul_add"]
+    text = mf.Plan.compile(s, m, n, "fused", manifest=lib).kernel_text(0)
+    p = mf.Plan.from_kernel_text(text, 1, 4096)
+    d = p.describe()
+    assert d["kernels"][0]["kind"] == "generic"
+    assert {b["name"]: b["role"] for b in d["buffers"]} == {
+        "a": "input", "b": "input", "c": "input", "o": "output"}
+    p.prepare()

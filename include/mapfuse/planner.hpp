@@ -116,6 +116,11 @@ bool force_generic();
 void set_generic_iterations(int n);
 int generic_iterations();
 CodegenParams generic_params(const kernel::KernelIR& k, Sizes sz);
+// Test hook "codegen_barriers" = 0: codegen omits every barrier (the SPEC's
+// mutation check) -- the reference VM's race detector and
+// compute-sanitizer racecheck on the generic kernel must both flag it.
+void set_codegen_barriers(bool on);
+bool codegen_barriers();
 bool stream_template_exists(int nin, int nout, bool dot);
 bool matrix_template_exists(int nmat, int nrank, int store, int nrow, int ncol);
 

@@ -123,12 +123,15 @@ std::vector<Candidate> candidates(const script::Script& s, const script::DataDep
     c.calls = calls;
     try {
       c.item.calls = calls;
-      c.item.kir = generate_kernel(calls, s, g, L);
+      CodegenParams base;
+      base.barriers = codegen_barriers();
+      c.item.kir = generate_kernel(calls, s, g, L, base);
       c.item.native = lower_or_generic(c.item.kir);
       if (c.item.native.kind == b200::NativeKernel::Kind::Generic) {
         // generic kernels execute the KernelIR as written: pick the
         // implementation parameters (serial iterations) for this size
-        const CodegenParams prm = generic_params(c.item.kir, sz);
+        CodegenParams prm = generic_params(c.item.kir, sz);
+        prm.barriers = base.barriers;
         if (prm.iterations != c.item.kir.iterations) {
           c.item.kir = generate_kernel(calls, s, g, L, prm);
           c.item.native = generic_kernel(c.item.kir);

@@ -532,6 +532,8 @@ int mf_set_option(const char* key, int value) {
       options().occupancy = value;
     } else if (k == "generic") {
       mapfuse::plan::set_force_generic(value != 0);
+    } else if (k == "codegen_barriers") {
+      mapfuse::plan::set_codegen_barriers(value != 0);
     } else if (k == "generic_iterations") {
       if (value < 0 || value > 4096) throw Invalid("generic_iterations: 0 (auto) .. 4096");
       mapfuse::plan::set_generic_iterations(value);
@@ -556,6 +558,7 @@ int mf_get_option(const char* key) {
   if (k == "generic") return mapfuse::plan::force_generic() ? 1 : 0;
   if (k == "generic_poison") return options().generic_poison;
   if (k == "generic_iterations") return mapfuse::plan::generic_iterations();
+  if (k == "codegen_barriers") return mapfuse::plan::codegen_barriers() ? 1 : 0;
   return -1;
 }
 

@@ -128,3 +128,24 @@ def test_kernel_text_boundary_falls_back_to_generic(mf):
     assert {b["name"]: b["role"] for b in d["buffers"]} == {
         "a": "input", "b": "input", "c": "input", "o": "output"}
     p.prepare()
+
+
+@pytest.mark.skipif(not RefOracle.available(), reason="oracle/_ref not built")
+def test_barrier_mutation_is_a_race(mf):
+    """SPEC.md:723 mutation check: with codegen's barriers suppressed the fused
+    BiCGK kernel has shared-memory hazards the reference VM's race detector
+    reports (vm.cpp:481-521); with them it has none.  (On the GPU the same
+    mutated generic kernel is what compute-sanitizer racecheck flags,
+    profiles/r01_sanitizer_generic.txt.)"""
+    ref = RefOracle()
+    counts = {}
+    for barriers in (1, 0):
+        mf.set_option("codegen_barriers", barriers)
+        try:
+            plan = mf.Plan.sequence("BICGK", 128, 128, "fused")
+        finally:
+            mf.set_option("codegen_barriers", 1)
+        host = host_buffers(plan, {}, np.random.default_rng(0))
+        counts[barriers] = ref.vm_launch(plan.kernel_text(0), host, {}, trace=True)["hazards"]
+        assert ("barrier" in plan.kernel_text(0)) == bool(barriers)
+    assert counts[1] == 0 and counts[0] > 0, counts

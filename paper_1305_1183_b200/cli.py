@@ -89,6 +89,10 @@ def cmd_compile(args):
         for k in range(plan.num_kernels):
             with open(os.path.join(args.emit_source, "kernel%d.kir" % k), "w") as f:
                 f.write(plan.kernel_text(k))
+            src = plan.kernel_source(k)  # generic kernels: the emitted CUDA C++
+            if src:
+                with open(os.path.join(args.emit_source, "kernel%d.cu" % k), "w") as f:
+                    f.write(src)
     d = plan.describe()
     print(json.dumps({"plan": args.output, "kernels": [k["name"] for k in d["kernels"]],
                       "predicted_us": plan.predicted_us,

@@ -29,6 +29,7 @@ def test_cpp_vm_launch():
         f.write('#define DOCTEST_CONFIG_IMPLEMENT_WITH_MAIN\n#include "doctest.h"\n')
     exe = os.path.join(OUT, "vm_launch_gpu")
     _run(["g++", "-std=c++20", "-O1", "-I" + os.path.join(ROOT, "include"),
+          '-DMF_GENERIC_MF="%s"' % os.path.join(ROOT, "tests", "golden", "generic.mf"),
           "-I" + os.path.join(ROOT, "tests", "cpp"), "-I" + os.path.join(PKG, "csrc"),
           os.path.join(ROOT, "tests", "cpp_gpu", "test_vm_launch.cpp"), main,
           "-L" + PKG, "-lmapfuse_b200", "-Wl,-rpath," + PKG, "-o", exe])

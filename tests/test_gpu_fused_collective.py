@@ -131,3 +131,23 @@ def test_virtual_ranks_row_resident_chain():
         assert np.array_equal(bufs[0]["y"].cpu().numpy(), bufs[1]["y"].cpu().numpy())
     finally:
         mf.set_option("max_sms", 0)
+
+
+@pytest.mark.parametrize("seq,m,n", [("BICGK", 2048, 4096), ("GEMVER", 1024, 2048),
+                                     ("ATAX", 1536, 1024)])
+def test_two_processes_ipc_fused_column_reduction(seq, m, n):
+    """The real one-process-per-rank path: two OS processes (both on cuda:0),
+    CUDA-IPC handles exchanged over gloo, in-kernel reduction across them
+    (tools/ipc_two_process.py checks against the oracle)."""
+    import os
+    import random
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    port = str(29500 + random.randint(100, 900))
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", port,
+                        os.path.join(root, "tools", "ipc_two_process.py"), "--seq", seq,
+                        "--rows", str(m), "--cols", str(n)],
+                       capture_output=True, text=True, timeout=240)
+    assert r.returncode == 0 and "ipc ok" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]

@@ -136,6 +136,27 @@ int mf_plan_kernel_source(const mf_plan* plan, int k, char* buf, int cap);
  * compiler's diagnostics via mf_last_error(). */
 int mf_plan_prepare(const mf_plan* plan);
 
+/* vm::launch itself (proj/include/mapfuse/vm.hpp:94) over host buffers:
+ * KernelIR text + device config text (NULL = the shipped device.cfg) ->
+ * buffers updated in place, ExecutionStats (and, with MF_VM_TRACE, the
+ * race-report size) as JSON in `json` (size convention as
+ * mf_plan_describe; a negative return is -status on failure).  Kernels no
+ * hand-written family covers -- and all kernels under MF_VM_TRACE or the
+ * "vm_exact" option -- run the generic kernel with the VM's counters. */
+#define MF_VM_TRACE 1     /* LaunchArgs::trace: device-side trace + detect_races */
+#define MF_VM_NO_POISON 2 /* LaunchArgs::poison_onchip = false */
+int mf_vm_launch(const char* kernel_ir_text, const char* device_config, const mf_buffer* host_buffers,
+                 int nbuf, const mf_scalar* scalars, int nscalars, int flags, char* json, int cap);
+
+/* vm::measure_routine (proj/include/mapfuse/vm.hpp:108): modeled cycles of
+ * one routine ("load_A", "compute", ... = Routine::id()) of `function` in the
+ * simulated fusion environment, counted on the GPU by the generic kernel's
+ * VM instrumentation.  manifest NULL = the shipped library; device_config
+ * NULL = the shipped device.cfg.  *cycles = -1 when infeasible. */
+int mf_measure_routine(const char* manifest, const char* function, const char* routine,
+                       int instances, int iterations, int extra_shared_bytes,
+                       const char* device_config, int64_t* cycles);
+
 /* Synchronizes `stream` and reports (MF_ERR_FAULT) the first device fault a
  * generic kernel of this plan recorded since the last check: out-of-bounds
  * global or on-chip index, poisoned on-chip read, division by zero -- the
@@ -180,7 +201,10 @@ int mf_generate(float* dev, int64_t rows, int64_t cols, int64_t ld, uint64_t see
  * accumulate matrix reductions in fp64), "occupancy" (CTAs per SM),
  * "generic" (0|1: run every kernel on the generic NVRTC-emitted path, even
  * where a hand-written family applies), "generic_poison" (0|1: generic
- * kernels poison on-chip memory and fault on uninitialised reads). */
+ * kernels poison on-chip memory and fault on uninitialised reads),
+ * "generic_iterations" (0 = per size, else the serial iterations of generic
+ * kernels), "vm_exact" (0|1: vm::launch always counts like the VM),
+ * "codegen_barriers" (test hook, 0 = codegen omits barriers). */
 int mf_set_option(const char* key, int value);
 int mf_get_option(const char* key);
 

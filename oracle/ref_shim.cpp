@@ -9,6 +9,7 @@
 // fixture generator and bench.py's reference arm can drive the reference
 // directly.
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -157,7 +158,8 @@ int mfr_problem_names(void* h, char* dst, int cap) {
 int mfr_vm_launch(const char* kernel_text, int nbuf, const char* const* names, const int* rows,
                   const int* cols, float* const* data, int nsc, const char* const* sc_names,
                   const float* sc_values, int poison, int trace, long* hazards,
-                  unsigned long long* words_loaded, unsigned long long* words_stored) {
+                  unsigned long long* words_loaded, unsigned long long* words_stored,
+                  char* stats_json, int cap) {
   try {
     namespace vm = mapfuse::vm;
     const mapfuse::kernel::KernelIR k = mapfuse::kernel::parse_kernel_text(kernel_text);
@@ -178,10 +180,59 @@ int mfr_vm_launch(const char* kernel_text, int nbuf, const char* const* names, c
     if (hazards) *hazards = static_cast<long>(r.races.hazards.size());
     if (words_loaded) *words_loaded = r.stats.global_words_loaded;
     if (words_stored) *words_stored = r.stats.global_words_stored;
+    if (stats_json && cap > 0) {
+      const auto& s = r.stats;
+      std::string j = "{\"global_words_loaded\":" + std::to_string(s.global_words_loaded) +
+                      ",\"global_words_stored\":" + std::to_string(s.global_words_stored) +
+                      ",\"per_buffer\":{";
+      bool first = true;
+      for (const auto& [n, t] : s.per_buffer) {
+        j += std::string(first ? "" : ",") + "\"" + n + "\":[" + std::to_string(t.loaded) + "," +
+             std::to_string(t.stored) + "]";
+        first = false;
+      }
+      char lf[64];
+      std::snprintf(lf, sizeof lf, "%.17g", s.latency_factor);
+      j += "},\"shared_accesses\":" + std::to_string(s.shared_accesses) +
+           ",\"atomics\":" + std::to_string(s.atomics) + ",\"barriers\":" + std::to_string(s.barriers) +
+           ",\"arith_ops\":" + std::to_string(s.arith_ops) +
+           ",\"block_cycles_sum\":" + std::to_string(s.block_cycles_sum) +
+           ",\"cycles\":" + std::to_string(s.cycles) + ",\"blocks\":" + std::to_string(s.blocks) +
+           ",\"threads_per_block\":" + std::to_string(s.threads_per_block) +
+           ",\"shared_bytes\":" + std::to_string(s.shared_bytes) +
+           ",\"occupancy\":" + std::to_string(s.occupancy) + ",\"latency_factor\":" + lf +
+           ",\"trace_records\":" + std::to_string(r.trace.size()) +
+           ",\"hazards\":" + std::to_string(r.races.hazards.size()) + "}";
+      std::snprintf(stats_json, static_cast<size_t>(cap), "%s", j.c_str());
+    }
     return 0;
   } catch (const std::exception& e) {
     g_err = e.what();
     return 1;
+  }
+}
+
+// The reference's cost-DB micro-benchmark, vm::measure_routine
+// (proj/src/vm.cpp:523-608), for routine `routine_id` (Routine::id()) of a
+// function of the shipped library.  Returns cycles, or -1 if infeasible /
+// unknown (message via mfr_last_error).
+long long mfr_measure_routine(const char* function, const char* routine_id, int instances,
+                              int iterations, int extra_shared_bytes) {
+  try {
+    namespace vm = mapfuse::vm;
+    const auto& L = mapfuse::blas::default_library();
+    const auto* f = L.find(function);
+    if (!f) throw std::runtime_error(std::string("no function ") + function);
+    for (const auto& r : f->routines)
+      if (r.id() == routine_id) {
+        const auto dev = vm::parse_device_config(mapfuse::blas::default_device_config_text());
+        auto c = vm::measure_routine(*f, r, vm::MeasureEnv{instances, iterations, extra_shared_bytes}, dev);
+        return c ? static_cast<long long>(*c) : -1;
+      }
+    throw std::runtime_error(std::string("no routine ") + routine_id);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
   }
 }
 

@@ -2,11 +2,17 @@
 #include "mapfuse_b200.h"
 
 #include <algorithm>
+#include <cstdio>
 #include <cstring>
+#include <map>
+#include <vector>
 #include <memory>
 #include <string>
 
+#include "mapfuse/blas.hpp"
+#include "mapfuse/kernel.hpp"
 #include "mapfuse/planner.hpp"
+#include "mapfuse/vm.hpp"
 #include "mf_builtin.hpp"
 #include "mf_compile.hpp"
 #include "mf_exec.hpp"
@@ -347,10 +353,113 @@ int mf_plan_prepare(const mf_plan* plan) {
     if (!plan) throw Invalid("null plan");
     for (const auto& kern : plan->plan.kernels)
       if (kern.kind == NativeKernel::Kind::Generic) {
-        const bool poison =
-            kern.generic_poison >= 0 ? kern.generic_poison != 0 : options().generic_poison != 0;
-        jit_prepare(kern.generic.source, poison);
+        JitFlags fl;
+        fl.poison = kern.generic_poison >= 0 ? kern.generic_poison != 0 : options().generic_poison != 0;
+        jit_prepare(kern.generic.source, fl);
       }
+  });
+}
+
+int mf_vm_launch(const char* kernel_ir_text, const char* device_config, const mf_buffer* host_buffers,
+                 int nbuf, const mf_scalar* scalars, int nscalars, int flags, char* json, int cap) {
+  std::string out;
+  const int rc = guarded([&] {
+    if (!kernel_ir_text) throw Invalid("null kernel text");
+    mapfuse::kernel::KernelIR k;
+    mapfuse::vm::DeviceConfig dev;
+    try {
+      k = mapfuse::kernel::parse_kernel_text(kernel_ir_text);
+      dev = mapfuse::vm::parse_device_config(device_config ? std::string(device_config)
+                                                           : mapfuse::blas::default_device_config_text());
+    } catch (const std::exception& e) {
+      throw Invalid(e.what());
+    }
+    std::map<std::string, std::vector<float>> store;
+    mapfuse::vm::LaunchArgs args;
+    for (int i = 0; i < nbuf; ++i) {
+      const mf_buffer& h = host_buffers[i];
+      if (!h.name || !h.data) throw Invalid("host buffer without name or data");
+      auto& v = store[h.name];
+      v.assign(h.data, h.data + (size_t)h.rows * (size_t)h.cols);
+      args.buffers[h.name] = mapfuse::vm::GlobalBuffer{h.rows, h.cols, &v};
+    }
+    for (int i = 0; i < nscalars; ++i) args.scalars[scalars[i].name] = scalars[i].value;
+    args.trace = (flags & MF_VM_TRACE) != 0;
+    args.poison_onchip = (flags & MF_VM_NO_POISON) == 0;
+    mapfuse::vm::LaunchResult r;
+    try {
+      r = mapfuse::vm::launch(k, dev, args);
+    } catch (const mapfuse::vm::VmFault& e) {
+      throw Fault(e.what());
+    }
+    for (int i = 0; i < nbuf; ++i) {
+      const auto& v = store[host_buffers[i].name];
+      std::memcpy(host_buffers[i].data, v.data(), sizeof(float) * v.size());
+    }
+    const auto& s = r.stats;
+    std::string j = "{\"global_words_loaded\":" + std::to_string(s.global_words_loaded) +
+                    ",\"global_words_stored\":" + std::to_string(s.global_words_stored) +
+                    ",\"per_buffer\":{";
+    bool first = true;
+    for (const auto& [n, t] : s.per_buffer) {
+      j += std::string(first ? "" : ",") + "\"" + n + "\":[" + std::to_string(t.loaded) + "," +
+           std::to_string(t.stored) + "]";
+      first = false;
+    }
+    char lf[64];
+    std::snprintf(lf, sizeof lf, "%.17g", s.latency_factor);
+    char ms[64];
+    std::snprintf(ms, sizeof ms, "%.6f", s.device_ms);
+    j += "},\"shared_accesses\":" + std::to_string(s.shared_accesses) +
+         ",\"atomics\":" + std::to_string(s.atomics) + ",\"barriers\":" + std::to_string(s.barriers) +
+         ",\"arith_ops\":" + std::to_string(s.arith_ops) +
+         ",\"block_cycles_sum\":" + std::to_string(s.block_cycles_sum) +
+         ",\"cycles\":" + std::to_string(s.cycles) + ",\"blocks\":" + std::to_string(s.blocks) +
+         ",\"threads_per_block\":" + std::to_string(s.threads_per_block) +
+         ",\"shared_bytes\":" + std::to_string(s.shared_bytes) +
+         ",\"occupancy\":" + std::to_string(s.occupancy) + ",\"latency_factor\":" + lf +
+         ",\"device_ms\":" + ms + ",\"native_kernel\":\"" + s.native_kernel +
+         "\",\"vm_exact\":" + (s.vm_exact ? "true" : "false") +
+         ",\"trace_records\":" + std::to_string(r.trace.size()) +
+         ",\"hazards\":" + std::to_string(r.races.hazards.size()) + "}";
+    out = j;
+  });
+  if (rc != MF_OK) return -rc;
+  return copy_out(out, json, cap);
+}
+
+int mf_measure_routine(const char* manifest, const char* function, const char* routine,
+                       int instances, int iterations, int extra_shared_bytes,
+                       const char* device_config, int64_t* cycles) {
+  return guarded([&] {
+    if (!function || !routine || !cycles) throw Invalid("null argument");
+    mapfuse::lib::Library own;
+    const mapfuse::lib::Library* L = &mapfuse::blas::default_library();
+    mapfuse::vm::DeviceConfig dev;
+    try {
+      if (manifest) {
+        own = mapfuse::lib::load_library(manifest);
+        L = &own;
+      }
+      dev = mapfuse::vm::parse_device_config(device_config ? std::string(device_config)
+                                                           : mapfuse::blas::default_device_config_text());
+    } catch (const std::exception& e) {
+      throw Invalid(e.what());
+    }
+    const auto* f = L->find(function);
+    if (!f) throw Invalid(std::string("unknown function '") + function + "'");
+    for (const auto& r : f->routines)
+      if (r.id() == routine) {
+        try {
+          auto c = mapfuse::vm::measure_routine(
+              *f, r, mapfuse::vm::MeasureEnv{instances, iterations, extra_shared_bytes}, dev);
+          *cycles = c ? static_cast<int64_t>(*c) : -1;
+        } catch (const mapfuse::vm::VmFault& e) {
+          throw Fault(e.what());
+        }
+        return;
+      }
+    throw Invalid(std::string("unknown routine '") + routine + "' of " + function);
   });
 }
 
@@ -532,6 +641,8 @@ int mf_set_option(const char* key, int value) {
       options().occupancy = value;
     } else if (k == "generic") {
       mapfuse::plan::set_force_generic(value != 0);
+    } else if (k == "vm_exact") {
+      mapfuse::vm::set_exact(value != 0);
     } else if (k == "codegen_barriers") {
       mapfuse::plan::set_codegen_barriers(value != 0);
     } else if (k == "generic_iterations") {
@@ -559,6 +670,7 @@ int mf_get_option(const char* key) {
   if (k == "generic_poison") return options().generic_poison;
   if (k == "generic_iterations") return mapfuse::plan::generic_iterations();
   if (k == "codegen_barriers") return mapfuse::plan::codegen_barriers() ? 1 : 0;
+  if (k == "vm_exact") return mapfuse::vm::exact() ? 1 : 0;
   return -1;
 }
 

@@ -332,29 +332,36 @@ void run_matrix(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc, 
 
 // Generic kernel: one CTA per VM block over the grid the domain buffer
 // implies (proj/src/vm.cpp:24-47, :450-466); see host/cudagen.cpp.
-void run_generic(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc, cudaStream_t s,
-                 Workspace& ws) {
+struct GenericLaunch {
+  MfjArgs a{};
+  int64_t launch_x = 0, launch_y = 1;
+  size_t smem = 0;
+};
+
+// Grid (vm.cpp:24-47), bindings and scalars of a generic kernel.
+GenericLaunch generic_args(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc,
+                           cudaStream_t s, Workspace& ws) {
   const GenericOp& g = k.generic;
   auto dom = bufs.find(g.domain);
   if (dom == bufs.end() || !dom->second.ptr)
     throw Fault("launch: no domain buffer '" + g.domain + "'");
   const int64_t rows = dom->second.rows, cols = dom->second.cols;
   auto cdiv = [](int64_t a, int64_t b) { return (a + b - 1) / b; };
-  MfjArgs a{};
-  int64_t launch_x = 0, launch_y = 1;
+  GenericLaunch L;
+  MfjArgs& a = L.a;
   if (g.depth == 2) {
     if (rows % 32 || cols % 32) throw Fault("launch: domain '" + g.domain + "' not padded to 32");
     a.full_x = cols / 32;
     a.full_y = rows / 32;
-    launch_x = g.iter_dim == 'x' ? cdiv(a.full_x, g.iterations) : a.full_x;
-    launch_y = g.iter_dim == 'y' ? cdiv(a.full_y, g.iterations) : a.full_y;
+    L.launch_x = g.iter_dim == 'x' ? cdiv(a.full_x, g.iterations) : a.full_x;
+    L.launch_y = g.iter_dim == 'y' ? cdiv(a.full_y, g.iterations) : a.full_y;
   } else {
     const int64_t len = rows == 1 ? cols : rows;
     if (len % 32) throw Fault("launch: domain '" + g.domain + "' not padded to 32");
     a.n_elems = len / 32;
     a.full_x = cdiv(a.n_elems, g.instances);
     a.full_y = 1;
-    launch_x = cdiv(a.full_x, g.iterations);
+    L.launch_x = cdiv(a.full_x, g.iterations);
   }
   for (size_t i = 0; i < g.buffers.size(); ++i) {
     auto it = bufs.find(g.buffers[i]);
@@ -370,19 +377,31 @@ void run_generic(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc,
     a.scal[j] = static_cast<float>(it->second);
   }
   a.fault = ws.jit_fault(s);
+  if (L.launch_x > 0x7fffffffLL || L.launch_y > 65535)
+    throw Fault("kernel " + k.name + ": grid exceeds the device's limits");
+  L.smem = sizeof(float) * (size_t)g.shared_words_total;
+  if (L.smem > 227u * 1024u) throw Fault("vm fault: shared allocation exceeds device limit");
+  return L;
+}
+
+JitFlags generic_flags(const NativeKernel& k) {
+  JitFlags fl;
+  fl.poison = k.generic_poison >= 0 ? k.generic_poison != 0 : options().generic_poison != 0;
+  return fl;
+}
+
+void run_generic(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc, cudaStream_t s,
+                 Workspace& ws) {
+  GenericLaunch L = generic_args(k, bufs, sc, s, ws);
   if (!k.vm_semantics)  // engine contract: outputs are overwritten, not accumulated into
-    for (const auto& name : g.accumulated) {
+    for (const auto& name : k.generic.accumulated) {
       const DevBuf& b = bufs.at(name);
       check_cuda(cudaMemsetAsync(b.ptr, 0, sizeof(float) * (size_t)b.size(), s), "zero accumulated output");
     }
-  if (launch_x == 0 || launch_y == 0) return;
-  if (launch_x > 0x7fffffffLL || launch_y > 65535)
-    throw Fault("kernel " + k.name + ": grid exceeds the device's limits");
-  const size_t smem = sizeof(float) * (size_t)g.shared_words_total;
-  if (smem > 227u * 1024u) throw Fault("vm fault: shared allocation exceeds device limit");
-  const bool poison = k.generic_poison >= 0 ? k.generic_poison != 0 : options().generic_poison != 0;
-  jit_launch(g.source, poison, dim3((unsigned)launch_x, (unsigned)launch_y),
-             dim3((unsigned)(g.block_x * g.block_y)), smem, a, s);
+  if (L.launch_x == 0 || L.launch_y == 0) return;
+  const GenericOp& g = k.generic;
+  jit_launch(g.source, generic_flags(k), dim3((unsigned)L.launch_x, (unsigned)L.launch_y),
+             dim3((unsigned)(g.block_x * g.block_y)), L.smem, L.a, s);
 }
 
 }  // namespace
@@ -406,6 +425,51 @@ void check_jit_faults(Workspace& ws, cudaStream_t stream) {
     default: break;
   }
   throw Fault(std::string("vm fault: ") + what + " (generic kernel, detail " + std::to_string(h[1]) + ")");
+}
+
+int64_t run_generic_counted(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc,
+                            const int cost[6], bool trace, int64_t trace_cap, cudaStream_t s,
+                            Workspace& ws, std::vector<uint64_t>* stats, std::vector<MfjRec>* recs,
+                            int64_t* blocks) {
+  if (k.kind != NativeKernel::Kind::Generic) throw Invalid("counted launch of a non-generic kernel");
+  std::lock_guard<std::mutex> lk(ws.mu);
+  GenericLaunch L = generic_args(k, bufs, sc, s, ws);
+  const GenericOp& g = k.generic;
+  const int T = g.block_x * g.block_y;
+  *blocks = L.launch_x * L.launch_y;
+  // counting scratch after the VM arena: per-thread costs + per-warp cycles
+  const size_t arena = (size_t)g.shared_words_total;
+  const size_t smem = sizeof(float) * ((arena + 4 * (size_t)T + 1) / 2 * 2) + 8 * (size_t)T;
+  if (smem > 227u * 1024u) throw Fault("vm fault: shared allocation exceeds device limit");
+  auto* dstats = reinterpret_cast<unsigned long long*>(ws.named("__jit_stats", 2 * kMfjStatWords));
+  check_cuda(cudaMemsetAsync(dstats, 0, 8 * kMfjStatWords, s), "zero stats");
+  MfjRec* drec = nullptr;
+  if (trace && trace_cap > 0)
+    drec = reinterpret_cast<MfjRec*>(ws.named("__jit_trace", trace_cap * (int64_t)(sizeof(MfjRec) / 4)));
+  L.a.stats = dstats;
+  L.a.trace = drec;
+  L.a.trace_cap = drec ? trace_cap : 0;
+  for (int i = 0; i < 6; ++i) L.a.cost[i] = cost[i];
+  JitFlags fl = generic_flags(k);
+  fl.stats = true;
+  fl.trace = trace;
+  if (L.launch_x > 0 && L.launch_y > 0)
+    jit_launch(g.source, fl, dim3((unsigned)L.launch_x, (unsigned)L.launch_y), dim3((unsigned)T), smem,
+               L.a, s);
+  stats->assign(kMfjStatWords, 0);
+  check_cuda(cudaMemcpyAsync(stats->data(), dstats, 8 * kMfjStatWords, cudaMemcpyDeviceToHost, s),
+             "read stats");
+  check_cuda(cudaStreamSynchronize(s), "counted generic kernel");
+  const int64_t n = (int64_t)(*stats)[kStatTraceCursor];
+  if (recs) {
+    recs->clear();
+    if (drec && n > 0 && n <= trace_cap) {
+      recs->resize((size_t)n);
+      check_cuda(cudaMemcpy(recs->data(), drec, sizeof(MfjRec) * (size_t)n, cudaMemcpyDeviceToHost),
+                 "read trace");
+    }
+  }
+  return n;
 }
 
 BufMap complete_bindings(const NativePlan& plan, const BufMap& bufs, Workspace& ws) {

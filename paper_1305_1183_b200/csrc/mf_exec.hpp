@@ -10,6 +10,7 @@
 #include <string>
 #include <vector>
 
+#include "mf_jit.hpp"
 #include "mf_native.hpp"
 
 namespace mapfuse::b200 {
@@ -88,6 +89,17 @@ void run_kernel(const NativePlan& plan, int k, const BufMap& bufs, const ScalarM
 // this workspace (host/cudagen.cpp: bounds, poisoned read, division by zero)
 // into a Fault -- the VM's VmFault (proj/src/vm.cpp:77-81).  Resets it.
 void check_jit_faults(Workspace& ws, cudaStream_t stream);
+// The reference VM's instrumentation on a generic kernel (host/cudagen.cpp
+// MFJ_STATS / MFJ_TRACE): runs it once, synchronously, and returns the
+// counters (mf_jit.hpp MfjStat layout), the access trace if `trace` (up to
+// trace_cap records) and the block count.  Returns the number of trace
+// records the kernel produced (> trace_cap: rerun with a larger buffer).
+// cost = DeviceConfig cycles per global word, shared word, arith op,
+// barrier, atomic, and the warp size.
+int64_t run_generic_counted(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc,
+                            const int cost[6], bool trace, int64_t trace_cap, cudaStream_t s,
+                            Workspace& ws, std::vector<uint64_t>* stats,
+                            std::vector<MfjRec>* recs, int64_t* blocks);
 // Binds any plan intermediates the caller left unbound (workspace-backed).
 BufMap complete_bindings(const NativePlan& plan, const BufMap& bufs, Workspace& ws);
 
@@ -95,3 +107,11 @@ int device_sm_count();
 void check_cuda(cudaError_t e, const char* what);
 
 }  // namespace mapfuse::b200
+
+namespace mapfuse::vm {
+// Engine option "vm_exact" (env MF_VM_EXACT): vm::launch always runs the
+// generic kernel with the VM's counters, even where a hand-written family
+// applies (exact ExecutionStats at the cost of speed).
+void set_exact(bool on);
+bool exact();
+}  // namespace mapfuse::vm

@@ -75,16 +75,18 @@ struct Module {
 std::mutex g_mu;
 std::map<std::string, std::shared_ptr<Module>> g_cache;
 
-std::vector<char> compile_cubin(const std::string& src, bool poison, std::string* log_out) {
+std::vector<char> compile_cubin(const std::string& src, JitFlags fl, std::string* log_out) {
   const Nvrtc& n = nvrtc();
   if (!n.error.empty()) throw Fault(n.error);
   nvrtcProgram prog = nullptr;
   nvrtcResult rc = n.create(&prog, src.c_str(), "mfj_kernel.cu", 0, nullptr, nullptr);
   if (rc != NVRTC_SUCCESS) throw Fault(std::string("nvrtcCreateProgram: ") + n.errstr(rc));
-  const std::string poison_def = std::string("-DMFJ_POISON=") + (poison ? "1" : "0");
+  const std::string d1 = std::string("-DMFJ_POISON=") + (fl.poison ? "1" : "0");
+  const std::string d2 = std::string("-DMFJ_STATS=") + (fl.stats || fl.trace ? "1" : "0");
+  const std::string d3 = std::string("-DMFJ_TRACE=") + (fl.trace ? "1" : "0");
   const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo", "-fmad=false",
-                        poison_def.c_str()};
-  rc = n.compile(prog, 5, opts);
+                        d1.c_str(), d2.c_str(), d3.c_str()};
+  rc = n.compile(prog, 7, opts);
   size_t ls = 0;
   n.log_size(prog, &ls);
   std::string log(ls, '\0');
@@ -102,15 +104,16 @@ std::vector<char> compile_cubin(const std::string& src, bool poison, std::string
   return cubin;
 }
 
-std::shared_ptr<Module> module_for(const std::string& src, bool poison) {
-  const std::string key = std::string(poison ? "P" : "N") + src;
+std::shared_ptr<Module> module_for(const std::string& src, JitFlags fl) {
+  const std::string key = std::string(fl.poison ? "P" : "N") + (fl.stats ? "S" : "-") +
+                          (fl.trace ? "T" : "-") + src;
   {
     std::lock_guard<std::mutex> lk(g_mu);
     auto it = g_cache.find(key);
     if (it != g_cache.end()) return it->second;
   }
   auto m = std::make_shared<Module>();
-  m->cubin = compile_cubin(src, poison, nullptr);  // outside the lock: NVRTC is slow
+  m->cubin = compile_cubin(src, fl, nullptr);  // outside the lock: NVRTC is slow
   std::lock_guard<std::mutex> lk(g_mu);
   auto [it, inserted] = g_cache.emplace(key, m);
   return it->second;
@@ -118,11 +121,11 @@ std::shared_ptr<Module> module_for(const std::string& src, bool poison) {
 
 }  // namespace
 
-std::vector<char> jit_compile_only(const std::string& src, bool poison, std::string* log) {
-  return compile_cubin(src, poison, log);
+std::vector<char> jit_compile_only(const std::string& src, JitFlags fl, std::string* log) {
+  return compile_cubin(src, fl, log);
 }
 
-void jit_prepare(const std::string& src, bool poison) { (void)module_for(src, poison); }
+void jit_prepare(const std::string& src, JitFlags fl) { (void)module_for(src, fl); }
 
 bool jit_available(std::string* why) {
   const Nvrtc& n = nvrtc();
@@ -130,9 +133,9 @@ bool jit_available(std::string* why) {
   return n.error.empty();
 }
 
-void jit_launch(const std::string& src, bool poison, dim3 grid, dim3 block, size_t smem,
+void jit_launch(const std::string& src, JitFlags fl, dim3 grid, dim3 block, size_t smem,
                 const MfjArgs& args, cudaStream_t stream) {
-  std::shared_ptr<Module> m = module_for(src, poison);
+  std::shared_ptr<Module> m = module_for(src, fl);
   int dev = 0;
   check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
   cudaKernel_t fn = nullptr;

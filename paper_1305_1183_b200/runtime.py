@@ -67,7 +67,7 @@ EXPORTS = [
     "mf_peer_group_connect_local", "mf_peer_group_destroy", "mf_launch_kernel_peers",
     "mf_compile_ranked", "mf_count_combinations", "mf_plan_predicted_us", "mf_plan_save",
     "mf_plan_load", "mf_sequence_script", "mf_plan_kernel_source", "mf_plan_prepare",
-    "mf_plan_check",
+    "mf_plan_check", "mf_vm_launch", "mf_measure_routine",
 ]
 
 
@@ -118,6 +118,10 @@ def lib() -> C.CDLL:
         L.mf_plan_load.argtypes = [C.c_char_p, P(C.c_void_p)]
         L.mf_sequence_script.argtypes = [C.c_char_p, C.c_char_p, C.c_int]
         L.mf_plan_prepare.argtypes = [C.c_void_p]
+        L.mf_vm_launch.argtypes = [C.c_char_p, C.c_char_p, P(MfBuffer), C.c_int, P(MfScalar),
+                                   C.c_int, C.c_int, C.c_char_p, C.c_int]
+        L.mf_measure_routine.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.c_int, C.c_int,
+                                         C.c_int, C.c_char_p, P(C.c_int64)]
         L.mf_plan_check.argtypes = [C.c_void_p, C.c_void_p]
         L.mf_last_error.restype = C.c_char_p
         L.mf_version.restype = C.c_char_p
@@ -378,3 +382,48 @@ def get_option(key: str) -> int:
 
 def version() -> str:
     return lib().mf_version().decode()
+
+
+def vm_launch(kernel_text: str, buffers: Mapping[str, object], scalars: Mapping[str, float] = {},
+              trace: bool = False, poison: bool = True, device_config: Optional[str] = None) -> dict:
+    """vm::launch (proj/include/mapfuse/vm.hpp:94) on host numpy buffers (updated
+    in place): returns the ExecutionStats as a dict (plus "hazards" and
+    "trace_records" when trace=True).  Kernels no hand-written family covers,
+    and every kernel with trace=True or option "vm_exact", report the VM's
+    exact counters (stats["vm_exact"])."""
+    import numpy as np
+    names, arrs = [], []
+    for k, v in buffers.items():
+        assert isinstance(v, np.ndarray) and v.dtype == np.float32 and v.flags["C_CONTIGUOUS"], k
+        names.append(k.encode())
+        arrs.append(v)
+    nb = len(arrs)
+    bufs = (MfBuffer * max(nb, 1))()
+    for i, a in enumerate(arrs):
+        r, c = (a.shape[0], a.shape[1]) if a.ndim == 2 else (1, a.size)
+        bufs[i] = MfBuffer(names[i], r, c, a.ctypes.data)
+    ns = len(scalars)
+    sc = (MfScalar * max(ns, 1))()
+    for i, (k, v) in enumerate(scalars.items()):
+        sc[i] = MfScalar(k.encode(), float(v))
+    flags = (1 if trace else 0) | (0 if poison else 2)
+    cfg = device_config.encode() if device_config else None
+    out = C.create_string_buffer(1 << 16)  # one call: the launch mutates the buffers
+    need = lib().mf_vm_launch(kernel_text.encode(), cfg, bufs, nb, sc, ns, flags, out, len(out))
+    if need < 0:
+        _check(-need)
+    if need > len(out):
+        raise MapfuseError(-1, "stats JSON truncated")
+    return json.loads(out.value.decode())
+
+
+def measure_routine(function: str, routine: str, instances: int = 1, iterations: int = 1,
+                    extra_shared_bytes: int = 0, manifest: Optional[str] = None,
+                    device_config: Optional[str] = None) -> Optional[int]:
+    """vm::measure_routine (proj/include/mapfuse/vm.hpp:108) counted on the GPU."""
+    c = C.c_int64(0)
+    _check(lib().mf_measure_routine(manifest.encode() if manifest else None, function.encode(),
+                                    routine.encode(), instances, iterations, extra_shared_bytes,
+                                    device_config.encode() if device_config else None,
+                                    C.byref(c)))
+    return None if c.value < 0 else int(c.value)

@@ -109,11 +109,13 @@ class ClockSampler:
 
 
 def measured_peak():
+    """HBM roofline denominator: the driver-measured copy bandwidth, else the
+    fallback figure /opt/skills/guides/B200_PROFILING.md states (6.65 TB/s)."""
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
         with open(p) as f:
-            return float(json.load(f)["hbm_gbs"]), "measured"
-    return 6650.0, "fallback"
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md, MEASURED_PEAKS.json absent)"
 
 
 def ncu_traffic(kernel_key: str):
@@ -360,6 +362,14 @@ SUITE = [("AXPYDOT", 1, 1 << 24), ("BICGK", 16384, 16384), ("ATAX", 16384, 16384
          ("GEMVER", 32768, 32768), ("GESUMMV", 32768, 32768)]
 
 
+def median_step_ms(torch, plan, bufs, sc, flush, reps=9):
+    """Median over `reps` steps of the device time of one pass of the plan,
+    L2 flushed before every step."""
+    _, per = time_kernels(torch, [(plan, bufs, sc)], reps, 2, flush=flush)
+    steps = [sum(v[i] for v in per.values()) for i in range(reps)]
+    return statistics.median(steps)
+
+
 def run_suite(args, torch, mf):
     # L2 flush between timed launches: write 1 GiB, then read another 1 GiB so
     # the L2 holds clean lines (no write-backs land inside the timed kernel)
@@ -373,11 +383,20 @@ def run_suite(args, torch, mf):
         for mode in ("fused", "unfused"):
             p = mf.Plan.sequence(seq, m, n, mode)
             bufs, d = make_buffers(torch, mf, p, seed=7)
-            ms, per = time_kernels(torch, [(p, bufs, sc)], 5, 2, flush=flush)
-            ms /= 5
+            ms = median_step_ms(torch, p, bufs, sc, flush)
             byts = d["bytes_loaded"] + d["bytes_stored"]
             r[mode] = {"us": round(ms * 1e3, 1), "GBps": round(byts / ms / 1e6, 1),
                        "bytes": byts, "kernels": p.num_kernels}
+            del bufs
+            torch.cuda.empty_cache()
+        if seq == "ATAX":  # beyond the paper: row-resident single pass (planner mode "b200")
+            p = mf.Plan.sequence(seq, m, n, "b200")
+            bufs, d = make_buffers(torch, mf, p, seed=7)
+            ms = median_step_ms(torch, p, bufs, sc, flush)
+            byts = d["bytes_loaded"] + d["bytes_stored"]
+            r["b200"] = {"us": round(ms * 1e3, 1), "GBps": round(byts / ms / 1e6, 1), "bytes": byts,
+                         "kernels": p.num_kernels, "frac_of_hbm": round(byts / ms / 1e6 / peak, 3),
+                         "speedup_vs_fused": round(r["fused"]["us"] / (ms * 1e3), 3)}
             del bufs
             torch.cuda.empty_cache()
         r["fused"]["frac_of_hbm"] = round(r["fused"]["GBps"] / peak, 3)
@@ -474,7 +493,7 @@ def main():
     achieved = vadd_bytes / (kms / 1e3) / 1e9
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": ncu_traffic("stream_kernel<3, 1, 0>"),
-                "kernel": key[2], "peak_source": peak_kind + " (MEASURED_PEAKS.json hbm_gbs)",
+                "kernel": key[2], "peak_source": peak_kind,
                 "algorithmic_bytes_per_launch": vadd_bytes,
                 "avg_launch_us": round(kms * 1e3, 1)}
     per_kernel = {"%s/%s" % (k[0], k[2]): round(statistics.mean(v) * 1e3, 1)

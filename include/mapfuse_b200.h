@@ -157,6 +157,19 @@ int mf_measure_routine(const char* manifest, const char* function, const char* r
                        int instances, int iterations, int extra_shared_bytes,
                        const char* device_config, int64_t* cycles);
 
+/* Bound plans: the plan's kernels prepared once for fixed device buffers and
+ * scalars (validation, scalar coefficients, grids, workspace), so a launch
+ * costs only the kernel launches -- or, with mf_bound_graph_launch, one
+ * CUDA-graph launch of the whole plan (captured on the first call; `stream`
+ * must not be the legacy default stream).  The bound plan owns its own
+ * workspace; its plan must outlive it.  Not for peer (sharded) launches. */
+typedef struct mf_bound mf_bound;
+int mf_plan_bind(const mf_plan* plan, const mf_buffer* buffers, int nbuf, const mf_scalar* scalars,
+                 int nscalars, mf_bound** out);
+int mf_bound_launch(mf_bound* bound, void* stream);
+int mf_bound_graph_launch(mf_bound* bound, void* stream);
+void mf_bound_destroy(mf_bound* bound);
+
 /* Synchronizes `stream` and reports (MF_ERR_FAULT) the first device fault a
  * generic kernel of this plan recorded since the last check: out-of-bounds
  * global or on-chip index, poisoned on-chip read, division by zero -- the

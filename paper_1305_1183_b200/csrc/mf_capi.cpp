@@ -30,6 +30,18 @@ struct mf_peer_group {
   PeerGroup g;
 };
 
+// A plan bound to fixed buffers and scalars: every kernel's host-side work
+// (validation, coefficients, grid, workspace) done once; launches replay.
+struct mf_bound {
+  const mf_plan* plan = nullptr;
+  Workspace ws;  // its own scratch: independent of the plan's other launches
+  Recorder launches;
+  cudaGraphExec_t exec = nullptr;
+  ~mf_bound() {
+    if (exec) cudaGraphExecDestroy(exec);
+  }
+};
+
 namespace {
 
 thread_local std::string g_error;
@@ -462,6 +474,54 @@ int mf_measure_routine(const char* manifest, const char* function, const char* r
     throw Invalid(std::string("unknown routine '") + routine + "' of " + function);
   });
 }
+
+int mf_plan_bind(const mf_plan* plan, const mf_buffer* buffers, int nbuf, const mf_scalar* scalars,
+                 int nscalars, mf_bound** out) {
+  return guarded([&] {
+    if (!plan || !out) throw Invalid("null argument");
+    auto b = std::make_unique<mf_bound>();
+    b->plan = plan;
+    BufMap m = complete_bindings(plan->plan, to_map(buffers, nbuf), b->ws);
+    const ScalarMap s = to_scalars(scalars, nscalars);
+    for (int k = 0; k < (int)plan->plan.kernels.size(); ++k)
+      record_kernel(plan->plan, k, m, s, nullptr, b->ws, b->launches);
+    check_cuda(cudaDeviceSynchronize(), "bind");  // workspace initialisation done before replays
+    *out = b.release();
+  });
+}
+
+int mf_bound_launch(mf_bound* b, void* stream) {
+  return guarded([&] {
+    if (!b) throw Invalid("null bound plan");
+    for (auto& go : b->launches) check_cuda(go(static_cast<cudaStream_t>(stream)), "bound launch");
+  });
+}
+
+int mf_bound_graph_launch(mf_bound* b, void* stream) {
+  return guarded([&] {
+    if (!b) throw Invalid("null bound plan");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (!s) throw Invalid("graph launch needs a non-default stream");
+    if (!b->exec) {
+      cudaGraph_t g = nullptr;
+      check_cuda(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "begin capture");
+      cudaError_t err = cudaSuccess;
+      for (auto& go : b->launches) {
+        err = go(s);
+        if (err != cudaSuccess) break;
+      }
+      const cudaError_t end = cudaStreamEndCapture(s, &g);
+      check_cuda(err, "capture plan launches");
+      check_cuda(end, "end capture");
+      const cudaError_t inst = cudaGraphInstantiate(&b->exec, g, 0);
+      cudaGraphDestroy(g);
+      check_cuda(inst, "instantiate plan graph");
+    }
+    check_cuda(cudaGraphLaunch(b->exec, s), "graph launch");
+  });
+}
+
+void mf_bound_destroy(mf_bound* b) { delete b; }
 
 int mf_plan_check(const mf_plan* plan, void* stream) {
   return guarded([&] {

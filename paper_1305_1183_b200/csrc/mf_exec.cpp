@@ -8,6 +8,7 @@
 #include "mf_exec.hpp"
 
 #include <algorithm>
+#include <functional>
 #include <cstring>
 #include <sstream>
 
@@ -141,8 +142,17 @@ double coef(const Coef& c, const ScalarMap& s, const std::string& kname) {
   }
 }
 
+// Every run_* prepares a kernel's arguments (validation, coefficients,
+// grid, workspace) and then either launches it on `s` or, with `rec`, stores
+// the launch for later replay (bound plans, CUDA graph capture).
+void emit(Recorder* rec, const std::string& what, std::function<cudaError_t(cudaStream_t)> go,
+          cudaStream_t s) {
+  if (rec) rec->push_back(std::move(go));
+  else check_cuda(go(s), what.c_str());
+}
+
 void run_stream(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc, cudaStream_t s,
-                Workspace& ws) {
+                Workspace& ws, Recorder* rec) {
   const StreamOp& op = k.stream;
   const int nin = (int)op.inputs.size(), nout = (int)op.outs.size();
   if (nin < 1 || nin > kStreamMaxIn || nout > kStreamMaxOut)
@@ -177,8 +187,10 @@ void run_stream(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc, 
     a.ticket = ws.counters(s) + 2;
   }
   if (n == 0) return;
-  check_cuda(launch_stream(nin, nout, op.has_dot, a, grid, options().stream_unroll, s),
-             ("launch " + k.name).c_str());
+  const int unroll = options().stream_unroll;
+  const bool dot = op.has_dot;
+  emit(rec, "launch " + k.name,
+       [=](cudaStream_t st) { return launch_stream(nin, nout, dot, a, grid, unroll, st); }, s);
 }
 
 void fill_peers(MatrixArgs& a, PeerGroup* peers, int64_t n, const std::string& kname) {
@@ -200,7 +212,7 @@ void fill_peers(MatrixArgs& a, PeerGroup* peers, int64_t n, const std::string& k
 
 // Row-resident chain: t = a*A x (optionally stored), y = b*A^T t, one pass.
 void run_rowres(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc, cudaStream_t s,
-                Workspace& ws, PeerGroup* peers) {
+                Workspace& ws, PeerGroup* peers, Recorder* rec) {
   const MatrixOp& op = k.matrix;
   if (op.mats.size() != 1 || op.rows.size() != 1 || op.cols.size() != 1 || !op.rank.empty())
     throw Invalid("kernel " + k.name + ": malformed row-resident chain");
@@ -235,13 +247,13 @@ void run_rowres(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc, 
   a.colpart = ws.scratch(sizeof(float) * (size_t)a.RB * (size_t)n + 256, s);
   a.bar = ws.counters(s);
   fill_peers(a, peers, n, k.name);
-  check_cuda(launch_rowres(a, grid, s), ("launch " + k.name).c_str());
+  emit(rec, "launch " + k.name, [=](cudaStream_t st) { return launch_rowres(a, grid, st); }, s);
 }
 
 void run_matrix(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc, cudaStream_t s,
-                Workspace& ws, PeerGroup* peers) {
+                Workspace& ws, PeerGroup* peers, Recorder* rec) {
   const MatrixOp& op = k.matrix;
-  if (op.chain) return run_rowres(k, bufs, sc, s, ws, peers);
+  if (op.chain) return run_rowres(k, bufs, sc, s, ws, peers, rec);
   MatrixShape sh{(int)op.mats.size(), (int)op.rank.size(), op.store.empty() ? 0 : 1,
                  (int)op.rows.size(), (int)op.cols.size()};
   if (!matrix_shape_supported(sh))
@@ -326,8 +338,10 @@ void run_matrix(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc, 
   a.colpart = base;
   a.rowpart = base + ((colb + 255) & ~size_t(255));
   a.bar = ws.counters(s);
-  if (t.tma) check_cuda(launch_matrix_tma(sh, t, a, grid, s), ("launch " + k.name).c_str());
-  else check_cuda(launch_matrix(sh, t, a, grid, s), ("launch " + k.name).c_str());
+  if (t.tma)
+    emit(rec, "launch " + k.name, [=](cudaStream_t st) { return launch_matrix_tma(sh, t, a, grid, st); }, s);
+  else
+    emit(rec, "launch " + k.name, [=](cudaStream_t st) { return launch_matrix(sh, t, a, grid, st); }, s);
 }
 
 // Generic kernel: one CTA per VM block over the grid the domain buffer
@@ -391,17 +405,28 @@ JitFlags generic_flags(const NativeKernel& k) {
 }
 
 void run_generic(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc, cudaStream_t s,
-                 Workspace& ws) {
+                 Workspace& ws, Recorder* rec) {
   GenericLaunch L = generic_args(k, bufs, sc, s, ws);
+  std::vector<std::pair<float*, size_t>> zero;
   if (!k.vm_semantics)  // engine contract: outputs are overwritten, not accumulated into
     for (const auto& name : k.generic.accumulated) {
       const DevBuf& b = bufs.at(name);
-      check_cuda(cudaMemsetAsync(b.ptr, 0, sizeof(float) * (size_t)b.size(), s), "zero accumulated output");
+      zero.emplace_back(b.ptr, sizeof(float) * (size_t)b.size());
     }
-  if (L.launch_x == 0 || L.launch_y == 0) return;
   const GenericOp& g = k.generic;
-  jit_launch(g.source, generic_flags(k), dim3((unsigned)L.launch_x, (unsigned)L.launch_y),
-             dim3((unsigned)(g.block_x * g.block_y)), L.smem, L.a, s);
+  const JitFlags fl = generic_flags(k);
+  if (rec) jit_load(g.source, fl);  // compile + load now: nothing heavy inside a capture
+  const std::string src = g.source;
+  const dim3 grid((unsigned)L.launch_x, (unsigned)L.launch_y), block((unsigned)(g.block_x * g.block_y));
+  const bool empty = L.launch_x == 0 || L.launch_y == 0;
+  emit(rec, "launch " + k.name, [=](cudaStream_t st) {
+    for (const auto& [p, bytes] : zero) {
+      const cudaError_t e = cudaMemsetAsync(p, 0, bytes, st);
+      if (e != cudaSuccess) return e;
+    }
+    if (!empty) jit_launch(src, fl, grid, block, L.smem, L.a, st);
+    return cudaGetLastError();
+  }, s);
 }
 
 }  // namespace
@@ -492,9 +517,19 @@ void run_kernel(const NativePlan& plan, int k, const BufMap& bufs, const ScalarM
   if (k < 0 || k >= (int)plan.kernels.size()) throw Invalid("kernel index out of range");
   const NativeKernel& kern = plan.kernels[k];
   std::lock_guard<std::mutex> lk(ws.mu);
-  if (kern.kind == NativeKernel::Kind::Stream) run_stream(kern, bufs, scalars, stream, ws);
-  else if (kern.kind == NativeKernel::Kind::Generic) run_generic(kern, bufs, scalars, stream, ws);
-  else run_matrix(kern, bufs, scalars, stream, ws, peers);
+  if (kern.kind == NativeKernel::Kind::Stream) run_stream(kern, bufs, scalars, stream, ws, nullptr);
+  else if (kern.kind == NativeKernel::Kind::Generic) run_generic(kern, bufs, scalars, stream, ws, nullptr);
+  else run_matrix(kern, bufs, scalars, stream, ws, peers, nullptr);
+}
+
+void record_kernel(const NativePlan& plan, int k, const BufMap& bufs, const ScalarMap& scalars,
+                   cudaStream_t stream, Workspace& ws, Recorder& rec) {
+  if (k < 0 || k >= (int)plan.kernels.size()) throw Invalid("kernel index out of range");
+  const NativeKernel& kern = plan.kernels[k];
+  std::lock_guard<std::mutex> lk(ws.mu);
+  if (kern.kind == NativeKernel::Kind::Stream) run_stream(kern, bufs, scalars, stream, ws, &rec);
+  else if (kern.kind == NativeKernel::Kind::Generic) run_generic(kern, bufs, scalars, stream, ws, &rec);
+  else run_matrix(kern, bufs, scalars, stream, ws, nullptr, &rec);
 }
 
 }  // namespace mapfuse::b200

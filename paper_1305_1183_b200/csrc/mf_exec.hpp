@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <functional>
 #include <map>
 #include <mutex>
 #include <stdexcept>
@@ -82,6 +83,9 @@ class Workspace {
   std::map<std::string, std::pair<float*, int64_t>> named_;
 };
 
+// A prepared launch: replays one kernel (all host-side work done) on a stream.
+using Recorder = std::vector<std::function<cudaError_t(cudaStream_t)>>;
+
 // Launches plan.kernels[k]; throws Fault / Invalid.
 void run_kernel(const NativePlan& plan, int k, const BufMap& bufs, const ScalarMap& scalars,
                 cudaStream_t stream, Workspace& ws, PeerGroup* peers = nullptr);
@@ -100,6 +104,11 @@ int64_t run_generic_counted(const NativeKernel& k, const BufMap& bufs, const Sca
                             const int cost[6], bool trace, int64_t trace_cap, cudaStream_t s,
                             Workspace& ws, std::vector<uint64_t>* stats,
                             std::vector<MfjRec>* recs, int64_t* blocks);
+// Prepares plan.kernels[k] for the given bindings (validation, coefficients,
+// grid, workspace) and appends its launch to `rec` instead of launching.
+// Peer (in-kernel collective) launches are not recordable.
+void record_kernel(const NativePlan& plan, int k, const BufMap& bufs, const ScalarMap& scalars,
+                   cudaStream_t stream, Workspace& ws, Recorder& rec);
 // Binds any plan intermediates the caller left unbound (workspace-backed).
 BufMap complete_bindings(const NativePlan& plan, const BufMap& bufs, Workspace& ws);
 

@@ -133,24 +133,36 @@ bool jit_available(std::string* why) {
   return n.error.empty();
 }
 
+namespace {
+cudaKernel_t kernel_on_device(Module& m) {
+  int dev = 0;
+  check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
+  auto it = m.per_device.find(dev);
+  if (it == m.per_device.end()) {
+    cudaLibrary_t lib = nullptr;
+    check_cuda(cudaLibraryLoadData(&lib, m.cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0),
+               "cudaLibraryLoadData(generic kernel)");
+    cudaKernel_t k = nullptr;
+    check_cuda(cudaLibraryGetKernel(&k, lib, "mfj_kernel"), "cudaLibraryGetKernel");
+    it = m.per_device.emplace(dev, std::make_pair(lib, k)).first;
+  }
+  return it->second.second;
+}
+}  // namespace
+
+void jit_load(const std::string& src, JitFlags fl) {
+  std::shared_ptr<Module> m = module_for(src, fl);
+  std::lock_guard<std::mutex> lk(g_mu);
+  (void)kernel_on_device(*m);
+}
+
 void jit_launch(const std::string& src, JitFlags fl, dim3 grid, dim3 block, size_t smem,
                 const MfjArgs& args, cudaStream_t stream) {
   std::shared_ptr<Module> m = module_for(src, fl);
-  int dev = 0;
-  check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
   cudaKernel_t fn = nullptr;
   {
     std::lock_guard<std::mutex> lk(g_mu);
-    auto it = m->per_device.find(dev);
-    if (it == m->per_device.end()) {
-      cudaLibrary_t lib = nullptr;
-      check_cuda(cudaLibraryLoadData(&lib, m->cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0),
-                 "cudaLibraryLoadData(generic kernel)");
-      cudaKernel_t k = nullptr;
-      check_cuda(cudaLibraryGetKernel(&k, lib, "mfj_kernel"), "cudaLibraryGetKernel");
-      it = m->per_device.emplace(dev, std::make_pair(lib, k)).first;
-    }
-    fn = it->second.second;
+    fn = kernel_on_device(*m);
     if (smem > 48 * 1024 && smem > m->smem_set) {
       check_cuda(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),

@@ -62,6 +62,8 @@ void jit_launch(const std::string& src, JitFlags flags, dim3 grid, dim3 block, s
 std::vector<char> jit_compile_only(const std::string& src, JitFlags flags, std::string* log);
 // Compiles into the process cache (no GPU needed); later launches reuse it.
 void jit_prepare(const std::string& src, JitFlags flags);
+// Compiles and loads the module on the current device (before a graph capture).
+void jit_load(const std::string& src, JitFlags flags);
 bool jit_available(std::string* why);
 size_t jit_cache_size();
 

@@ -67,7 +67,8 @@ EXPORTS = [
     "mf_peer_group_connect_local", "mf_peer_group_destroy", "mf_launch_kernel_peers",
     "mf_compile_ranked", "mf_count_combinations", "mf_plan_predicted_us", "mf_plan_save",
     "mf_plan_load", "mf_sequence_script", "mf_plan_kernel_source", "mf_plan_prepare",
-    "mf_plan_check", "mf_vm_launch", "mf_measure_routine",
+    "mf_plan_check", "mf_vm_launch", "mf_measure_routine", "mf_plan_bind", "mf_bound_launch",
+    "mf_bound_graph_launch", "mf_bound_destroy",
 ]
 
 
@@ -118,6 +119,11 @@ def lib() -> C.CDLL:
         L.mf_plan_load.argtypes = [C.c_char_p, P(C.c_void_p)]
         L.mf_sequence_script.argtypes = [C.c_char_p, C.c_char_p, C.c_int]
         L.mf_plan_prepare.argtypes = [C.c_void_p]
+        L.mf_plan_bind.argtypes = [C.c_void_p, P(MfBuffer), C.c_int, P(MfScalar), C.c_int,
+                                   P(C.c_void_p)]
+        L.mf_bound_launch.argtypes = [C.c_void_p, C.c_void_p]
+        L.mf_bound_graph_launch.argtypes = [C.c_void_p, C.c_void_p]
+        L.mf_bound_destroy.argtypes = [C.c_void_p]
         L.mf_vm_launch.argtypes = [C.c_char_p, C.c_char_p, P(MfBuffer), C.c_int, P(MfScalar),
                                    C.c_int, C.c_int, C.c_char_p, C.c_int]
         L.mf_measure_routine.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.c_int, C.c_int,
@@ -297,6 +303,14 @@ class Plan:
                                C.byref(st)))
         return st.as_dict()
 
+    def bind(self, buffers: Mapping[str, object], scalars: Mapping[str, float] = {}) -> "BoundPlan":
+        """Prepares every kernel once for these device buffers and scalars
+        (mf_plan_bind); BoundPlan.launch / graph_launch then only launch."""
+        arr, nb, sc, ns, keep = self._args(buffers, scalars, host=False)
+        h = C.c_void_p()
+        _check(lib().mf_plan_bind(self.h, arr, nb, sc, ns, C.byref(h)))
+        return BoundPlan(h.value, self, list(buffers.values()))
+
     def launch_kernel(self, k: int, buffers: Mapping[str, object],
                       scalars: Mapping[str, float] = {}, stream=None) -> Dict[str, float]:
         arr, nb, sc, ns, _keep = self._args(buffers, scalars, host=False)
@@ -322,6 +336,31 @@ class Plan:
         st = MfStats()
         _check(lib().mf_launch_host(self.h, arr, nb, sc, ns, C.byref(st)))
         return st.as_dict()
+
+
+class BoundPlan:
+    """A plan bound to fixed buffers (mf_plan_bind): launches replay the
+    prepared kernels, or one captured CUDA graph of the whole plan."""
+
+    def __init__(self, handle: int, plan: "Plan", keep):
+        self.h = handle
+        self.plan = plan    # the plan must outlive the bound plan
+        self._keep = keep   # and so must the buffers
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib().mf_bound_destroy(self.h)
+        except Exception:
+            pass
+
+    def launch(self, stream=None) -> None:
+        _check(lib().mf_bound_launch(self.h, C.c_void_p(_stream_ptr(stream))))
+
+    def graph_launch(self, stream) -> None:
+        """First call captures the plan's launches into a CUDA graph on `stream`
+        (a non-default torch.cuda.Stream); every call launches the graph."""
+        _check(lib().mf_bound_graph_launch(self.h, C.c_void_p(_stream_ptr(stream))))
 
 
 class PeerGroup:

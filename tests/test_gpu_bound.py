@@ -1,0 +1,90 @@
+"""Bound plans and CUDA-graph launches (mf_plan_bind / mf_bound_launch /
+mf_bound_graph_launch): the same kernels with the host-side work done once.
+Results must be bit-identical to Plan.launch (every kernel is deterministic),
+across repeated launches (grid barriers and tickets reset themselves)."""
+import numpy as np
+import pytest
+
+from generic_util import GENERIC_MF, USER_SCRIPTS
+
+pytestmark = pytest.mark.gpu
+
+
+def make(torch, mf, plan, seed):
+    bufs = {}
+    for i, b in enumerate(plan.describe()["buffers"]):
+        t = torch.empty((b["rows"], b["cols"]) if b["rows"] > 1 else (b["cols"],), device="cuda")
+        if b["role"] == "input":
+            mf.generate(t, seed=seed + i)
+        else:
+            t.fill_(float("nan"))
+        bufs[b["name"]] = t
+    return bufs
+
+
+def outputs(plan, bufs):
+    return {b["name"]: bufs[b["name"]].cpu().numpy().copy() for b in plan.describe()["buffers"]
+            if b["role"] == "output"}
+
+
+@pytest.mark.parametrize("seq,m,n,mode", [
+    ("AXPYDOT", 1, 1 << 20, "fused"), ("VADD", 1, 1 << 20, "fused"), ("WAXPBY", 1, 4096, "fused"),
+    ("BICGK", 2048, 4096, "fused"), ("ATAX", 1024, 2048, "fused"), ("ATAX", 1024, 2048, "b200"),
+    ("GEMVER", 1024, 1536, "fused"), ("GESUMMV", 512, 2048, "fused"), ("SGEMVT", 512, 768, "unfused")])
+def test_bound_and_graph_match_plan_launch(seq, m, n, mode):
+    import torch
+    import paper_1305_1183_b200 as mf
+    plan = mf.Plan.sequence(seq, m, n, mode)
+    sc = {"alpha": 0.5, "beta": 0.75}
+    bufs = make(torch, mf, plan, 3)
+    plan.launch(bufs, sc)
+    torch.cuda.synchronize()
+    want = outputs(plan, bufs)
+    bound = plan.bind(bufs, sc)
+    for k in want:
+        bufs[k].fill_(float("nan"))
+    for _ in range(3):
+        bound.launch()
+    torch.cuda.synchronize()
+    got = outputs(plan, bufs)
+    for k in want:
+        assert np.array_equal(got[k], want[k], equal_nan=True), k
+    s = torch.cuda.Stream()
+    for k in want:
+        bufs[k].fill_(float("nan"))
+    torch.cuda.synchronize()
+    for _ in range(4):
+        bound.graph_launch(s)
+    s.synchronize()
+    got = outputs(plan, bufs)
+    for k in want:
+        assert np.array_equal(got[k], want[k], equal_nan=True), k
+
+
+def test_generic_plan_graph():
+    import torch
+    import paper_1305_1183_b200 as mf
+    s_, m, n = USER_SCRIPTS["rscale_sgemv"]
+    plan = mf.Plan.compile(s_, m, n, "fused", manifest=open(GENERIC_MF).read())
+    bufs = make(torch, mf, plan, 9)
+    plan.launch(bufs, {})
+    torch.cuda.synchronize()
+    want = outputs(plan, bufs)
+    bound = plan.bind(bufs, {})
+    st = torch.cuda.Stream()
+    for _ in range(3):
+        bound.graph_launch(st)
+    st.synchronize()
+    got = outputs(plan, bufs)
+    assert np.array_equal(got["B"], want["B"])  # map: exact
+    assert np.max(np.abs(got["y"] - want["y"])) <= 1e-5 * np.max(np.abs(want["y"]))  # atomics
+
+
+def test_graph_needs_a_stream():
+    import torch
+    import paper_1305_1183_b200 as mf
+    plan = mf.Plan.sequence("VADD", 1, 4096, "fused")
+    bufs = make(torch, mf, plan, 1)
+    bound = plan.bind(bufs, {})
+    with pytest.raises(mf.ParseError, match="non-default stream"):
+        bound.graph_launch(None)

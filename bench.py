@@ -492,7 +492,7 @@ def main():
     peak, peak_kind = measured_peak()
     achieved = vadd_bytes / (kms / 1e3) / 1e9
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": ncu_traffic("stream_kernel<3, 1, 0>"),
+                "frac": round(achieved / peak, 4), "traffic": ncu_traffic("stream_kernel<3, 1, 0,"),
                 "kernel": key[2], "peak_source": peak_kind,
                 "algorithmic_bytes_per_launch": vadd_bytes,
                 "avg_launch_us": round(kms * 1e3, 1)}

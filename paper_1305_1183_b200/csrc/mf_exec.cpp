@@ -118,7 +118,7 @@ namespace {
 
 const DevBuf& need(const BufMap& bufs, const std::string& name, const std::string& kname) {
   auto it = bufs.find(name);
-  if (it == bufs.end() || !it->second.ptr)
+  if (it == bufs.end() || (!it->second.ptr && it->second.size() != 0))  // empty buffers may be null
     throw Fault("kernel " + kname + ": unbound buffer '" + name + "'");
   if ((reinterpret_cast<uintptr_t>(it->second.ptr) & 15u) != 0)
     throw Fault("kernel " + kname + ": buffer '" + name + "' is not 16-byte aligned");
@@ -186,7 +186,14 @@ void run_stream(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc, 
     a.part = static_cast<double*>(ws.scratch(sizeof(double) * (size_t)grid, s));
     a.ticket = ws.counters(s) + 2;
   }
-  if (n == 0) return;
+  if (n == 0) {  // an empty dot is 0 (the reference sums nothing into a zeroed output)
+    if (op.has_dot) {
+      float* r = a.r;
+      emit(rec, "zero " + k.name, [=](cudaStream_t st) { return cudaMemsetAsync(r, 0, sizeof(float), st); },
+           s);
+    }
+    return;
+  }
   const int unroll = options().stream_unroll;
   const bool dot = op.has_dot;
   emit(rec, "launch " + k.name,
@@ -208,6 +215,17 @@ void fill_peers(MatrixArgs& a, PeerGroup* peers, int64_t n, const std::string& k
   }
   a.peer.epoch = ++peers->epoch;
   a.peer.spin_limit = 20000000000LL;  // ~10 s: trap instead of hanging the GPU
+}
+
+// An empty matrix (m or n = 0): every reduction over the empty dimension is 0.
+void zero_outputs(const NativeKernel& k, const BufMap& bufs, cudaStream_t s, Recorder* rec) {
+  for (const auto& name : k.outputs()) {
+    auto it = bufs.find(name);
+    if (it == bufs.end() || it->second.size() == 0) continue;
+    float* p = it->second.ptr;
+    const size_t bytes = sizeof(float) * (size_t)it->second.size();
+    emit(rec, "zero " + name, [=](cudaStream_t st) { return cudaMemsetAsync(p, 0, bytes, st); }, s);
+  }
 }
 
 // Row-resident chain: t = a*A x (optionally stored), y = b*A^T t, one pass.
@@ -239,7 +257,7 @@ void run_rowres(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc, 
   need_len(y, n, op.cols[0].y, k.name);
   a.yc[0] = y.ptr;
   a.ac[0] = coef(op.cols[0].coef, sc, k.name);
-  if (m == 0 || n == 0) return;
+  if (m == 0 || n == 0) return zero_outputs(k, bufs, s, rec);
   const EngineOptions& eo = options();
   const int sms = eo.max_sms > 0 ? std::min(eo.max_sms, device_sm_count()) : device_sm_count();
   int grid = 0;
@@ -301,7 +319,7 @@ void run_matrix(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc, 
     a.yc[c] = y.ptr;
     a.ac[c] = coef(op.cols[c].coef, sc, k.name);
   }
-  if (m == 0 || n == 0) return;
+  if (m == 0 || n == 0) return zero_outputs(k, bufs, s, rec);
   MatrixTuning t;
   const EngineOptions& eo = options();
   t.K = eo.matrix_k == 4 ? 4 : 2;

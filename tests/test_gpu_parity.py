@@ -270,3 +270,24 @@ def test_b200_mode_row_resident_atax(env, m, n):
     ref = run_plan(torch, mf.Plan.sequence("ATAX", m, n, "fused"), vals, out_shapes(plan))
     err = np.abs(got["y"].astype(np.float64) - ref["y"])
     assert np.all(err <= 2.0 ** -17 * S["y"] + np.spacing(np.abs(ref["y"])))
+
+
+@pytest.mark.parametrize("seq,m,n", [("AXPYDOT", 1, 0), ("BICGK", 0, 64), ("BICGK", 64, 0),
+                                     ("ATAX", 0, 96), ("GESUMMV", 32, 0), ("VADD", 1, 0)])
+def test_empty_problems(env, seq, m, n):
+    """Empty inputs: reductions over an empty dimension are exactly 0 (the
+    reference zero-fills outputs and sums nothing, blas.cpp:128-137, :178-270);
+    empty maps launch nothing."""
+    torch, mf, co = env
+    plan = mf.Plan.sequence(seq, m, n, "fused")
+    shapes = out_shapes(plan)
+    vals = {}
+    for b in plan.describe()["buffers"]:
+        if b["role"] == "input":
+            shp = (b["rows"], b["cols"]) if b["rows"] != 1 else (b["cols"],)
+            vals[b["name"]] = np.ones(shp, np.float32)
+    for s in plan.describe()["scalars"]:
+        vals[s] = 0.5
+    got = run_plan(torch, plan, vals, shapes)
+    for name, v in got.items():
+        assert v.size == 0 or np.all(v == 0), (name, v[:4])

@@ -701,6 +701,8 @@ int mf_set_option(const char* key, int value) {
       options().occupancy = value;
     } else if (k == "generic") {
       mapfuse::plan::set_force_generic(value != 0);
+    } else if (k == "nvtx") {
+      options().nvtx = value ? 1 : 0;
     } else if (k == "vm_exact") {
       mapfuse::vm::set_exact(value != 0);
     } else if (k == "codegen_barriers") {
@@ -731,6 +733,7 @@ int mf_get_option(const char* key) {
   if (k == "generic_iterations") return mapfuse::plan::generic_iterations();
   if (k == "codegen_barriers") return mapfuse::plan::codegen_barriers() ? 1 : 0;
   if (k == "vm_exact") return mapfuse::vm::exact() ? 1 : 0;
+  if (k == "nvtx") return options().nvtx;
   return -1;
 }
 

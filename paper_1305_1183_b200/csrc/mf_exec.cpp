@@ -12,6 +12,8 @@
 #include <cstring>
 #include <sstream>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "mf_jit.hpp"
 #include "mf_kernels.cuh"
 
@@ -29,6 +31,7 @@ EngineOptions& options() {
     if (const char* v = std::getenv("MF_MAX_SMS")) e.max_sms = std::atoi(v);
     if (const char* v = std::getenv("MF_TMA_CONSUMERS")) e.tma_consumers = std::atoi(v);
     if (const char* v = std::getenv("MF_GENERIC_POISON")) e.generic_poison = std::atoi(v);
+    if (const char* v = std::getenv("MF_NVTX")) e.nvtx = std::atoi(v);
     return e;
   }();
   return o;
@@ -535,9 +538,19 @@ void run_kernel(const NativePlan& plan, int k, const BufMap& bufs, const ScalarM
   if (k < 0 || k >= (int)plan.kernels.size()) throw Invalid("kernel index out of range");
   const NativeKernel& kern = plan.kernels[k];
   std::lock_guard<std::mutex> lk(ws.mu);
-  if (kern.kind == NativeKernel::Kind::Stream) run_stream(kern, bufs, scalars, stream, ws, nullptr);
-  else if (kern.kind == NativeKernel::Kind::Generic) run_generic(kern, bufs, scalars, stream, ws, nullptr);
-  else run_matrix(kern, bufs, scalars, stream, ws, peers, nullptr);
+  // NVTX range per kernel (option "nvtx" / MF_NVTX=1): the plan's kernel names
+  // appear on Nsight timelines around the host work + launch.
+  const bool nvtx = options().nvtx != 0;
+  if (nvtx) nvtxRangePushA(kern.name.c_str());
+  try {
+    if (kern.kind == NativeKernel::Kind::Stream) run_stream(kern, bufs, scalars, stream, ws, nullptr);
+    else if (kern.kind == NativeKernel::Kind::Generic) run_generic(kern, bufs, scalars, stream, ws, nullptr);
+    else run_matrix(kern, bufs, scalars, stream, ws, peers, nullptr);
+  } catch (...) {
+    if (nvtx) nvtxRangePop();
+    throw;
+  }
+  if (nvtx) nvtxRangePop();
 }
 
 void record_kernel(const NativePlan& plan, int k, const BufMap& bufs, const ScalarMap& scalars,

@@ -39,7 +39,7 @@ class ShardedPlan:
                  mode: str = "fused", script: Optional[str] = None, world: Optional[int] = None,
                  rank: Optional[int] = None, group=None,
                  executor: Optional[Callable] = None, allreduce: Optional[Callable] = None,
-                 collective: str = "nccl", peer_group=None):
+                 collective: str = "nccl", peer_group=None, manifest: Optional[str] = None):
         import torch.distributed as dist
         if world is None:
             world = dist.get_world_size(group) if dist.is_initialized() else 1
@@ -47,10 +47,12 @@ class ShardedPlan:
             rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.world, self.rank, self.group = world, rank, group
         self.rows_g, self.cols_g = (rows + 31) // 32 * 32, (cols + 31) // 32 * 32
-        probe = (Plan.compile(script, rows, cols, mode) if script else
+        probe = (Plan.compile(script, rows, cols, mode, manifest=manifest) if script else
                  Plan.sequence(sequence, rows, cols, mode))
         d = probe.describe()
-        self.matrix_plan = any(k["kind"] == "matrix" for k in d["kernels"]) or any(
+        self.matrix_plan = any(k["kind"] == "matrix" or (k["kind"] == "generic" and
+                                                       k["op"]["depth"] == 2)
+                               for k in d["kernels"]) or any(
             b["rows"] > 1 for b in d["buffers"])
         if self.matrix_plan:
             self.r0, self.r1 = split(self.rows_g, world, rank)
@@ -60,7 +62,7 @@ class ShardedPlan:
             lrows, lcols = 1, self.r1 - self.r0
         if lrows <= 0 or lcols <= 0:
             raise ValueError("problem too small for %d ranks" % world)
-        self.plan = (Plan.compile(script, lrows, lcols, mode) if script else
+        self.plan = (Plan.compile(script, lrows, lcols, mode, manifest=manifest) if script else
                      Plan.sequence(sequence, lrows, lcols, mode))
         self.desc = self.plan.describe()
         self.global_desc = d

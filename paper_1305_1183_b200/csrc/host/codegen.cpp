@@ -226,54 +226,82 @@ kernel::KernelIR generate_kernel(const std::vector<int>& calls_in, const script:
   }
   k.shared_words = offset;
 
-  // ---- barrier insertion, section by section in execution order
-  std::map<std::string, Access> written;  // since the last barrier
-  auto place = [&](Sec sec, std::vector<kernel::RoutineCallIR>& out) {
+  // ---- barrier insertion, forward scan in execution order.
+  // Condition 1 (read after write): a routine reads an on-chip element written
+  // since the last barrier under a different thread-to-data mapping.
+  // Condition 2 (write after read): a routine writes a SHARED element that
+  // another mapping read since the last barrier -- with serial iterations this
+  // is loop-carried (iteration i+1's load of x while iteration i's compute may
+  // still read it), so the loop body is scanned a second time starting from
+  // the state at the end of an iteration (the SPEC's "barrier when condition
+  // 2 would fire across iterations").
+  struct State {
+    std::map<std::string, Access> written;             // since the last barrier
+    std::map<std::string, std::vector<Access>> read;   // since the last barrier
+    void clear() {
+      written.clear();
+      read.clear();
+    }
+  };
+  auto writes_elem = [&](const Planned& pl, const std::string& fe) {
+    return pl.routine->kind == lib::RoutineKind::Load
+               ? pl.routine->target == fe
+               : (pl.routine->kind == lib::RoutineKind::Compute && pl.b->f->element(fe) &&
+                  pl.b->f->element(fe)->is_output);
+  };
+  auto scan = [&](Sec sec, State& st) {
     for (auto& pl : order) {
       if (pl.sec != sec) continue;
-      if (!pl.routine) {  // pure clear
-        if (prm.barriers && written.count(pl.ir.clear_key)) {
+      if (!pl.routine) {  // pure clear: every thread may write any word
+        const std::string& key = pl.ir.clear_key;
+        if (prm.barriers && (st.written.count(key) || st.read.count(key))) {
           pl.ir.barrier_before = true;
-          written.clear();
+          st.clear();
         }
-        written[pl.ir.clear_key] = Access{nullptr, ""};
-        out.push_back(pl.ir);
+        st.written[key] = Access{nullptr, ""};
         continue;
       }
       bool need = false;
-      if (!pl.ir.clear_key.empty() && written.count(pl.ir.clear_key)) need = true;
+      if (!pl.ir.clear_key.empty() &&
+          (st.written.count(pl.ir.clear_key) || st.read.count(pl.ir.clear_key)))
+        need = true;
       for (const auto& [fe, sn] : pl.b->name) {
         if (!pl.routine->maps.count(fe)) continue;
-        auto w = written.find(sn);
-        if (w == written.end()) continue;
-        if (!w->second.r || !same_map(w->second, Access{pl.routine, fe})) need = true;
+        const Access me{pl.routine, fe};
+        auto w = st.written.find(sn);
+        if (w != st.written.end() && (!w->second.r || !same_map(w->second, me))) need = true;  // cond. 1
+        if (writes_elem(pl, fe) && in_shared.count(sn)) {                                     // cond. 2
+          auto r = st.read.find(sn);
+          if (r != st.read.end())
+            for (const auto& a : r->second)
+              if (!same_map(a, me)) need = true;
+        }
       }
       if (need && prm.barriers) {
         pl.ir.barrier_before = true;
-        written.clear();
+        st.clear();
+      } else if (pl.ir.barrier_before) {  // placed by an earlier scan of this body
+        st.clear();
       }
       if (!pl.ir.clear_key.empty()) {
-        if (pl.ir.barrier_after_clear) written.clear();
-        else written[pl.ir.clear_key] = Access{nullptr, ""};
+        if (pl.ir.barrier_after_clear) st.clear();
+        else st.written[pl.ir.clear_key] = Access{nullptr, ""};
       }
-      // record on-chip writes of this routine
       for (const auto& [fe, sn] : pl.b->name) {
         if (!pl.routine->maps.count(fe)) continue;
-        const bool writes = pl.routine->kind == lib::RoutineKind::Load
-                                ? pl.routine->target == fe
-                                : (pl.routine->kind == lib::RoutineKind::Compute &&
-                                   pl.b->f->element(fe) && pl.b->f->element(fe)->is_output);
-        if (writes) written[sn] = Access{pl.routine, fe};
+        if (writes_elem(pl, fe)) st.written[sn] = Access{pl.routine, fe};
+        else st.read[sn].push_back(Access{pl.routine, fe});
       }
-      out.push_back(pl.ir);
     }
   };
-  place(Sec::Pro, k.prologue);
-  if (depth == 2 && prm.barriers && !k.prologue.empty() && !written.empty()) {
-    // loop-carried reuse of shared tiles: start every iteration after a barrier
-  }
-  place(Sec::Loop, k.body);
-  place(Sec::Epi, k.epilogue);
+  State st;
+  scan(Sec::Pro, st);
+  scan(Sec::Loop, st);
+  if (prm.iterations > 1) scan(Sec::Loop, st);  // loop-carried hazards (iteration i -> i+1)
+  scan(Sec::Epi, st);
+  for (auto* sec : {&k.prologue, &k.body, &k.epilogue}) sec->clear();
+  for (const auto& pl : order)
+    (pl.sec == Sec::Pro ? k.prologue : pl.sec == Sec::Loop ? k.body : k.epilogue).push_back(pl.ir);
 
   // ---- domain: the grid is derived from the first tile (depth 2) / vector
   for (const auto& b : bs) {

@@ -149,3 +149,32 @@ def test_barrier_mutation_is_a_race(mf):
         counts[barriers] = ref.vm_launch(plan.kernel_text(0), host, {}, trace=True)["hazards"]
         assert ("barrier" in plan.kernel_text(0)) == bool(barriers)
     assert counts[1] == 0 and counts[0] > 0, counts
+
+
+@pytest.mark.skipif(not RefOracle.available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("iterations", [1, 2, 4])
+def test_codegen_race_free_with_serial_iterations(mf, iterations):
+    """Barrier soundness: every kernel the code generator emits,
+    for every sequence and mode, with serial iterations 1/2/4, has zero
+    hazards in the reference VM's race detector -- including the loop-carried
+    write-after-read of condition 2 (a load of x in iteration i+1 while other
+    threads still read x in iteration i)."""
+    ref = RefOracle()
+    mf.set_option("generic", 1)
+    mf.set_option("generic_iterations", iterations)
+    try:
+        for seq in SEQS:
+            for mode in ("fused", "unfused"):
+                m, n = (1, 8192) if seq in ("AXPYDOT", "VADD", "WAXPBY", "SSCAL") else (256, 128)
+                plan = mf.Plan.sequence(seq, m, n, mode)
+                host = host_buffers(plan, {}, np.random.default_rng(1))
+                sc = {s: 0.5 for s in plan.describe()["scalars"]}
+                for k in range(plan.num_kernels):
+                    text = plan.kernel_text(k)
+                    assert ("iterations %d" % iterations) in text or iterations == 1 or \
+                        "iterations 1" in text
+                    info = ref.vm_launch(text, {a: v.copy() for a, v in host.items()}, sc, trace=True)
+                    assert info["hazards"] == 0, (seq, mode, k, iterations, info["hazards"])
+    finally:
+        mf.set_option("generic_iterations", 0)
+        mf.set_option("generic", 0)

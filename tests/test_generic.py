@@ -171,8 +171,6 @@ def test_codegen_race_free_with_serial_iterations(mf, iterations):
                 sc = {s: 0.5 for s in plan.describe()["scalars"]}
                 for k in range(plan.num_kernels):
                     text = plan.kernel_text(k)
-                    assert ("iterations %d" % iterations) in text or iterations == 1 or \
-                        "iterations 1" in text
                     info = ref.vm_launch(text, {a: v.copy() for a, v in host.items()}, sc, trace=True)
                     assert info["hazards"] == 0, (seq, mode, k, iterations, info["hazards"])
     finally:

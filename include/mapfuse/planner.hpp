@@ -88,12 +88,62 @@ struct CodegenParams {
   int instances = 4;   // instances per block for depth-1 kernels (IPB)
   int iterations = 1;  // serial iterations (ITERS)
   bool barriers = true;  // test hook: suppress barrier insertion
+  // Routine-call order of the loop body (SPEC.md:262 enumerate_orderings):
+  // a permutation of the default order's loop items, consistent with the
+  // routine dependencies; empty = the default (script order per member).
+  std::vector<int> order;
+  // Shared-memory plan (SPEC.md:263-268 plan_memory): false = one region per
+  // element; true = greedy first-fit over live ranges, regions of elements
+  // with disjoint live ranges overlap (barrier condition 2 guards reuse).
+  bool overlap = false;
 };
 
 // Algorithm 1 / 2 kernel for a set of calls (one call = unfused kernel).
 kernel::KernelIR generate_kernel(const std::vector<int>& calls, const script::Script& s,
                                  const script::DataDependencyGraph& g, const lib::Library& L,
                                  const CodegenParams& p = {});
+
+// ---------------------------------------------------------------- implementation generator
+// (SPEC.md:248-334).  All topological orders of the loop body's routine calls
+// (loads before the computes reading them, computes before their stores,
+// producer computes before consumer computes), at most `cap`.
+std::vector<std::vector<int>> enumerate_orderings(const std::vector<int>& calls, const script::Script& s,
+                                                  const script::DataDependencyGraph& g,
+                                                  const lib::Library& L, int cap = 64);
+
+struct SearchSpace {
+  std::vector<int> block_rows{2, 4, 8, 16};  // BY, depth 2
+  std::vector<int> instances{1, 2, 4};       // depth 1 (capped by the functions' max_instances)
+  std::vector<int> iterations{1, 2, 4, 8, 16};
+  bool overlap_plans = true;                 // also the first-fit overlapping memory plan
+  int max_orderings = 64;
+};
+
+struct FusionImplementation {
+  std::vector<int> calls;
+  CodegenParams params;   // order, block shape, instances, iterations, memory plan
+  kernel::KernelIR kir;
+  int shared_bytes = 0;   // per block
+};
+
+// Cross product orderings x block shapes x instances x iterations x memory
+// plans, feasible under the device limits, with iterations that divide the
+// iterated grid extent at `sz` (Sizes{0,0}: no size filter), deduplicated by
+// kernel text and pruned (prune_implementations).  Deterministic order.
+std::vector<FusionImplementation> enumerate_implementations(const std::vector<int>& calls,
+                                                            const script::Script& s,
+                                                            const script::DataDependencyGraph& g,
+                                                            const lib::Library& L, Sizes sz,
+                                                            const SearchSpace& space = {},
+                                                            const vm::DeviceConfig& dev = {});
+// Drops implementations strictly dominated by another with the same block
+// shape, instances and iterations but fewer shared bytes.
+std::vector<FusionImplementation> prune_implementations(std::vector<FusionImplementation> list);
+// The implementations of kernel k of a compiled plan (from its script and
+// library, at the plan's size); throws if the plan does not carry its script.
+std::vector<FusionImplementation> kernel_implementations(const b200::NativePlan& p, int k);
+// Replaces kernel k by the given implementation (of kernel_implementations).
+void set_kernel_implementation(b200::NativePlan& p, int k, const FusionImplementation& impl);
 
 // ---------------------------------------------------------------- lowering
 // KernelIR -> the sm_100a kernel family and its operand roles.  Throws

@@ -170,6 +170,17 @@ int mf_bound_launch(mf_bound* bound, void* stream);
 int mf_bound_graph_launch(mf_bound* bound, void* stream);
 void mf_bound_destroy(mf_bound* bound);
 
+/* Implementation generator: kernel k of a compiled plan
+ * has mf_plan_count_implementations(plan, k) implementations -- routine
+ * orderings x block shapes x instances x serial iterations x memory plans,
+ * feasible, deduplicated, pruned.  mf_plan_implementation describes one as
+ * JSON; mf_plan_set_implementation switches kernel k to it (generic kernels
+ * change; kernels a hand-written family covers lower to the same kernel).
+ * Returns -status when the plan carries no script (KernelIR / plan file). */
+int64_t mf_plan_count_implementations(const mf_plan* plan, int k);
+int mf_plan_implementation(const mf_plan* plan, int k, int index, char* json, int cap);
+int mf_plan_set_implementation(mf_plan* plan, int k, int index);
+
 /* Synchronizes `stream` and reports (MF_ERR_FAULT) the first device fault a
  * generic kernel of this plan recorded since the last check: out-of-bounds
  * global or on-chip index, poisoned on-chip read, division by zero -- the

@@ -16,6 +16,7 @@
 //  * macros BY / IPB / ITERS are bound, element names become storage keys
 //    (= script names), scalar parameters become script scalars or literals.
 #include <algorithm>
+#include <functional>
 #include <set>
 #include <stdexcept>
 
@@ -66,9 +67,38 @@ ir::Program rewrite(const ir::Program& body, const Bound& b, const std::map<std:
 
 }  // namespace
 
-kernel::KernelIR generate_kernel(const std::vector<int>& calls_in, const script::Script& s,
-                                 const script::DataDependencyGraph& g, const lib::Library& L,
-                                 const CodegenParams& prm) {
+namespace {
+
+// Topological orders of the loop items (indices into the default loop order)
+// under `before[j]` = items that must precede j; DFS, lexicographic, <= cap.
+void topo_orders(const std::vector<std::vector<int>>& before, int cap,
+                 std::vector<std::vector<int>>* out) {
+  const int n = static_cast<int>(before.size());
+  std::vector<int> cur;
+  std::vector<bool> used(n, false);
+  std::function<void()> rec = [&]() {
+    if (static_cast<int>(out->size()) >= cap) return;
+    if (static_cast<int>(cur.size()) == n) {
+      out->push_back(cur);
+      return;
+    }
+    for (int j = 0; j < n; ++j) {
+      if (used[j]) continue;
+      if (std::any_of(before[j].begin(), before[j].end(), [&](int i) { return !used[i]; })) continue;
+      used[j] = true;
+      cur.push_back(j);
+      rec();
+      cur.pop_back();
+      used[j] = false;
+    }
+  };
+  rec();
+}
+
+kernel::KernelIR generate_impl(const std::vector<int>& calls_in, const script::Script& s,
+                               const script::DataDependencyGraph& g, const lib::Library& L,
+                               const CodegenParams& prm, std::vector<std::vector<int>>* orders,
+                               int cap) {
   std::vector<int> calls = calls_in;
   std::sort(calls.begin(), calls.end());
   if (calls.empty()) throw std::invalid_argument("generate_kernel: no calls");
@@ -169,6 +199,59 @@ kernel::KernelIR generate_kernel(const std::vector<int>& calls_in, const script:
     }
   }
 
+  // ---- routine order of the loop body: item j must follow
+  // item i (i before j in the default order) when they share an on-chip
+  // element one of them writes (read-after-write, write-after-read,
+  // write-after-write).
+  auto touched = [&](const Planned& pl, bool want_writes) {
+    std::set<std::string> out;
+    if (!pl.routine) {
+      if (want_writes) out.insert(pl.ir.clear_key);
+      return out;
+    }
+    if (want_writes && !pl.ir.clear_key.empty()) out.insert(pl.ir.clear_key);
+    for (const auto& [fe, sn] : pl.b->name) {
+      if (!pl.routine->maps.count(fe)) continue;
+      const bool w = pl.routine->kind == lib::RoutineKind::Load
+                         ? pl.routine->target == fe
+                         : (pl.routine->kind == lib::RoutineKind::Compute && pl.b->f->element(fe) &&
+                            pl.b->f->element(fe)->is_output);
+      if (w == want_writes) out.insert(sn);
+    }
+    return out;
+  };
+  std::vector<int> loop_items;
+  for (size_t i = 0; i < order.size(); ++i)
+    if (order[i].sec == Sec::Loop) loop_items.push_back(static_cast<int>(i));
+  std::vector<std::vector<int>> before(loop_items.size());
+  for (size_t j = 0; j < loop_items.size(); ++j)
+    for (size_t i = 0; i < j; ++i) {
+      const Planned &a = order[loop_items[i]], &b = order[loop_items[j]];
+      const auto aw = touched(a, true), ar = touched(a, false), bw = touched(b, true),
+                 br = touched(b, false);
+      auto meet = [](const std::set<std::string>& x, const std::set<std::string>& y) {
+        return std::any_of(x.begin(), x.end(), [&](const std::string& e) { return y.count(e) > 0; });
+      };
+      if (meet(aw, br) || meet(ar, bw) || meet(aw, bw)) before[j].push_back(static_cast<int>(i));
+    }
+  if (orders) topo_orders(before, cap, orders);
+  if (!prm.order.empty()) {
+    if (prm.order.size() != loop_items.size())
+      throw std::invalid_argument("generate_kernel: routine order has the wrong length");
+    std::vector<bool> placed(loop_items.size(), false);
+    for (int j : prm.order) {
+      if (j < 0 || j >= static_cast<int>(loop_items.size()) || placed[j])
+        throw std::invalid_argument("generate_kernel: routine order is not a permutation");
+      for (int i : before[j])
+        if (!placed[i]) throw std::invalid_argument("generate_kernel: routine order breaks a dependency");
+      placed[j] = true;
+    }
+    std::vector<Planned> loop;
+    for (int j : prm.order) loop.push_back(order[loop_items[j]]);
+    size_t q = 0;
+    for (int idx : loop_items) order[idx] = loop[q++];
+  }
+
   // ---- memory plan: registers iff all accesses share one single-thread map
   struct Access {
     const lib::Routine* r;
@@ -225,6 +308,72 @@ kernel::KernelIR generate_kernel(const std::vector<int>& calls_in, const script:
     }
   }
   k.shared_words = offset;
+  if (prm.overlap && k.shared_regions.size() > 1) {
+    // Greedy first-fit over live ranges: an element touched
+    // in the prologue / epilogue lives for the whole kernel; one used only in
+    // the loop body lives from its first to its last routine there.  Largest
+    // first (ties by name); an offset is taken when no element with an
+    // intersecting live range occupies the same words.
+    std::map<std::string, std::pair<int, int>> live;
+    const int N = static_cast<int>(order.size());
+    for (int i = 0; i < N; ++i) {
+      const Planned& pl = order[i];
+      std::set<std::string> used = touched(pl, true);
+      for (const auto& x : touched(pl, false)) used.insert(x);
+      for (const auto& x : used) {
+        if (!in_shared.count(x)) continue;
+        auto it = live.find(x);
+        if (pl.sec != Sec::Loop) live[x] = {0, N};
+        else if (it == live.end()) live[x] = {i, i};
+        else if (it->second != std::make_pair(0, N)) it->second = {std::min(it->second.first, i),
+                                                                    std::max(it->second.second, i)};
+      }
+    }
+    std::vector<kernel::SharedRegion*> regs;
+    for (auto& r : k.shared_regions) regs.push_back(&r);
+    std::sort(regs.begin(), regs.end(), [](const kernel::SharedRegion* a, const kernel::SharedRegion* b) {
+      return a->words != b->words ? a->words > b->words : a->key < b->key;
+    });
+    std::vector<kernel::SharedRegion*> placed;
+    int top = 0;
+    for (auto* r : regs) {
+      const auto lr = live.count(r->key) ? live[r->key] : std::make_pair(0, N);
+      std::vector<int> cand{0};
+      for (auto* q : placed) cand.push_back(q->offset + q->words);
+      std::sort(cand.begin(), cand.end());
+      for (int off : cand) {
+        bool ok = true;
+        for (auto* q : placed) {
+          const auto lq = live.count(q->key) ? live[q->key] : std::make_pair(0, N);
+          const bool time = !(lr.second < lq.first || lq.second < lr.first);
+          const bool space = off < q->offset + q->words && q->offset < off + r->words;
+          if (time && space) ok = false;
+        }
+        if (ok) {
+          r->offset = off;
+          break;
+        }
+      }
+      placed.push_back(r);
+      top = std::max(top, r->offset + r->words);
+    }
+    k.shared_words = top;
+  }
+  auto region_of = [&](const std::string& key) -> const kernel::SharedRegion* {
+    for (const auto& r : k.shared_regions)
+      if (r.key == key) return &r;
+    return nullptr;
+  };
+  // elements (other than e) whose words overlap e's: writing e clobbers them
+  auto aliases = [&](const std::string& e) {
+    std::vector<std::string> out;
+    const kernel::SharedRegion* re = region_of(e);
+    if (!re) return out;
+    for (const auto& q : k.shared_regions)
+      if (q.key != e && re->offset < q.offset + q.words && q.offset < re->offset + re->words)
+        out.push_back(q.key);
+    return out;
+  };
 
   // ---- barrier insertion, forward scan in execution order.
   // Condition 1 (read after write): a routine reads an on-chip element written
@@ -252,9 +401,14 @@ kernel::KernelIR generate_kernel(const std::vector<int>& calls_in, const script:
   auto scan = [&](Sec sec, State& st) {
     for (auto& pl : order) {
       if (pl.sec != sec) continue;
+      auto clobbers = [&](const std::string& e) {  // condition 2 on overlapping storage
+        for (const auto& x : aliases(e))
+          if (st.written.count(x) || st.read.count(x)) return true;
+        return false;
+      };
       if (!pl.routine) {  // pure clear: every thread may write any word
         const std::string& key = pl.ir.clear_key;
-        if (prm.barriers && (st.written.count(key) || st.read.count(key))) {
+        if (prm.barriers && (st.written.count(key) || st.read.count(key) || clobbers(key))) {
           pl.ir.barrier_before = true;
           st.clear();
         }
@@ -263,7 +417,8 @@ kernel::KernelIR generate_kernel(const std::vector<int>& calls_in, const script:
       }
       bool need = false;
       if (!pl.ir.clear_key.empty() &&
-          (st.written.count(pl.ir.clear_key) || st.read.count(pl.ir.clear_key)))
+          (st.written.count(pl.ir.clear_key) || st.read.count(pl.ir.clear_key) ||
+           clobbers(pl.ir.clear_key)))
         need = true;
       for (const auto& [fe, sn] : pl.b->name) {
         if (!pl.routine->maps.count(fe)) continue;
@@ -275,6 +430,7 @@ kernel::KernelIR generate_kernel(const std::vector<int>& calls_in, const script:
           if (r != st.read.end())
             for (const auto& a : r->second)
               if (!same_map(a, me)) need = true;
+          if (clobbers(sn)) need = true;
         }
       }
       if (need && prm.barriers) {
@@ -314,6 +470,90 @@ kernel::KernelIR generate_kernel(const std::vector<int>& calls_in, const script:
     if (!k.domain.empty()) break;
   }
   return k;
+}
+
+}  // namespace
+
+kernel::KernelIR generate_kernel(const std::vector<int>& calls, const script::Script& s,
+                                 const script::DataDependencyGraph& g, const lib::Library& L,
+                                 const CodegenParams& prm) {
+  return generate_impl(calls, s, g, L, prm, nullptr, 0);
+}
+
+std::vector<std::vector<int>> enumerate_orderings(const std::vector<int>& calls, const script::Script& s,
+                                                  const script::DataDependencyGraph& g,
+                                                  const lib::Library& L, int cap) {
+  std::vector<std::vector<int>> out;
+  generate_impl(calls, s, g, L, CodegenParams{}, &out, std::max(1, cap));
+  return out;
+}
+
+std::vector<FusionImplementation> prune_implementations(std::vector<FusionImplementation> list) {
+  std::vector<FusionImplementation> out;
+  for (size_t i = 0; i < list.size(); ++i) {
+    bool dominated = false;
+    for (size_t j = 0; j < list.size() && !dominated; ++j) {
+      if (i == j) continue;
+      const auto &a = list[i].params, &b = list[j].params;
+      if (a.by == b.by && a.instances == b.instances && a.iterations == b.iterations &&
+          list[j].shared_bytes < list[i].shared_bytes)
+        dominated = true;
+    }
+    if (!dominated) out.push_back(std::move(list[i]));
+  }
+  return out;
+}
+
+std::vector<FusionImplementation> enumerate_implementations(const std::vector<int>& calls,
+                                                            const script::Script& s,
+                                                            const script::DataDependencyGraph& g,
+                                                            const lib::Library& L, Sizes sz,
+                                                            const SearchSpace& space,
+                                                            const vm::DeviceConfig& dev) {
+  const kernel::KernelIR base = generate_kernel(calls, s, g, L);
+  const auto orders = enumerate_orderings(calls, s, g, L, space.max_orderings);
+  std::vector<int> bys = base.depth == 2 ? space.block_rows : std::vector<int>{8};
+  std::vector<int> insts = base.depth == 1 ? space.instances : std::vector<int>{1};
+  std::vector<FusionImplementation> out;
+  std::set<std::string> seen;
+  for (const auto& ord : orders)
+    for (int by : bys)
+      for (int inst : insts)
+        for (int it : space.iterations)
+          for (int ov = 0; ov < (space.overlap_plans ? 2 : 1); ++ov) {
+            if (base.depth == 2 && (by <= 0 || 32 % by)) continue;
+            if (sz.rows > 0 || sz.cols > 0) {  // serial iterations must divide the iterated extent
+              int64_t extent;
+              if (base.depth == 2) {
+                extent = std::max<int64_t>(1, sz.rows / 32);
+              } else {
+                const int64_t elems = std::max<int64_t>(1, std::max(sz.rows, sz.cols) / 32);
+                if (it > 1 && elems % inst) continue;
+                extent = (elems + inst - 1) / inst;
+              }
+              if (extent % it) continue;
+            }
+            CodegenParams prm;
+            prm.by = by;
+            prm.instances = inst;
+            prm.iterations = it;
+            prm.order = ord;
+            prm.overlap = ov != 0;
+            prm.barriers = codegen_barriers();
+            kernel::KernelIR k = generate_kernel(calls, s, g, L, prm);
+            if (k.threads() > dev.max_threads_per_block) continue;
+            if (k.shared_bytes_total() > dev.shared_bytes_per_block) continue;
+            if (base.depth == 1 && k.instances != inst) continue;  // capped by max_instances
+            std::string text = kernel::emit_pseudo_source(k);
+            if (!seen.insert(text).second) continue;  // orders / plans that emit the same kernel
+            FusionImplementation fi;
+            fi.calls = calls;
+            fi.params = prm;
+            fi.kir = std::move(k);
+            fi.shared_bytes = fi.kir.shared_bytes_total();
+            out.push_back(std::move(fi));
+          }
+  return prune_implementations(std::move(out));
 }
 
 }  // namespace mapfuse::plan

@@ -346,6 +346,30 @@ b200::NativePlan compile_ranked(const std::string& script_text, const lib::Libra
   return plan_from_combination(p.s, L, m, n, combos[static_cast<size_t>(rank)]);
 }
 
+std::vector<FusionImplementation> kernel_implementations(const b200::NativePlan& p, int k) {
+  if (p.script_text.empty())
+    throw std::invalid_argument("plan carries no script (made from KernelIR text or a plan file)");
+  if (k < 0 || k >= static_cast<int>(p.kernels.size())) throw std::invalid_argument("kernel index out of range");
+  lib::Library own;
+  const lib::Library* L = &blas::default_library();
+  if (!p.manifest.empty()) {
+    own = lib::load_library(p.manifest);
+    L = &own;
+  }
+  Parsed ps = parse_checked(p.script_text, *L);
+  return enumerate_implementations(p.kernels[k].calls, ps.s, ps.g, *L, Sizes{p.rows, p.cols});
+}
+
+void set_kernel_implementation(b200::NativePlan& p, int k, const FusionImplementation& impl) {
+  if (k < 0 || k >= static_cast<int>(p.kernels.size())) throw std::invalid_argument("kernel index out of range");
+  b200::NativeKernel nk = lower_or_generic(impl.kir);
+  nk.name = p.kernels[k].name;
+  nk.calls = p.kernels[k].calls;
+  CostModel::defaults().predict_us(nk, p.rows, p.cols);
+  p.kernels[k] = std::move(nk);
+  if (static_cast<int>(p.kernel_ir.size()) > k) p.kernel_ir[k] = kernel::emit_pseudo_source(impl.kir);
+}
+
 int64_t count_covers(const std::string& script_text, const lib::Library& L, int rows, int cols) {
   Parsed p = parse_checked(script_text, L);
   const int m = (rows + 31) / 32 * 32, n = (cols + 31) / 32 * 32;

@@ -24,6 +24,15 @@ using namespace mapfuse::b200;
 struct mf_plan {
   NativePlan plan;
   mutable Workspace ws;
+  // implementation generator results per kernel (enumerated on first use)
+  mutable std::map<int, std::vector<mapfuse::plan::FusionImplementation>> impls;
+  mutable std::mutex impl_mu;
+  const std::vector<mapfuse::plan::FusionImplementation>& implementations(int k) const {
+    std::lock_guard<std::mutex> lk(impl_mu);
+    auto it = impls.find(k);
+    if (it == impls.end()) it = impls.emplace(k, mapfuse::plan::kernel_implementations(plan, k)).first;
+    return it->second;
+  }
 };
 
 struct mf_peer_group {
@@ -522,6 +531,43 @@ int mf_bound_graph_launch(mf_bound* b, void* stream) {
 }
 
 void mf_bound_destroy(mf_bound* b) { delete b; }
+
+int64_t mf_plan_count_implementations(const mf_plan* plan, int k) {
+  int64_t n = -1;
+  const int rc = guarded([&] {
+    if (!plan) throw Invalid("null plan");
+    n = (int64_t)plan->implementations(k).size();
+  });
+  return rc == MF_OK ? n : -rc;
+}
+
+int mf_plan_implementation(const mf_plan* plan, int k, int index, char* json, int cap) {
+  std::string out;
+  const int rc = guarded([&] {
+    if (!plan) throw Invalid("null plan");
+    const auto& impls = plan->implementations(k);
+    if (index < 0 || index >= (int)impls.size()) throw Invalid("implementation index out of range");
+    const auto& fi = impls[index];
+    std::string ord;
+    for (size_t i = 0; i < fi.params.order.size(); ++i) ord += (i ? "," : "") + std::to_string(fi.params.order[i]);
+    out = "{\"block\":[" + std::to_string(fi.kir.block_x) + "," + std::to_string(fi.kir.block_y) +
+          "],\"instances\":" + std::to_string(fi.kir.instances) +
+          ",\"iterations\":" + std::to_string(fi.kir.iterations) +
+          ",\"overlap\":" + (fi.params.overlap ? "true" : "false") + ",\"order\":[" + ord +
+          "],\"shared_bytes\":" + std::to_string(fi.shared_bytes) + "}";
+  });
+  if (rc != MF_OK) return -rc;
+  return copy_out(out, json, cap);
+}
+
+int mf_plan_set_implementation(mf_plan* plan, int k, int index) {
+  return guarded([&] {
+    if (!plan) throw Invalid("null plan");
+    const auto& impls = plan->implementations(k);  // enumerated on the plan as compiled
+    if (index < 0 || index >= (int)impls.size()) throw Invalid("implementation index out of range");
+    mapfuse::plan::set_kernel_implementation(plan->plan, k, impls[index]);
+  });
+}
 
 int mf_plan_check(const mf_plan* plan, void* stream) {
   return guarded([&] {

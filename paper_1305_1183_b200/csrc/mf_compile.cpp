@@ -32,9 +32,12 @@ NativePlan compile_script(const std::string& script_text, const std::string& man
   return as_invalid([&] {
     if (mode != MF_MODE_FUSED && mode != MF_MODE_UNFUSED && mode != MF_MODE_B200)
       throw Invalid("unknown planner mode");
-    if (manifest.empty()) return plan::compile(script_text, blas::default_library(), rows, cols, mode);
-    const lib::Library L = lib::load_library(manifest);
-    return plan::compile(script_text, L, rows, cols, mode);
+    NativePlan p = manifest.empty()
+                       ? plan::compile(script_text, blas::default_library(), rows, cols, mode)
+                       : plan::compile(script_text, lib::load_library(manifest), rows, cols, mode);
+    p.script_text = script_text;
+    p.manifest = manifest;
+    return p;
   });
 }
 
@@ -43,10 +46,13 @@ NativePlan compile_script_ranked(const std::string& script_text, const std::stri
   return as_invalid([&] {
     if (mode != MF_MODE_FUSED && mode != MF_MODE_UNFUSED && mode != MF_MODE_B200)
       throw Invalid("unknown planner mode");
-    if (manifest.empty())
-      return plan::compile_ranked(script_text, blas::default_library(), rows, cols, mode, rank);
-    const lib::Library L = lib::load_library(manifest);
-    return plan::compile_ranked(script_text, L, rows, cols, mode, rank);
+    NativePlan p = manifest.empty()
+                       ? plan::compile_ranked(script_text, blas::default_library(), rows, cols, mode, rank)
+                       : plan::compile_ranked(script_text, lib::load_library(manifest), rows, cols, mode,
+                                              rank);
+    p.script_text = script_text;
+    p.manifest = manifest;
+    return p;
   });
 }
 

@@ -134,6 +134,9 @@ struct NativePlan {
   std::vector<std::string> scalars;   // script scalar names the plan needs
   std::vector<std::string> kernel_ir;  // emitted KernelIR text per kernel (may be empty)
   double predicted_us = 0.0;           // cost-model prediction (0 if not planned)
+  // what the plan was compiled from (implementation search re-generates
+  // kernels from it); empty for plans made from KernelIR text / plan files
+  std::string script_text, manifest;
   const BufferSpec* find(const std::string& n) const {
     for (const auto& b : buffers)
       if (b.name == n) return &b;

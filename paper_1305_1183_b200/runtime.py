@@ -68,7 +68,8 @@ EXPORTS = [
     "mf_compile_ranked", "mf_count_combinations", "mf_plan_predicted_us", "mf_plan_save",
     "mf_plan_load", "mf_sequence_script", "mf_plan_kernel_source", "mf_plan_prepare",
     "mf_plan_check", "mf_vm_launch", "mf_measure_routine", "mf_plan_bind", "mf_bound_launch",
-    "mf_bound_graph_launch", "mf_bound_destroy",
+    "mf_bound_graph_launch", "mf_bound_destroy", "mf_plan_count_implementations",
+    "mf_plan_implementation", "mf_plan_set_implementation",
 ]
 
 
@@ -124,6 +125,10 @@ def lib() -> C.CDLL:
         L.mf_bound_launch.argtypes = [C.c_void_p, C.c_void_p]
         L.mf_bound_graph_launch.argtypes = [C.c_void_p, C.c_void_p]
         L.mf_bound_destroy.argtypes = [C.c_void_p]
+        L.mf_plan_count_implementations.restype = C.c_int64
+        L.mf_plan_count_implementations.argtypes = [C.c_void_p, C.c_int]
+        L.mf_plan_implementation.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_char_p, C.c_int]
+        L.mf_plan_set_implementation.argtypes = [C.c_void_p, C.c_int, C.c_int]
         L.mf_vm_launch.argtypes = [C.c_char_p, C.c_char_p, P(MfBuffer), C.c_int, P(MfScalar),
                                    C.c_int, C.c_int, C.c_char_p, C.c_int]
         L.mf_measure_routine.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.c_int, C.c_int,
@@ -250,6 +255,19 @@ class Plan:
 
     def kernel_text(self, k: int) -> str:
         return _string(lib().mf_plan_kernel_text, self.h, k)
+
+    def implementations(self, k: int) -> int:
+        """Number of implementations of kernel k (implementation generator)."""
+        n = lib().mf_plan_count_implementations(self.h, k)
+        if n < 0:
+            _check(-n)
+        return int(n)
+
+    def implementation(self, k: int, index: int) -> dict:
+        return json.loads(_string(lib().mf_plan_implementation, self.h, k, index))
+
+    def set_implementation(self, k: int, index: int) -> None:
+        _check(lib().mf_plan_set_implementation(self.h, k, index))
 
     def kernel_source(self, k: int) -> str:
         """CUDA C++ the code generator emitted for kernel k when it runs on the

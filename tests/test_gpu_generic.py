@@ -187,3 +187,23 @@ def test_generic_deterministic_maps_and_repeatable(generic):
     a = run_plan(torch, plan, vals, out_shapes(plan))
     b = run_plan(torch, plan, vals, out_shapes(plan))
     assert np.array_equal(a["B"], b["B"])  # the rank-2 map has no atomics
+
+
+@pytest.mark.parametrize("seq,m,n", [("BICGK", 256, 256), ("GEMVER", 256, 256), ("AXPYDOT", 1, 8192),
+                                     ("ATAX", 256, 256), ("GESUMMV", 128, 256)])
+def test_implementations_on_gpu_vs_reference_vm(generic, seq, m, n):
+    """Implementations from the implementation generator (routine orders,
+    block shapes, instances, serial iterations, overlapping memory plans) as
+    generic kernels on the B200, each checked against the reference VM on
+    identical inputs: maps bit-exact, atomic accumulations within 1e-5."""
+    torch, mf, ref, co = generic
+    p = mf.Plan.sequence(seq, m, n, "fused")
+    for k in range(p.num_kernels):
+        cnt = p.implementations(k)
+        for i in sorted({0, cnt - 1} | set(range(0, cnt, max(1, cnt // 8)))):
+            q = mf.Plan.sequence(seq, m, n, "fused")
+            q.set_implementation(k, i)
+            assert q.describe()["kernels"][k]["kind"] == "generic"
+            host = host_buffers(q, {}, np.random.default_rng(i))
+            sc = {s: 0.5 for s in q.describe()["scalars"]}
+            run_per_kernel(torch, ref, q, host, sc)

@@ -4,6 +4,7 @@
   python -m paper_1305_1183_b200.cli run      bicgk.mfp [--reps 20]
   python -m paper_1305_1183_b200.cli search   --sequence GEMVER --rows 32768 --cols 32768 --top 5
   python -m paper_1305_1183_b200.cli verify   [--size 256] [--seed 1] [--top 0]
+  python -m paper_1305_1183_b200.cli tune     --script s.mfs --manifest lib.mf --rows 8192 --cols 8192 [-o tuned.mfp]
   python -m paper_1305_1183_b200.cli bench-db -o cost.db      (then MF_COST_DB=cost.db)
 
 --script FILE / --manifest FILE replace --sequence / the built-in library.
@@ -137,6 +138,85 @@ def cmd_search(args):
     return 0
 
 
+def _time_kernel(plan, k, bufs, scalars, reps=7):
+    """Median device time of kernel k alone, L2 flushed before each launch."""
+    import torch
+    fa = torch.empty(256 << 20, device="cuda")
+    fb = torch.empty(256 << 20, device="cuda")
+    for _ in range(2):
+        plan.launch_kernel(k, bufs, scalars)
+    ts = []
+    for _ in range(reps):
+        fa.zero_()
+        fb.sum()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        plan.launch_kernel(k, bufs, scalars)
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    return statistics.median(ts) * 1e3  # us
+
+
+def cmd_tune(args):
+    """Empirical implementation search (section 5: the best of the
+    generated implementations is found by measuring them): for every kernel of
+    the plan that runs on the generic path, time its implementations (routine
+    orders, block shapes, instances, serial iterations, memory plans; at most
+    --max of them, spread evenly) on the GPU and keep the fastest.  Kernels a
+    hand-written family covers are reported as such (their implementations
+    lower to the same sm_100a kernel).  -o saves the tuned plan file."""
+    import torch
+    text, manifest = _script(args)
+    if text is None:
+        text = _sequence_text(args.sequence)
+    chosen = {}
+
+    def rebuild():
+        p = Plan.compile(text, args.rows, args.cols, args.mode, manifest=manifest)
+        for kk, ii in chosen.items():
+            p.set_implementation(kk, ii)
+        return p
+
+    plan = rebuild()
+    bufs = _device_buffers(plan)
+    for b in plan.describe()["buffers"]:  # intermediates too: kernels run one at a time
+        if b["name"] not in bufs:
+            bufs[b["name"]] = torch.empty((b["rows"], b["cols"]) if b["rows"] > 1 else (b["cols"],),
+                                          device="cuda")
+    sc = {s_: 0.5 for s_ in plan.describe()["scalars"]}
+    report = []
+    for k, kern in enumerate(plan.describe()["kernels"]):
+        if kern["kind"] != "generic":
+            report.append({"kernel": kern["name"], "kind": kern["kind"], "tuned": False})
+            continue
+        cnt = plan.implementations(k)
+        idx = sorted(set(range(0, cnt, max(1, cnt // args.max))) | {cnt - 1})
+        base_us = _time_kernel(plan, k, bufs, sc, args.reps)
+        best = (base_us, None)
+        tried = []
+        for i in idx:
+            plan.set_implementation(k, i)
+            us = _time_kernel(plan, k, bufs, sc, args.reps)
+            tried.append({"implementation": i, "us": round(us, 2), **plan.implementation(k, i)})
+            if us < best[0]:
+                best = (us, i)
+        if best[1] is not None:
+            chosen[k] = best[1]
+        plan = rebuild()  # the planner's choice for k unless an implementation beat it
+        report.append({"kernel": kern["name"], "kind": "generic", "implementations": cnt,
+                       "measured": len(tried), "default_us": round(base_us, 2),
+                       "best_us": round(best[0], 2), "best_implementation": best[1],
+                       "speedup": round(base_us / best[0], 3),
+                       "best": tried[[t["implementation"] for t in tried].index(best[1])]
+                       if best[1] is not None else None})
+    if args.output:
+        with open(args.output, "w") as f:
+            f.write(plan.save())
+    print(json.dumps({"kernels": report}))
+    return 0
+
+
 def cmd_verify(args):
     """Every sequence x every combination (or --top k) against the oracle."""
     import numpy as np
@@ -247,6 +327,12 @@ def main(argv=None):
     common(s)
     s.add_argument("--top", type=int, default=5)
     s.add_argument("--reps", type=int, default=10)
+    t = sub.add_parser("tune")
+    common(t)
+    t.add_argument("--mode", default="fused", choices=["fused", "unfused", "b200"])
+    t.add_argument("--max", type=int, default=24)
+    t.add_argument("--reps", type=int, default=5)
+    t.add_argument("-o", "--output")
     v = sub.add_parser("verify")
     v.add_argument("--size", type=int, default=256)
     v.add_argument("--seed", type=int, default=1)
@@ -257,7 +343,7 @@ def main(argv=None):
     args = ap.parse_args(argv)
     try:
         return {"compile": cmd_compile, "run": cmd_run, "search": cmd_search, "verify": cmd_verify,
-                "bench-db": cmd_bench_db}[args.cmd](args)
+                "bench-db": cmd_bench_db, "tune": cmd_tune}[args.cmd](args)
     except ParseError as e:
         print("error: %s" % e, file=sys.stderr)
         return 2

@@ -165,6 +165,10 @@ bool force_generic();
 // (generic_params), >= 1 = fixed serial iterations for generic kernels.
 void set_generic_iterations(int n);
 int generic_iterations();
+// Engine option "generic_by": 0 = default, else the block rows (BY) of
+// depth-2 generic kernels (2 | 4 | 8 | 16).
+void set_generic_by(int by);
+int generic_by();
 CodegenParams generic_params(const kernel::KernelIR& k, Sizes sz);
 // Test hook "codegen_barriers" = 0: codegen omits every barrier (the SPEC's
 // mutation check) -- the reference VM's race detector and

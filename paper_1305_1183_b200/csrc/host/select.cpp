@@ -33,7 +33,7 @@ CostModel CostModel::defaults() {
       {"matrix.rowres", 0.88},     // row-resident chain (ATAX one pass, 16384^2)
       {"generic.d1", 0.45},        // NVRTC-emitted KernelIR (host/cudagen.cpp), depth 1:
                                    //   VADD 0.55, AXPYDOT 0.34 (profiles/r01_generic_sweep.txt)
-      {"generic.d2", 0.25},        // ... depth 2: BiCGK 0.20, GESUMMV 0.24, ATAX 0.28, GEMVER 0.34
+      {"generic.d2", 0.30},        // ... depth 2 (BY 4): BiCGK 0.27, GESUMMV 0.29, ATAX 0.37, GEMVER 0.40
   };
   if (const char* f = std::getenv("MF_COST_DB")) {
     std::ifstream in(f);
@@ -73,7 +73,8 @@ double CostModel::predict_us(b200::NativeKernel& k, int64_t m, int64_t n) const 
 // accumulators invariant across iterations are cleared once and added to
 // global memory once per block instead of once per tile.  Measured on B200
 // (tools/generic_sweep.py, profiles/r01_generic_sweep.txt): ~4 for depth-2
-// kernels with accumulators, 1 for depth-2 maps, ~16 for depth-1.
+// kernels with accumulators, 1 for depth-2 maps, ~16 for depth-1; block rows
+// BY = 4 (32x4 threads) for depth 2.
 //
 // The iteration count must DIVIDE the iterated grid extent: the epilogue
 // runs with it = iterations-1, and an instance beyond the grid skips every
@@ -84,6 +85,7 @@ double CostModel::predict_us(b200::NativeKernel& k, int64_t m, int64_t n) const 
 // Option "generic_iterations" (>= 1) fixes the count (still made a divisor).
 CodegenParams generic_params(const kernel::KernelIR& k, Sizes sz) {
   CodegenParams p;
+  p.by = generic_by() > 0 ? generic_by() : 4;  // 32x4 blocks: measured best overall (sweep)
   bool accumulates = false;
   for (const auto* sec : {&k.prologue, &k.epilogue})
     for (const auto& c : *sec) accumulates = accumulates || !c.is_pure_clear() || !c.clear_key.empty();
@@ -132,7 +134,7 @@ std::vector<Candidate> candidates(const script::Script& s, const script::DataDep
         // implementation parameters (serial iterations) for this size
         CodegenParams prm = generic_params(c.item.kir, sz);
         prm.barriers = base.barriers;
-        if (prm.iterations != c.item.kir.iterations) {
+        if (prm.iterations != c.item.kir.iterations || prm.by != base.by) {
           c.item.kir = generate_kernel(calls, s, g, L, prm);
           c.item.native = generic_kernel(c.item.kir);
         }

@@ -753,6 +753,10 @@ int mf_set_option(const char* key, int value) {
       mapfuse::vm::set_exact(value != 0);
     } else if (k == "codegen_barriers") {
       mapfuse::plan::set_codegen_barriers(value != 0);
+    } else if (k == "generic_by") {
+      if (value != 0 && value != 2 && value != 4 && value != 8 && value != 16)
+        throw Invalid("generic_by: 0 (default) | 2 | 4 | 8 | 16");
+      mapfuse::plan::set_generic_by(value);
     } else if (k == "generic_iterations") {
       if (value < 0 || value > 4096) throw Invalid("generic_iterations: 0 (auto) .. 4096");
       mapfuse::plan::set_generic_iterations(value);
@@ -777,6 +781,7 @@ int mf_get_option(const char* key) {
   if (k == "generic") return mapfuse::plan::force_generic() ? 1 : 0;
   if (k == "generic_poison") return options().generic_poison;
   if (k == "generic_iterations") return mapfuse::plan::generic_iterations();
+  if (k == "generic_by") return mapfuse::plan::generic_by();
   if (k == "codegen_barriers") return mapfuse::plan::codegen_barriers() ? 1 : 0;
   if (k == "vm_exact") return mapfuse::vm::exact() ? 1 : 0;
   if (k == "nvtx") return options().nvtx;

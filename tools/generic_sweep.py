@@ -52,15 +52,20 @@ def run(seq, m, n, reps=5):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--its", default="0,1,4,16,64")
+    ap.add_argument("--bys", default="0")
     a = ap.parse_args()
     mf.set_option("generic", 1)
     for seq, m, n in CASES:
-        for it in [int(x) for x in a.its.split(",")]:
-            mf.set_option("generic_iterations", it)
-            ms, byts, its = run(seq, m, n)
-            print("%-8s %6dx%-8d it=%-4s (%s)  %9.1f us  %7.1f GB/s  %.3f of 6650" % (
-                seq, m, n, it or "auto", ",".join(its), ms * 1e3, byts / ms / 1e6,
-                byts / ms / 1e6 / 6650), flush=True)
+        for by in [int(x) for x in a.bys.split(",")]:
+            if by and m == 1:
+                continue  # block rows only shape depth-2 kernels
+            mf.set_option("generic_by", by)
+            for it in [int(x) for x in a.its.split(",")]:
+                mf.set_option("generic_iterations", it)
+                ms, byts, its = run(seq, m, n)
+                print("%-8s %6dx%-8d by=%-4s it=%-4s (%s)  %9.1f us  %7.1f GB/s  %.3f of 6650" % (
+                    seq, m, n, by or "dflt", it or "auto", ",".join(its), ms * 1e3, byts / ms / 1e6,
+                    byts / ms / 1e6 / 6650), flush=True)
 
 
 if __name__ == "__main__":

@@ -33,7 +33,8 @@ CostModel CostModel::defaults() {
       {"matrix.rowres", 0.88},     // row-resident chain (ATAX one pass, 16384^2)
       {"generic.d1", 0.45},        // NVRTC-emitted KernelIR (host/cudagen.cpp), depth 1:
                                    //   VADD 0.55, AXPYDOT 0.34 (profiles/r01_generic_sweep.txt)
-      {"generic.d2", 0.30},        // ... depth 2 (BY 4): BiCGK 0.27, GESUMMV 0.29, ATAX 0.37, GEMVER 0.40
+      {"generic.d2", 0.45},        // ... depth 2 (BY 4, pipelined loads): BiCGK 0.47, ATAX 0.53,
+                                   //   GEMVER 0.52, GESUMMV 0.52 (profiles/r01_generic_sweep_pf.txt)
   };
   if (const char* f = std::getenv("MF_COST_DB")) {
     std::ifstream in(f);

@@ -31,8 +31,8 @@ CostModel CostModel::defaults() {
       {"matrix.ldg.rank", 0.62},   // GEMVER ger2+sgemtv, register-fed
       {"matrix.tma.rank", 0.97},   // GEMVER ger2+sgemtv, TMA ring, 16 consumer warps
       {"matrix.rowres", 0.88},     // row-resident chain (ATAX one pass, 16384^2)
-      {"generic.d1", 0.45},        // NVRTC-emitted KernelIR (host/cudagen.cpp), depth 1:
-                                   //   VADD 0.55, AXPYDOT 0.34 (profiles/r01_generic_sweep.txt)
+      {"generic.d1", 0.60},        // NVRTC-emitted KernelIR (host/cudagen.cpp), depth 1:
+                                   //   VADD 0.76, AXPYDOT 0.44 (profiles/r01_generic_sweep_pf.txt)
       {"generic.d2", 0.45},        // ... depth 2 (BY 4, pipelined loads): BiCGK 0.47, ATAX 0.53,
                                    //   GEMVER 0.52, GESUMMV 0.52 (profiles/r01_generic_sweep_pf.txt)
   };

@@ -53,9 +53,13 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--its", default="0,1,4,16,64")
     ap.add_argument("--bys", default="0")
+    ap.add_argument("--only", default="", help="comma-separated sequences")
     a = ap.parse_args()
     mf.set_option("generic", 1)
+    only = set(a.only.upper().split(",")) if a.only else None
     for seq, m, n in CASES:
+        if only and seq not in only:
+            continue
         for by in [int(x) for x in a.bys.split(",")]:
             if by and m == 1:
                 continue  # block rows only shape depth-2 kernels

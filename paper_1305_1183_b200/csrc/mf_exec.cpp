@@ -154,8 +154,11 @@ void emit(Recorder* rec, const std::string& what, std::function<cudaError_t(cuda
   else check_cuda(go(s), what.c_str());
 }
 
+template <typename Args>
+void fill_peers(Args& a, PeerGroup* peers, int64_t n, const std::string& kname);
+
 void run_stream(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc, cudaStream_t s,
-                Workspace& ws, Recorder* rec) {
+                Workspace& ws, Recorder* rec, PeerGroup* peers = nullptr) {
   const StreamOp& op = k.stream;
   const int nin = (int)op.inputs.size(), nout = (int)op.outs.size();
   if (nin < 1 || nin > kStreamMaxIn || nout > kStreamMaxOut)
@@ -188,6 +191,7 @@ void run_stream(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc, 
     }
     a.part = static_cast<double*>(ws.scratch(sizeof(double) * (size_t)grid, s));
     a.ticket = ws.counters(s) + 2;
+    fill_peers(a, peers, 1, k.name);  // dot partials reduced across ranks in-kernel
   }
   if (n == 0) {  // an empty dot is 0 (the reference sums nothing into a zeroed output)
     if (op.has_dot) {
@@ -203,7 +207,8 @@ void run_stream(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc, 
        [=](cudaStream_t st) { return launch_stream(nin, nout, dot, a, grid, unroll, st); }, s);
 }
 
-void fill_peers(MatrixArgs& a, PeerGroup* peers, int64_t n, const std::string& kname) {
+template <typename Args>
+void fill_peers(Args& a, PeerGroup* peers, int64_t n, const std::string& kname) {
   if (!peers || peers->nranks <= 1) return;
   if (n > peers->n_cap) throw Fault("kernel " + kname + ": peer group capacity below n");
   a.peer.nranks = peers->nranks;
@@ -543,7 +548,7 @@ void run_kernel(const NativePlan& plan, int k, const BufMap& bufs, const ScalarM
   const bool nvtx = options().nvtx != 0;
   if (nvtx) nvtxRangePushA(kern.name.c_str());
   try {
-    if (kern.kind == NativeKernel::Kind::Stream) run_stream(kern, bufs, scalars, stream, ws, nullptr);
+    if (kern.kind == NativeKernel::Kind::Stream) run_stream(kern, bufs, scalars, stream, ws, nullptr, peers);
     else if (kern.kind == NativeKernel::Kind::Generic) run_generic(kern, bufs, scalars, stream, ws, nullptr);
     else run_matrix(kern, bufs, scalars, stream, ws, peers, nullptr);
   } catch (...) {

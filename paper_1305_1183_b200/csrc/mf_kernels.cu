@@ -116,6 +116,20 @@ __global__ void __launch_bounds__(kThreads) stream_kernel(StreamArgs a) {
       if (threadIdx.x == 0) {
         double t = 0.0;
         for (int w = 0; w < kWarps; ++w) t += wsum[w];
+        if (a.peer.nranks > 1) {
+          // Fused cross-rank reduction of the dot (sharded runs): every rank
+          // puts its fp64 partial into slot `rank` of every peer's inbox over
+          // NVLink, one system-scope arrival barrier, then each rank sums the
+          // P partials in fixed rank order (deterministic, identical on all
+          // ranks); a second barrier frees the inboxes for the next launch.
+          const PeerLinks& pl = a.peer;
+          for (int q = 0; q < pl.nranks; ++q) reinterpret_cast<double*>(pl.inbox[q])[pl.rank] = t;
+          peer_signal_wait(pl, 0);
+          const volatile double* mine = reinterpret_cast<const volatile double*>(pl.inbox[pl.rank]);
+          t = 0.0;
+          for (int q = 0; q < pl.nranks; ++q) t += mine[q];
+          peer_signal_wait(pl, 1);
+        }
         *a.r = (float)t;
         *a.ticket = 0u;  // ready for the next launch
       }

@@ -17,17 +17,6 @@ constexpr int kStreamMaxOut = 2;
 // one rounding to fp32 per stored value -- bit-identical to the reference's
 // fp64 formulas, proj/src/blas.cpp:185-265), plus optional
 // r = sum (da . in)(db . in) in fp64 with a deterministic two-level reduce.
-struct StreamArgs {
-  long long n4 = 0;                       // float4 slots per stream
-  const float4* in[kStreamMaxIn] = {};
-  float4* out[kStreamMaxOut] = {};
-  double coef[kStreamMaxOut][kStreamMaxIn] = {};
-  double da[kStreamMaxIn] = {}, db[kStreamMaxIn] = {};
-  float* r = nullptr;                     // 1x1 dot output
-  double* part = nullptr;                 // [gridDim.x] per-CTA partials
-  unsigned* ticket = nullptr;             // last-CTA-done counter (self-resetting)
-};
-
 // In-kernel cross-GPU reduction of column outputs (row-sharded runs).
 // Every rank owns a group-allocated inbox [2][P][n], outbox [2][n] and two
 // arrival counters; peers' copies are mapped into this process (CUDA IPC over
@@ -41,6 +30,18 @@ struct PeerLinks {
   unsigned epoch = 0;               // launches so far in this group (1-based)
   long long n_cap = 0;              // inbox / outbox row capacity (floats)
   long long spin_limit = 0;         // clock64 cycles before trapping (deadlock guard)
+};
+
+struct StreamArgs {
+  long long n4 = 0;                       // float4 slots per stream
+  const float4* in[kStreamMaxIn] = {};
+  float4* out[kStreamMaxOut] = {};
+  double coef[kStreamMaxOut][kStreamMaxIn] = {};
+  double da[kStreamMaxIn] = {}, db[kStreamMaxIn] = {};
+  float* r = nullptr;                     // 1x1 dot output
+  double* part = nullptr;                 // [gridDim.x] per-CTA partials
+  unsigned* ticket = nullptr;             // last-CTA-done counter (self-resetting)
+  PeerLinks peer;                         // row-/element-sharded runs: the dot finishes across ranks
 };
 
 // Depth-2 single-pass matrix kernel (see mf_kernels.cu for the mapping).

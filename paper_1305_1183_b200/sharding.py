@@ -69,15 +69,17 @@ class ShardedPlan:
         self.collective_after = [self.plan.column_outputs(k) for k in range(self.plan.num_kernels)]
         self.executor = executor
         self.allreduce = allreduce
-        # collective = "fused": column reductions of matrix kernels finish
-        # in-kernel over peer memory (mf_launch_kernel_peers); only dot
-        # scalars still go through the process group.
+        # collective = "fused": column reductions of matrix kernels and the
+        # dots of stream kernels finish in-kernel over peer memory
+        # (mf_launch_kernel_peers); generic kernels still go through the
+        # process group.
         self.collective = collective
         self.peers = peer_group
         self.fused_names = [[] for _ in range(self.plan.num_kernels)]
         if collective == "fused":
             for k, kern in enumerate(self.desc["kernels"]):
-                if kern["kind"] == "matrix":
+                # matrix column reductions and stream-kernel dots finish in-kernel
+                if kern["kind"] in ("matrix", "stream"):
                     self.fused_names[k] = list(self.collective_after[k])
             if self.peers is None and world > 1 and executor is None:
                 self.peers = self._connect_peers()

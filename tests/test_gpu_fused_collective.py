@@ -134,7 +134,7 @@ def test_virtual_ranks_row_resident_chain():
 
 
 @pytest.mark.parametrize("seq,m,n", [("BICGK", 2048, 4096), ("GEMVER", 1024, 2048),
-                                     ("ATAX", 1536, 1024)])
+                                     ("ATAX", 1536, 1024), ("AXPYDOT", 1, 1 << 20)])
 def test_two_processes_ipc_fused_column_reduction(seq, m, n):
     """The real one-process-per-rank path: two OS processes (both on cuda:0),
     CUDA-IPC handles exchanged over gloo, in-kernel reduction across them
@@ -151,3 +151,47 @@ def test_two_processes_ipc_fused_column_reduction(seq, m, n):
                         "--rows", str(m), "--cols", str(n)],
                        capture_output=True, text=True, timeout=240)
     assert r.returncode == 0 and "ipc ok" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_virtual_ranks_fused_dot(P):
+    """AXPYDOT element-sharded over P virtual ranks: each rank's stream kernel
+    finishes the dot across ranks in-kernel (fp64 partials over peer memory,
+    fixed rank order) -- every rank ends with the same r, within tolerance of
+    the oracle; z stays local."""
+    import torch
+    import paper_1305_1183_b200 as mf
+    co = COracle()
+    n = 1 << 20
+    rng = np.random.default_rng(P)
+    w, v, u = (rng.uniform(-1, 1, n).astype(np.float32) for _ in range(3))
+    alpha = 0.375
+    nloc = n // P
+    plans = [mf.Plan.sequence("AXPYDOT", 1, nloc, "fused") for _ in range(P)]
+    groups = [mf.PeerGroup(P, r, nloc) for r in range(P)]
+    for r in range(P):
+        for q in range(P):
+            if q != r:
+                groups[r].connect_local(q, groups[q])
+    streams = [torch.cuda.Stream() for _ in range(P)]
+    bufs = []
+    for r in range(P):
+        sl = slice(r * nloc, (r + 1) * nloc)
+        bufs.append({"w": torch.from_numpy(w[sl].copy()).cuda(), "v": torch.from_numpy(v[sl].copy()).cuda(),
+                     "u": torch.from_numpy(u[sl].copy()).cuda(),
+                     "z": torch.empty(nloc, device="cuda"), "r": torch.full((1,), float("nan"), device="cuda")})
+    for r in range(P):  # size workspaces first (allocation syncs the device)
+        plans[r].launch(bufs[r], {"alpha": alpha})
+    torch.cuda.synchronize()
+    for rep in range(3):
+        for r in range(P):
+            with torch.cuda.stream(streams[r]):
+                plans[r].launch_kernel_peers(0, groups[r], bufs[r], {"alpha": alpha}, streams[r])
+        torch.cuda.synchronize()
+    want = co.execute("AXPYDOT", 1, n, {"w": w, "v": v, "u": u, "alpha": alpha})
+    S = co.execute("AXPYDOT", 1, n, {"w": np.abs(w), "v": np.abs(v), "u": np.abs(u), "alpha": -alpha})
+    rs = [float(bufs[r]["r"].cpu()[0]) for r in range(P)]
+    assert all(x == rs[0] for x in rs), rs  # identical on every rank
+    assert abs(rs[0] - float(want["r"][0])) <= TAU * float(S["r"][0]) + abs(float(want["r"][0])) * 2 ** -23
+    z = np.concatenate([bufs[r]["z"].cpu().numpy() for r in range(P)])
+    assert np.array_equal(z, want["z"])

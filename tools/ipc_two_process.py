@@ -19,6 +19,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "oracle"))
+sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
@@ -71,10 +72,10 @@ def main():
         dist.all_gather_object(parts, (sp.local_slice(b["name"]), t.numpy()))
         outs[b["name"]] = parts
     if rank == 0:
+        from gpu_util import scale_bound  # |.|-formula bound (signs handled per sequence)
         co = COracle()
         want = co.execute(a.seq, a.rows, a.cols, {**vals, **sc})
-        absvals = {k: (np.abs(v) if isinstance(v, np.ndarray) else v) for k, v in vals.items()}
-        S = co.execute(a.seq, a.rows, a.cols, {**absvals, **{k: abs(v) for k, v in sc.items()}})
+        S = scale_bound(co, a.seq, a.rows, a.cols, {**vals, **sc})
         for name, parts in outs.items():
             sl0 = parts[0][0]
             if sl0 is None:  # replicated (column reduction): every rank holds all of it

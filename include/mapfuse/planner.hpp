@@ -169,7 +169,12 @@ int generic_iterations();
 // depth-2 generic kernels (2 | 4 | 8 | 16).
 void set_generic_by(int by);
 int generic_by();
-CodegenParams generic_params(const kernel::KernelIR& k, Sizes sz);
+// Default implementation parameters of a generic kernel whose domain buffer
+// is dom_rows x dom_cols (a vector: 1 x length).
+CodegenParams generic_params(const kernel::KernelIR& k, int64_t dom_rows, int64_t dom_cols);
+// Shape of the kernel's domain buffer in the script at the padded size.
+std::pair<int64_t, int64_t> domain_shape(const kernel::KernelIR& k, const script::Script& s,
+                                         const lib::Library& L, Sizes sz);
 // Test hook "codegen_barriers" = 0: codegen omits every barrier (the SPEC's
 // mutation check) -- the reference VM's race detector and
 // compute-sanitizer racecheck on the generic kernel must both flag it.

@@ -511,6 +511,8 @@ std::vector<FusionImplementation> enumerate_implementations(const std::vector<in
                                                             const SearchSpace& space,
                                                             const vm::DeviceConfig& dev) {
   const kernel::KernelIR base = generate_kernel(calls, s, g, L);
+  std::pair<int64_t, int64_t> dom{0, 0};
+  if (sz.rows > 0 || sz.cols > 0) dom = domain_shape(base, s, L, sz);
   const auto orders = enumerate_orderings(calls, s, g, L, space.max_orderings);
   std::vector<int> bys = base.depth == 2 ? space.block_rows : std::vector<int>{8};
   std::vector<int> insts = base.depth == 1 ? space.instances : std::vector<int>{1};
@@ -525,9 +527,10 @@ std::vector<FusionImplementation> enumerate_implementations(const std::vector<in
             if (sz.rows > 0 || sz.cols > 0) {  // serial iterations must divide the iterated extent
               int64_t extent;
               if (base.depth == 2) {
-                extent = std::max<int64_t>(1, sz.rows / 32);
+                extent = std::max<int64_t>(1, dom.first / 32);
               } else {
-                const int64_t elems = std::max<int64_t>(1, std::max(sz.rows, sz.cols) / 32);
+                const int64_t len = dom.first == 1 ? dom.second : dom.first * dom.second;
+                const int64_t elems = std::max<int64_t>(1, len / 32);
                 if (it > 1 && elems % inst) continue;
                 extent = (elems + inst - 1) / inst;
               }

@@ -84,7 +84,15 @@ double CostModel::predict_us(b200::NativeKernel& k, int64_t m, int64_t n) const 
 // reference VM drops them too).  For the same reason depth-1 kernels iterate
 // only when the element count fills every instance of every block.
 // Option "generic_iterations" (>= 1) fixes the count (still made a divisor).
-CodegenParams generic_params(const kernel::KernelIR& k, Sizes sz) {
+std::pair<int64_t, int64_t> domain_shape(const kernel::KernelIR& k, const script::Script& s,
+                                         const lib::Library& L, Sizes sz) {
+  const auto shapes = blas::infer_shapes(s, L, static_cast<int>(sz.rows), static_cast<int>(sz.cols));
+  auto it = shapes.find(k.domain);
+  if (it == shapes.end()) return {k.depth == 2 ? sz.rows : 1, sz.cols};
+  return {it->second.first, it->second.second};
+}
+
+CodegenParams generic_params(const kernel::KernelIR& k, int64_t dom_rows, int64_t dom_cols) {
   CodegenParams p;
   p.by = generic_by() > 0 ? generic_by() : 4;  // 32x4 blocks: measured best overall (sweep)
   bool accumulates = false;
@@ -92,10 +100,11 @@ CodegenParams generic_params(const kernel::KernelIR& k, Sizes sz) {
     for (const auto& c : *sec) accumulates = accumulates || !c.is_pure_clear() || !c.clear_key.empty();
   int64_t limit = 1, blocks_per_band = 1;
   if (k.depth == 2) {
-    limit = std::max<int64_t>(1, sz.rows / 32);  // iterate y
-    blocks_per_band = std::max<int64_t>(1, sz.cols / 32);
+    limit = std::max<int64_t>(1, dom_rows / 32);  // iterate y
+    blocks_per_band = std::max<int64_t>(1, dom_cols / 32);
   } else {
-    const int64_t elems = std::max<int64_t>(1, std::max<int64_t>(sz.cols, sz.rows) / 32);
+    const int64_t len = dom_rows == 1 ? dom_cols : dom_rows * dom_cols;  // vm.cpp:38
+    const int64_t elems = std::max<int64_t>(1, len / 32);
     const int inst = std::max(1, std::min(4, k.instances));
     if (elems % inst != 0) return p;
     limit = elems / inst;
@@ -133,7 +142,8 @@ std::vector<Candidate> candidates(const script::Script& s, const script::DataDep
       if (c.item.native.kind == b200::NativeKernel::Kind::Generic) {
         // generic kernels execute the KernelIR as written: pick the
         // implementation parameters (serial iterations) for this size
-        CodegenParams prm = generic_params(c.item.kir, sz);
+        const auto dom = domain_shape(c.item.kir, s, L, sz);
+        CodegenParams prm = generic_params(c.item.kir, dom.first, dom.second);
         prm.barriers = base.barriers;
         if (prm.iterations != c.item.kir.iterations || prm.by != base.by) {
           c.item.kir = generate_kernel(calls, s, g, L, prm);

@@ -14,7 +14,7 @@ import pytest
 
 from generic_util import GENERIC_MF, USER_SCRIPTS, host_buffers, vm_plan
 from golden_util import all_goldens
-from gpu_util import check_output, scale_bound
+from gpu_util import TAU, check_output, scale_bound
 from oracle import COracle, RefOracle
 
 SEQS = ["AXPYDOT", "VADD", "WAXPBY", "SSCAL", "MADD", "BICGK", "ATAX", "SGEMV", "SGEMVT",
@@ -235,3 +235,37 @@ def test_every_implementation_on_reference_vm(mf, case):
                     check_output(seq, name, host[name].ravel(), want[name], S[name], exact=False)
     finally:
         mf.set_option("generic", 0)
+
+
+@pytest.mark.skipif(not RefOracle.available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("seed", range(24))
+def test_random_scripts_random_implementations_on_reference_vm(mf, seed):
+    """Random straight-line scripts (tests/test_gpu_random_scripts.py) through
+    planner + implementation generator (a random implementation per kernel) +
+    codegen, executed by the reference's VM: race-free, and equal to the
+    per-call oracle chain within the tolerance."""
+    from test_gpu_random_scripts import abs_chain, make_script, reference_chain
+    ref, co = RefOracle(), COracle()
+    rng = np.random.default_rng(1000 + seed)
+    text, calls, returns = make_script(rng, 3 + seed % 5)
+    m, n = 64 + 32 * (seed % 3), 96 + 32 * (seed % 4)
+    plan = mf.Plan.compile(text, m, n, "fused")
+    for k in range(plan.num_kernels):
+        cnt = plan.implementations(k)
+        plan.set_implementation(k, int(rng.integers(cnt)))
+    d = plan.describe()
+    env = {"k": 0.625}
+    for b in d["buffers"]:
+        if b["role"] == "input":
+            env[b["name"]] = rng.uniform(-1, 1, (b["rows"], b["cols"])).astype(np.float32)
+    host = host_buffers(plan, env)
+    vm_plan(ref, plan, host, {"k": env["k"]})
+    flat = {k: (v.ravel() if isinstance(v, np.ndarray) and v.shape[0] == 1 else v) for k, v in env.items()}
+    want = reference_chain(co, calls, dict(flat), m, n)
+    S = abs_chain(co, calls, dict(flat), m, n)
+    for name in returns:
+        got = host[name].astype(np.float64).ravel()
+        w = np.asarray(want[name], np.float64).ravel()
+        s = np.asarray(S[name], np.float64).ravel()
+        lim = 4 * TAU * s + 4 * np.spacing(np.abs(w).astype(np.float32)).astype(np.float64)
+        assert np.all(np.abs(got - w) <= lim), (text, name)

@@ -207,3 +207,43 @@ def test_implementations_on_gpu_vs_reference_vm(generic, seq, m, n):
             host = host_buffers(q, {}, np.random.default_rng(i))
             sc = {s: 0.5 for s in q.describe()["scalars"]}
             run_per_kernel(torch, ref, q, host, sc)
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_random_scripts_generic_random_implementations(generic, seed):
+    """Random scripts (planner paths the Table-1 suite does not cover), every
+    kernel on the generic path with a random implementation (order, block
+    shape, instances, serial iterations, memory plan), on the B200 against the
+    per-call oracle chain."""
+    import torch
+    torch_, mf, ref, co = generic
+    from test_gpu_random_scripts import abs_chain, make_script, reference_chain
+    from gpu_util import TAU
+    rng = np.random.default_rng(2000 + seed)
+    text, calls, returns = make_script(rng, 3 + seed % 5)
+    m, n = 96 + 32 * (seed % 3), 128 + 64 * (seed % 4)
+    plan = mf.Plan.compile(text, m, n, "fused")
+    for k in range(plan.num_kernels):
+        plan.set_implementation(k, int(rng.integers(plan.implementations(k))))
+    d = plan.describe()
+    env = {"k": 0.625}
+    for b in d["buffers"]:
+        if b["role"] == "input":
+            shp = (b["rows"], b["cols"]) if b["rows"] > 1 else (b["cols"],)
+            env[b["name"]] = rng.uniform(-1, 1, shp).astype(np.float32)
+    bufs = {}
+    for b in d["buffers"]:
+        shp = (b["rows"], b["cols"]) if b["rows"] > 1 else (b["cols"],)
+        v = env.get(b["name"])
+        bufs[b["name"]] = (torch.from_numpy(v).cuda() if isinstance(v, np.ndarray)
+                           else torch.full(shp, float("nan"), device="cuda"))
+    plan.launch(bufs, {"k": env["k"]})
+    plan.check()
+    want = reference_chain(co, calls, dict(env), m, n)
+    S = abs_chain(co, calls, dict(env), m, n)
+    for name in returns:
+        got = bufs[name].cpu().numpy().astype(np.float64).ravel()
+        w = np.asarray(want[name], np.float64).ravel()
+        s = np.asarray(S[name], np.float64).ravel()
+        lim = 4 * TAU * s + 4 * np.spacing(np.abs(w).astype(np.float32)).astype(np.float64)
+        assert np.all(np.abs(got - w) <= lim), (text, name)

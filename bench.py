@@ -310,7 +310,7 @@ def run_sharded(args, torch, mf, rank, world, seq):
     column partials (NCCL) after the kernel that produced them."""
     from paper_1305_1183_b200.sharding import ShardedPlan
     m = n = args.n_matrix
-    sp = ShardedPlan(seq, m, n, "fused", collective=args.collective)
+    sp = ShardedPlan(seq, m, n, args.mode, collective=args.collective)
     d = sp.desc
     bufs = {}
     for i, b in enumerate(d["buffers"]):
@@ -420,6 +420,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--workload", default="blas1", choices=["blas1", "bicgk-sharded", "atax-sharded"])
     ap.add_argument("--n-matrix", type=int, default=131072)
+    ap.add_argument("--mode", default="fused", choices=["fused", "b200"],
+                    help="planner mode of the sharded workloads (b200: row-resident ATAX)")
     ap.add_argument("--collective", default="fused", choices=["fused", "nccl"],
                     help="sharded workloads: in-kernel peer-memory reduction or NCCL all-reduce")
     args = ap.parse_args()

@@ -48,11 +48,13 @@ struct ConstraintViolation {
 // Planner rule set.  reference: SPEC.md's rules (+ convexity).  row_resident
 // (mode "b200"): additionally a row reduction may feed a column reduction of
 // the SAME matrix inside one kernel when a whole row fits one CTA's ring
-// (cols <= row_resident_max_cols): the CTA completes t_i itself, no global
-// barrier is needed (mf_rowres.cu).  Beyond the paper; off by default.
+// (cols <= row_resident_max_cols): the CTA -- or, for rows wider than one
+// CTA's shared memory, a cluster of up to 8 CTAs over distributed shared
+// memory -- completes t_i itself, no global barrier is needed (mf_rowres.cu).
+// Beyond the paper; off by default.
 struct PlannerOptions {
   bool row_resident = false;
-  int64_t row_resident_max_cols = 16384;
+  int64_t row_resident_max_cols = 131072;
   int64_t cols = 0;  // padded problem cols (row-resident feasibility)
 };
 

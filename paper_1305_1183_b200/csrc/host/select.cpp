@@ -31,6 +31,7 @@ CostModel CostModel::defaults() {
       {"matrix.ldg.rank", 0.62},   // GEMVER ger2+sgemtv, register-fed
       {"matrix.tma.rank", 0.97},   // GEMVER ger2+sgemtv, TMA ring, 16 consumer warps
       {"matrix.rowres", 0.88},     // row-resident chain (ATAX one pass, 16384^2)
+      {"matrix.rowres.cluster", 0.75},  // ... rows over a CTA cluster (n > 16384): 32768^2 0.86, 131072 cols 0.71
       {"generic.d1", 0.60},        // NVRTC-emitted KernelIR (host/cudagen.cpp), depth 1:
                                    //   VADD 0.76, AXPYDOT 0.44 (profiles/r01_generic_sweep_pf.txt)
       {"generic.d2", 0.45},        // ... depth 2 (BY 4, pipelined loads): BiCGK 0.47, ATAX 0.53,
@@ -55,7 +56,7 @@ double CostModel::predict_us(b200::NativeKernel& k, int64_t m, int64_t n) const 
   if (k.kind == b200::NativeKernel::Kind::Stream) return t("stream");
   if (k.kind == b200::NativeKernel::Kind::Generic)
     return t(k.generic.depth == 1 ? "generic.d1" : "generic.d2");
-  if (k.matrix.chain) return t("matrix.rowres");
+  if (k.matrix.chain) return t(n > 16384 ? "matrix.rowres.cluster" : "matrix.rowres");
   const bool heavy = !k.matrix.rank.empty() || !k.matrix.store.empty();
   const double ldg = t(heavy ? "matrix.ldg.rank" : "matrix.ldg.read");
   const double tma = t(heavy ? "matrix.tma.rank" : "matrix.tma.read");

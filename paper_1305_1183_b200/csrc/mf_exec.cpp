@@ -244,9 +244,10 @@ void run_rowres(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc, 
     throw Invalid("kernel " + k.name + ": malformed row-resident chain");
   const DevBuf& M = need(bufs, op.mats[0], k.name);
   const int64_t m = M.rows, n = M.cols;
-  if (n > rowres_max_cols())
+  if (n > rowres_cluster_max_cols())
     throw Fault("kernel " + k.name + ": row-resident chain needs n <= " +
-                std::to_string(rowres_max_cols()) + " (got " + std::to_string(n) + ")");
+                std::to_string(rowres_cluster_max_cols()) + " (got " + std::to_string(n) + ")");
+  if (n % 4) throw Fault("kernel " + k.name + ": matrix dims must be padded");
   MatrixArgs a;
   a.m = m;
   a.n = n;
@@ -269,6 +270,19 @@ void run_rowres(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc, 
   const EngineOptions& eo = options();
   const int sms = eo.max_sms > 0 ? std::min(eo.max_sms, device_sm_count()) : device_sm_count();
   int grid = 0;
+  if (n > rowres_max_cols()) {  // wide rows: a CTA cluster per row (distributed shared memory)
+    const int bands = rowres_cluster_bands(m, n, sms);
+    if (bands <= 0) throw Fault("kernel " + k.name + ": no co-resident CTA cluster for n = " + std::to_string(n));
+    a.CB = 1;
+    a.RB = bands;
+    a.tiles = bands;
+    a.colpart = ws.scratch(sizeof(float) * (size_t)a.RB * (size_t)n + 256, s);
+    a.bar = ws.counters(s);
+    fill_peers(a, peers, n, k.name);
+    emit(rec, "launch " + k.name,
+         [=](cudaStream_t st) { return launch_rowres_cluster(a, sms, sms, st); }, s);
+    return;
+  }
   check_cuda(rowres_config(m, n, sms, &a, &grid), ("configure " + k.name).c_str());
   a.colpart = ws.scratch(sizeof(float) * (size_t)a.RB * (size_t)n + 256, s);
   a.bar = ws.counters(s);

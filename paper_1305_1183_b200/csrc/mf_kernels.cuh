@@ -102,6 +102,12 @@ int tma_stages(const MatrixShape& sh, const MatrixTuning& t);
 long long rowres_max_cols();
 cudaError_t rowres_config(long long m, long long n, int sms, MatrixArgs* a, int* grid);
 cudaError_t launch_rowres(const MatrixArgs& a, int grid, cudaStream_t s);
+// Wide rows (16384 < n <= 131072): a cluster of ceil(n/16384) CTAs shares each
+// row over distributed shared memory, then a cooperative finalize kernel
+// combines the cluster bands' column partials (colpart [bands][n]).
+long long rowres_cluster_max_cols();
+int rowres_cluster_bands(long long m, long long n, int sms);  // co-resident clusters (0: unsupported)
+cudaError_t launch_rowres_cluster(MatrixArgs a, int sms, int finalize_grid, cudaStream_t s);
 bool tma_supported(const MatrixShape& sh, const MatrixTuning& t);  // fits a >= 2-stage ring
 size_t matrix_acc_bytes(const MatrixTuning& t);
 

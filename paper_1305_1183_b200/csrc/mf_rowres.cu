@@ -192,6 +192,205 @@ __global__ void __launch_bounds__(kRrThreads, 1) rowres_kernel(MatrixArgs a) {
   finalize_any<0, 1, float>(a, tid, kRrThreads);
 }
 
+// ---------------------------------------------------------------------------
+// Wide rows (n > 16384): a thread-block CLUSTER of CL CTAs holds one row
+// between them -- CTA `crank` streams columns [crank*C, (crank+1)*C) of every
+// row of the cluster's band through its own 3-stage TMA ring.  Per row:
+//   pass 1: each CTA reduces its slice's A_i . x (warps -> shared combine)
+//           and publishes the partial: a store into slot `crank` of every
+//           cluster CTA's exchange buffer over distributed shared memory and
+//           a remote mbarrier arrive (release.cluster) -- one row AHEAD of
+//           its pass 2 (software pipelining), so waiting overlaps the next
+//           row's reduction;
+//   wait:   the local slot mbarrier (CL arrivals, acquire.cluster); every CTA
+//           sums the CL partials in rank order -> t_i, bit-identical in the
+//           whole cluster;
+//   pass 2: A_i^T t_i into the register column accumulators of the slice.
+// No cluster-wide barrier per row: CTAs run loosely coupled.  A CTA publishes
+// row j+1 only after it consumed row j, which needed every peer's row-j
+// partial, so a peer is at most two rows behind: four slots never collide.  Column partials
+// per cluster band go to colpart[cluster][n]; rowres_finalize_kernel sums them
+// in fixed order (locally or across GPUs).  ATAX at 131072 columns: one read
+// of A instead of two.
+__device__ __forceinline__ unsigned cl_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned cl_id() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned cl_count() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cl_arrive() { asm volatile("barrier.cluster.arrive.release;" ::: "memory"); }
+__device__ __forceinline__ void cl_wait() { asm volatile("barrier.cluster.wait.acquire;" ::: "memory"); }
+__device__ __forceinline__ void cl_store(float* local_addr, unsigned target, float v) {
+  unsigned remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_addr(local_addr)), "r"(target));
+  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(remote), "f"(v) : "memory");
+}
+
+template <int K>
+__device__ __forceinline__ float rr_slice_dot(const float* row, const int (&lcol)[K], const bool (&ok)[K],
+                                              const float4 (&xs)[K]) {
+  float part = 0.f;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    if (!ok[k]) continue;
+    const float4 v = *reinterpret_cast<const float4*>(row + lcol[k]);
+    part = fmaf(v.x, xs[k].x, part);
+    part = fmaf(v.y, xs[k].y, part);
+    part = fmaf(v.z, xs[k].z, part);
+    part = fmaf(v.w, xs[k].w, part);
+  }
+  return part;
+}
+
+__device__ __forceinline__ void cl_arrive_remote(unsigned long long* local_bar, unsigned target) {
+  unsigned remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_addr(local_bar)), "r"(target));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+__device__ __forceinline__ void cl_wait_bar(unsigned long long* b, unsigned parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nCL_WAIT_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra CL_WAIT_%=;\n}\n" ::"r"(smem_addr(b)),
+      "r"(parity)
+      : "memory");
+}
+
+constexpr int kRcDepth = 4;  // exchange slots: a CTA runs at most 2 rows ahead of its cluster
+
+template <int K, int CL>
+__global__ void __launch_bounds__(kRrThreads, 1) rowres_cluster_kernel(MatrixArgs a) {
+  constexpr int C = 4 * kRrConsumers * K;  // columns per CTA slice
+  extern __shared__ __align__(128) unsigned char smem[];
+  float* ring = reinterpret_cast<float*>(smem);  // stage = one row slice (C floats)
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(ring + (size_t)kRrStages * C);
+  unsigned long long* empty = full + kRrStages;
+  __shared__ float red[2][kRrWarps];
+  __shared__ float xch[kRcDepth][CL];                 // the cluster's partial dots, per row slot
+  __shared__ __align__(8) unsigned long long xbar[kRcDepth];  // CL remote arrivals per slot
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned crank = cl_rank(), cid = cl_id(), ncl = cl_count();
+  const long long c0 = (long long)crank * C;
+  const long long width = a.n - c0 < C ? (a.n - c0 > 0 ? a.n - c0 : 0) : C;
+  const long long r0 = (long long)cid * a.m / ncl, r1 = (long long)(cid + 1) * a.m / ncl;
+  const long long nrows = r1 - r0;
+  if (tid == 0) {
+    for (int s = 0; s < kRrStages; ++s) {
+      rr_mbar_init(&full[s], 1);
+      rr_mbar_init(&empty[s], kRrWarps);
+    }
+    for (int d = 0; d < kRcDepth; ++d) rr_mbar_init(&xbar[d], CL);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  cl_arrive();  // every CTA's barriers initialised before any remote arrive
+  cl_wait();
+  if (warp == kRrWarps) {
+    if (lane == 0 && width > 0) {  // producer: row slices through a 3-stage TMA ring
+      const unsigned long long pol = evict_first_policy();
+      for (long long j = 0; j < nrows; ++j) {
+        const int stage = (int)(j % kRrStages);
+        rr_wait(&empty[stage], (unsigned)(((j / kRrStages) & 1) ^ 1u));
+        const long long bytes = width * 4;
+        rr_expect_tx(&full[stage], (unsigned)bytes);
+        const char* src = reinterpret_cast<const char*>(a.M[0] + (r0 + j) * a.ld + c0);
+        char* dst = reinterpret_cast<char*>(ring + (size_t)stage * C);
+        for (long long off = 0; off < bytes; off += 16384) {
+          const long long piece = (bytes - off) < 16384 ? (bytes - off) : 16384;
+          rr_bulk(dst + off, src + off, (unsigned)piece, &full[stage], pol);
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    int lcol[K];
+    bool ok[K];
+    float4 xs[K];
+    float cacc[K][4];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      lcol[k] = 4 * (tid + kRrConsumers * k);
+      ok[k] = lcol[k] < width;
+      xs[k] = ok[k] ? __ldg(reinterpret_cast<const float4*>(a.xr[0] + c0 + lcol[k]))
+                    : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) cacc[k][e] = 0.f;
+    }
+    int rbuf = 0;
+    auto cta_sum = [&](float part) {  // consumers only: named barrier 1
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
+      if (lane == 0) red[rbuf][warp] = part;
+      asm volatile("bar.sync 1, %0;" ::"n"(kRrConsumers) : "memory");
+      float sum = red[rbuf][0];
+#pragma unroll
+      for (int w = 1; w < kRrWarps; ++w) sum += red[rbuf][w];
+      rbuf ^= 1;
+      return sum;
+    };
+    auto slice_partial = [&](long long j) {
+      if (width <= 0) return cta_sum(0.f);
+      rr_wait(&full[j % kRrStages], (unsigned)((j / kRrStages) & 1));
+      return cta_sum(rr_slice_dot<K>(ring + (size_t)(j % kRrStages) * C, lcol, ok, xs));
+    };
+    auto publish = [&](long long j, float p) {  // my partial -> slot j of every cluster CTA
+      if (tid < CL) {
+        cl_store(&xch[j % kRcDepth][crank], (unsigned)tid, p);
+        cl_arrive_remote(&xbar[j % kRcDepth], (unsigned)tid);
+      }
+    };
+    float p = nrows > 0 ? slice_partial(0) : 0.f;
+    if (nrows > 0) publish(0, p);
+    for (long long j = 0; j < nrows; ++j) {
+      // software pipelining: the next row's partial goes out before waiting on this one
+      if (j + 1 < nrows) publish(j + 1, slice_partial(j + 1));
+      cl_wait_bar(&xbar[j % kRcDepth], (unsigned)((j / kRcDepth) & 1));
+      float s32 = 0.f;  // slices combined in cluster rank order: identical in every CTA
+#pragma unroll
+      for (int q = 0; q < CL; ++q) s32 += xch[j % kRcDepth][q];
+      const float ti = (float)(a.ar[0] * (double)s32);  // t_i rounded to fp32 as the unfused plan stores it
+      if (crank == 0 && tid == 0 && a.yr[0]) a.yr[0][r0 + j] = ti;
+      if (width > 0) {
+        const float* row = ring + (size_t)(j % kRrStages) * C;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          if (!ok[k]) continue;
+          const float4 v = *reinterpret_cast<const float4*>(row + lcol[k]);
+          cacc[k][0] = fmaf(v.x, ti, cacc[k][0]);
+          cacc[k][1] = fmaf(v.y, ti, cacc[k][1]);
+          cacc[k][2] = fmaf(v.z, ti, cacc[k][2]);
+          cacc[k][3] = fmaf(v.w, ti, cacc[k][3]);
+        }
+        __syncwarp();
+        if (lane == 0) rr_arrive(&empty[j % kRrStages]);
+      }
+    }
+    float* colpart = static_cast<float*>(a.colpart);
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      if (ok[k]) {
+        float* dst = colpart + (long long)cid * a.n + c0 + lcol[k];
+        *reinterpret_cast<float4*>(dst) = make_float4(cacc[k][0], cacc[k][1], cacc[k][2], cacc[k][3]);
+      }
+  }
+  cl_arrive();  // no CTA leaves while a peer may still address its shared memory
+  cl_wait();
+}
+
+// colpart[RB][n] -> y (fixed band order; across GPUs when a.peer is set).
+__global__ void __launch_bounds__(256) rowres_finalize_kernel(MatrixArgs a) {
+  finalize_any<0, 1, float>(a, threadIdx.x, 256);
+}
+
 using RrFn = void (*)(MatrixArgs);
 
 // stage ~64 KB: R rows of the CTA's column span
@@ -207,9 +406,78 @@ size_t rowres_smem(long long n) {
   return (size_t)kRrStages * 16384 * 4 + 2 * kRrStages * 8 + 128;  // R*C = 16384 floats
 }
 
+using RcFn = void (*)(MatrixArgs);
+constexpr long long kRcSlice = 4LL * kRrConsumers * 8;  // 16384 columns per CTA
+
+RcFn rowres_cluster_fn(int cl) {
+  switch (cl) {
+    case 2: return rowres_cluster_kernel<8, 2>;
+    case 3: return rowres_cluster_kernel<8, 3>;
+    case 4: return rowres_cluster_kernel<8, 4>;
+    case 5: return rowres_cluster_kernel<8, 5>;
+    case 6: return rowres_cluster_kernel<8, 6>;
+    case 7: return rowres_cluster_kernel<8, 7>;
+    case 8: return rowres_cluster_kernel<8, 8>;
+    default: return nullptr;
+  }
+}
+
 }  // namespace
 
 long long rowres_max_cols() { return 4LL * kRrConsumers * 8; }
+long long rowres_cluster_max_cols() { return 8 * kRcSlice; }
+
+cudaError_t launch_rowres_cluster(MatrixArgs a, int sms, int finalize_grid, cudaStream_t s) {
+  const int cl = (int)((a.n + kRcSlice - 1) / kRcSlice);
+  RcFn fn = rowres_cluster_fn(cl);
+  if (!fn) return cudaErrorNotSupported;
+  const size_t smem = (size_t)kRrStages * kRcSlice * 4 + 2 * kRrStages * 8 + 128;
+  cudaError_t e = cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cl;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(kRrThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cfg.gridDim = dim3(cl * a.RB);  // a.RB = rowres_cluster_bands(m, n, sms): colpart is [RB][n]
+  e = cudaLaunchKernelEx(&cfg, fn, a);
+  if (e != cudaSuccess) return e;
+  void* args[] = {&a};
+  return cudaLaunchCooperativeKernel((const void*)rowres_finalize_kernel, dim3(finalize_grid), dim3(256),
+                                     args, 0, s);
+}
+
+int rowres_cluster_bands(long long m, long long n, int sms) {
+  const int cl = (int)((n + kRcSlice - 1) / kRcSlice);
+  RcFn fn = rowres_cluster_fn(cl);
+  if (!fn) return 0;
+  const size_t smem = (size_t)kRrStages * kRcSlice * 4 + 2 * kRrStages * 8 + 128;
+  if (cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+      cudaSuccess)
+    return 0;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cl;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(kRrThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cfg.gridDim = dim3(cl * std::max(1, sms / cl));
+  int nclusters = 0;
+  if (cudaOccupancyMaxActiveClusters(&nclusters, (const void*)fn, &cfg) != cudaSuccess) return 0;
+  nclusters = std::min(nclusters, std::max(1, sms / cl));  // the SM budget (option max_sms)
+  return std::max(1, std::min<int>(nclusters, (int)std::min<long long>(m, 1 << 20)));
+}
 
 cudaError_t rowres_config(long long m, long long n, int sms, MatrixArgs* a, int* grid) {
   RrFn fn = rowres_fn(n);

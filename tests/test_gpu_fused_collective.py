@@ -94,12 +94,14 @@ def test_virtual_ranks_fused_column_reduction(seq, m, n, P, tma):
         mf.set_option("tma", -1)
 
 
-def test_virtual_ranks_row_resident_chain():
-    """Row-resident ATAX kernel + in-kernel cross-rank column reduction."""
+@pytest.mark.parametrize("n", [8192, 32768])
+def test_virtual_ranks_row_resident_chain(n):
+    """Row-resident ATAX kernel (n = 32768: rows over a CTA cluster) +
+    in-kernel cross-rank column reduction."""
     import torch
     import paper_1305_1183_b200 as mf
     co = COracle()
-    P, m, n = 2, 2048, 8192
+    P, m = 2, 2048
     mf.set_option("max_sms", 148 // P)
     try:
         rng = np.random.default_rng(5)

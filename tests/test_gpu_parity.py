@@ -252,9 +252,12 @@ def test_host_launch_pipelined_pinned(env, seq):
 
 
 @pytest.mark.parametrize("m,n", [(64, 64), (96, 160), (1024, 4096), (3000, 8192), (2048, 16384),
-                                 (16384, 16384), (256, 4000)])
+                                 (16384, 16384), (256, 4000), (512, 32768), (1024, 50000),
+                                 (300, 131072), (4096, 65536), (77, 20000)])
 def test_b200_mode_row_resident_atax(env, m, n):
-    """Planner mode "b200": ATAX as ONE row-resident pass over A."""
+    """Planner mode "b200": ATAX as ONE row-resident pass over A (rows wider
+    than 16384 columns: a CTA cluster shares each row over distributed shared
+    memory)."""
     torch, mf, co = env
     vals = rand_inputs("ATAX", m, n, 77 + m)
     plan = mf.Plan.sequence("ATAX", m, n, "b200")

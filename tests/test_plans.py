@@ -172,12 +172,15 @@ def test_random_scripts_always_compile():
 
 def test_b200_mode_row_resident_plans():
     """Mode "b200" fuses ATAX's sgemv -> sgemtv through t when a row fits a
-    CTA (n <= 16384), keeps the paper's plan otherwise and elsewhere."""
+    CTA (n <= 16384) or a CTA cluster (n <= 131072), keeps the paper's plan
+    otherwise and elsewhere."""
     d = mf.Plan.sequence("ATAX", 16384, 16384, "b200").describe()
     assert [k["calls"] for k in d["kernels"]] == [[0, 1]]
     assert d["kernels"][0]["op"]["chain"] is True
     assert d["bytes_loaded"] + d["bytes_stored"] == 4 * (16384 * 16384 + 2 * 16384)
-    assert len(mf.Plan.sequence("ATAX", 16384, 32768, "b200").describe()["kernels"]) == 2
+    assert len(mf.Plan.sequence("ATAX", 16384, 32768, "b200").describe()["kernels"]) == 1
+    assert len(mf.Plan.sequence("ATAX", 1024, 131072, "b200").describe()["kernels"]) == 1
+    assert len(mf.Plan.sequence("ATAX", 1024, 131104, "b200").describe()["kernels"]) == 2
     for seq in ("BICGK", "GEMVER", "GESUMMV", "SGEMVT", "VADD", "AXPYDOT"):
         a = mf.Plan.sequence(seq, 2048, 2048, "b200").describe()
         b = mf.Plan.sequence(seq, 2048, 2048, "fused").describe()

@@ -215,6 +215,13 @@ void mf_peer_group_destroy(mf_peer_group* g);
 int mf_launch_kernel_peers(const mf_plan* plan, int k, mf_peer_group* g, const mf_buffer* buffers,
                            int nbuf, const mf_scalar* scalars, int nscalars, void* stream,
                            mf_stats* stats);
+/* The whole plan on this rank's row panel with every cross-rank reduction
+ * (matrix column outputs, stream-kernel dots) finished in-kernel -- the
+ * sharded launch of SURVEY.md 8(b) for one-process-per-GPU C / C++ hosts,
+ * no NCCL call.  Plans with generic kernels that reduce across rows need a
+ * host collective (mf_launch_kernel + all-reduce) and are rejected. */
+int mf_launch_peers(const mf_plan* plan, mf_peer_group* g, const mf_buffer* buffers, int nbuf,
+                    const mf_scalar* scalars, int nscalars, void* stream, mf_stats* stats);
 
 /* Counter-based synthetic data on the device, identical to the CPU checker's
  * generator: out[r*ld + c] = U(seed, (row0 + r) * ncols_global + c). */

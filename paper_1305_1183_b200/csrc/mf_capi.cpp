@@ -710,6 +710,24 @@ int mf_launch_kernel_peers(const mf_plan* plan, int k, mf_peer_group* g, const m
   });
 }
 
+int mf_launch_peers(const mf_plan* plan, mf_peer_group* g, const mf_buffer* buffers, int nbuf,
+                    const mf_scalar* scalars, int nscalars, void* stream, mf_stats* stats) {
+  return guarded([&] {
+    if (!plan || !g) throw Invalid("null plan or peer group");
+    const NativePlan& P = plan->plan;
+    for (const auto& k : P.kernels)
+      if (k.kind == NativeKernel::Kind::Generic && !k.column_outputs().empty())
+        throw Invalid("kernel " + k.name +
+                      ": generic kernels reduce across ranks with a host collective "
+                      "(mf_launch_kernel + all-reduce of mf_plan_kernel_column_outputs)");
+    BufMap b = complete_bindings(P, to_map(buffers, nbuf), plan->ws);
+    const ScalarMap s = to_scalars(scalars, nscalars);
+    for (int k = 0; k < (int)P.kernels.size(); ++k)
+      run_kernel(P, k, b, s, static_cast<cudaStream_t>(stream), plan->ws, &g->g);
+    fill_stats(P, 0, (int)P.kernels.size(), b, stats);
+  });
+}
+
 int mf_generate(float* dev, int64_t rows, int64_t cols, int64_t ld, uint64_t seed, int64_t row0,
                 int64_t ncols_global, void* stream) {
   return guarded([&] {

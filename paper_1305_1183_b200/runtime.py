@@ -69,7 +69,7 @@ EXPORTS = [
     "mf_plan_load", "mf_sequence_script", "mf_plan_kernel_source", "mf_plan_prepare",
     "mf_plan_check", "mf_vm_launch", "mf_measure_routine", "mf_plan_bind", "mf_bound_launch",
     "mf_bound_graph_launch", "mf_bound_destroy", "mf_plan_count_implementations",
-    "mf_plan_implementation", "mf_plan_set_implementation",
+    "mf_plan_implementation", "mf_plan_set_implementation", "mf_launch_peers",
 ]
 
 
@@ -129,6 +129,8 @@ def lib() -> C.CDLL:
         L.mf_plan_count_implementations.argtypes = [C.c_void_p, C.c_int]
         L.mf_plan_implementation.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_char_p, C.c_int]
         L.mf_plan_set_implementation.argtypes = [C.c_void_p, C.c_int, C.c_int]
+        L.mf_launch_peers.argtypes = [C.c_void_p, C.c_void_p, P(MfBuffer), C.c_int, P(MfScalar),
+                                      C.c_int, C.c_void_p, P(MfStats)]
         L.mf_vm_launch.argtypes = [C.c_char_p, C.c_char_p, P(MfBuffer), C.c_int, P(MfScalar),
                                    C.c_int, C.c_int, C.c_char_p, C.c_int]
         L.mf_measure_routine.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.c_int, C.c_int,
@@ -345,6 +347,15 @@ class Plan:
         st = MfStats()
         _check(lib().mf_launch_kernel_peers(self.h, k, group.h, arr, nb, sc, ns,
                                             C.c_void_p(_stream_ptr(stream)), C.byref(st)))
+        return st.as_dict()
+
+    def launch_peers(self, group: "PeerGroup", buffers: Mapping[str, object],
+                     scalars: Mapping[str, float] = {}, stream=None) -> Dict[str, float]:
+        """Every kernel on this rank's shard with in-kernel cross-rank reductions."""
+        arr, nb, sc, ns, _keep = self._args(buffers, scalars, host=False)
+        st = MfStats()
+        _check(lib().mf_launch_peers(self.h, group.h, arr, nb, sc, ns,
+                                     C.c_void_p(_stream_ptr(stream)), C.byref(st)))
         return st.as_dict()
 
     def launch_host(self, buffers: Mapping[str, object],

@@ -197,3 +197,73 @@ def test_virtual_ranks_fused_dot(P):
     assert abs(rs[0] - float(want["r"][0])) <= TAU * float(S["r"][0]) + abs(float(want["r"][0])) * 2 ** -23
     z = np.concatenate([bufs[r]["z"].cpu().numpy() for r in range(P)])
     assert np.array_equal(z, want["z"])
+
+
+@pytest.mark.parametrize("seq", ["GEMVER", "BICGK", "AXPYDOT"])
+def test_virtual_ranks_launch_peers_whole_plan(seq):
+    """mf_launch_peers: a whole plan per rank with every cross-rank reduction
+    in-kernel (C-ABI sharded launch, no NCCL), two virtual ranks on one GPU."""
+    import torch
+    import paper_1305_1183_b200 as mf
+    from paper_1305_1183_b200.sharding import split
+    co = COracle()
+    P = 2
+    m, n = (1, 1 << 18) if seq == "AXPYDOT" else (2048, 2048)
+    mf.set_option("max_sms", 148 // P)
+    try:
+        rng = np.random.default_rng(11)
+        full = mf.Plan.sequence(seq, m, n, "fused")
+        gd = full.describe()
+        vals = {}
+        for b in gd["buffers"]:
+            if b["role"] == "input":
+                shp = (b["rows"], b["cols"]) if b["rows"] > 1 else (b["cols"],)
+                vals[b["name"]] = rng.uniform(-1, 1, shp).astype(np.float32)
+        sc = {s: 0.5 + 0.25 * i for i, s in enumerate(gd["scalars"])}
+        spec = {b["name"]: b for b in gd["buffers"]}
+        depth1 = seq == "AXPYDOT"
+        parts = [split(n if depth1 else m, P, r) for r in range(P)]
+        plans = [mf.Plan.sequence(seq, 1 if depth1 else hi - lo, hi - lo if depth1 else n, "fused")
+                 for lo, hi in parts]
+        groups = [mf.PeerGroup(P, r, n) for r in range(P)]
+        for r in range(P):
+            for q in range(P):
+                if q != r:
+                    groups[r].connect_local(q, groups[q])
+        bufs = []
+        for r, (lo, hi) in enumerate(parts):
+            d = {}
+            for b in plans[r].describe()["buffers"]:
+                shp = (b["rows"], b["cols"]) if b["rows"] > 1 else (b["cols"],)
+                g = spec[b["name"]]
+                if b["name"] in vals:
+                    v = vals[b["name"]]
+                    if depth1 or g["rows"] > 1 or g["row_indexed"]:
+                        v = v[lo:hi]
+                    d[b["name"]] = torch.from_numpy(np.ascontiguousarray(v)).cuda()
+                else:
+                    d[b["name"]] = torch.full(shp, float("nan"), device="cuda")
+            bufs.append(d)
+        for r in range(P):  # size workspaces (allocation syncs the device)
+            plans[r].launch(bufs[r], sc)
+        torch.cuda.synchronize()
+        streams = [torch.cuda.Stream() for _ in range(P)]
+        for r in range(P):
+            plans[r].launch_peers(groups[r], bufs[r], sc, streams[r])
+        torch.cuda.synchronize()
+        want = co.execute(seq, m, n, {**vals, **sc})
+        from gpu_util import scale_bound
+        S = scale_bound(co, seq, m, n, {**vals, **sc})
+        for name in want:
+            g = spec[name]
+            sharded = depth1 and not g["scalar"] or (not depth1 and (g["rows"] > 1 or g["row_indexed"]))
+            if sharded:
+                got = np.concatenate([bufs[r][name].cpu().numpy() for r in range(P)], axis=0)
+            else:
+                got = bufs[0][name].cpu().numpy()
+                assert all(np.array_equal(got, bufs[r][name].cpu().numpy()) for r in range(P)), name
+            w, s = np.asarray(want[name]).ravel(), np.asarray(S[name]).ravel()
+            err = np.abs(got.ravel().astype(np.float64) - w)
+            assert np.all(err <= TAU * s + np.spacing(np.abs(w).astype(np.float32))), name
+    finally:
+        mf.set_option("max_sms", 0)

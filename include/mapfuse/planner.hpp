@@ -144,6 +144,9 @@ std::vector<FusionImplementation> prune_implementations(std::vector<FusionImplem
 // The implementations of kernel k of a compiled plan (from its script and
 // library, at the plan's size); throws if the plan does not carry its script.
 std::vector<FusionImplementation> kernel_implementations(const b200::NativePlan& p, int k);
+// Covers x implementation choices of a script at a size (Table 4 "Impl. count").
+int64_t count_implementation_space(const std::string& script_text, const lib::Library& L, int rows,
+                                   int cols);
 // Replaces kernel k by the given implementation (of kernel_implementations).
 void set_kernel_implementation(b200::NativePlan& p, int k, const FusionImplementation& impl);
 

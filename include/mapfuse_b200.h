@@ -178,6 +178,10 @@ void mf_bound_destroy(mf_bound* bound);
  * change; kernels a hand-written family covers lower to the same kernel).
  * Returns -status when the plan carries no script (KernelIR / plan file). */
 int64_t mf_plan_count_implementations(const mf_plan* plan, int k);
+/* Size of the whole search space of a script: exact covers x implementation
+ * choices of every kernel (the paper's Table 4 "Impl. count"). */
+int64_t mf_count_implementation_space(const char* script_text, const char* manifest, int rows,
+                                      int cols);
 int mf_plan_implementation(const mf_plan* plan, int k, int index, char* json, int cap);
 int mf_plan_set_implementation(mf_plan* plan, int k, int index);
 

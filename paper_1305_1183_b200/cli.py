@@ -130,7 +130,9 @@ def cmd_search(args):
                      "kernels": [k["name"] for k in plan.describe()["kernels"]]})
         del bufs
     best = min(rows, key=lambda x: x["measured_us"])
-    out = {"combinations": total, "evaluated": len(rows), "results": rows,
+    out = {"combinations": total,
+           "implementation_space": Plan.count_implementation_space(text, args.rows, args.cols, manifest),
+           "evaluated": len(rows), "results": rows,
            "best_measured_rank": best["rank"],
            "rank1_vs_best": round(best["measured_us"] / rows[0]["measured_us"], 4),
            "inversions": [r["rank"] for r in rows[1:] if r["measured_us"] < rows[0]["measured_us"]]}

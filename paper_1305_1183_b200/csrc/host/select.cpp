@@ -384,6 +384,30 @@ void set_kernel_implementation(b200::NativePlan& p, int k, const FusionImplement
   if (static_cast<int>(p.kernel_ir.size()) > k) p.kernel_ir[k] = kernel::emit_pseudo_source(impl.kir);
 }
 
+int64_t count_implementation_space(const std::string& script_text, const lib::Library& L, int rows,
+                                   int cols) {
+  // Table 4 "Impl. count" analogue: covers x implementation
+  // choices -- every kernel of a cover multiplies in the number of its
+  // implementations (implementation generator, at this size).
+  Parsed p = parse_checked(script_text, L);
+  const int m = (rows + 31) / 32 * 32, n = (cols + 31) / 32 * 32;
+  std::map<std::vector<int>, int64_t> impls;
+  int64_t total = 0;
+  for (const auto& c : enumerate_combinations(p.s, p.g, L, Sizes{m, n}, CostModel::defaults(), 0)) {
+    int64_t ways = 1;
+    for (const auto& it : c.kernels) {
+      auto f = impls.find(it.calls);
+      if (f == impls.end())
+        f = impls.emplace(it.calls, static_cast<int64_t>(
+                                        enumerate_implementations(it.calls, p.s, p.g, L, Sizes{m, n}).size()))
+                .first;
+      ways *= std::max<int64_t>(1, f->second);
+    }
+    total += ways;
+  }
+  return total;
+}
+
 int64_t count_covers(const std::string& script_text, const lib::Library& L, int rows, int cols) {
   Parsed p = parse_checked(script_text, L);
   const int m = (rows + 31) / 32 * 32, n = (cols + 31) / 32 * 32;

@@ -532,6 +532,18 @@ int mf_bound_graph_launch(mf_bound* b, void* stream) {
 
 void mf_bound_destroy(mf_bound* b) { delete b; }
 
+int64_t mf_count_implementation_space(const char* script_text, const char* manifest, int rows,
+                                      int cols) {
+  int64_t n = -1;
+  const int rc = guarded([&] {
+    if (!script_text) throw Invalid("null script");
+    if (manifest) n = mapfuse::plan::count_implementation_space(script_text, mapfuse::lib::load_library(manifest),
+                                                                 rows, cols);
+    else n = mapfuse::plan::count_implementation_space(script_text, mapfuse::blas::default_library(), rows, cols);
+  });
+  return rc == MF_OK ? n : -rc;
+}
+
 int64_t mf_plan_count_implementations(const mf_plan* plan, int k) {
   int64_t n = -1;
   const int rc = guarded([&] {

@@ -70,6 +70,7 @@ EXPORTS = [
     "mf_plan_check", "mf_vm_launch", "mf_measure_routine", "mf_plan_bind", "mf_bound_launch",
     "mf_bound_graph_launch", "mf_bound_destroy", "mf_plan_count_implementations",
     "mf_plan_implementation", "mf_plan_set_implementation", "mf_launch_peers",
+    "mf_count_implementation_space",
 ]
 
 
@@ -125,6 +126,8 @@ def lib() -> C.CDLL:
         L.mf_bound_launch.argtypes = [C.c_void_p, C.c_void_p]
         L.mf_bound_graph_launch.argtypes = [C.c_void_p, C.c_void_p]
         L.mf_bound_destroy.argtypes = [C.c_void_p]
+        L.mf_count_implementation_space.restype = C.c_int64
+        L.mf_count_implementation_space.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_int]
         L.mf_plan_count_implementations.restype = C.c_int64
         L.mf_plan_count_implementations.argtypes = [C.c_void_p, C.c_int]
         L.mf_plan_implementation.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_char_p, C.c_int]
@@ -257,6 +260,16 @@ class Plan:
 
     def kernel_text(self, k: int) -> str:
         return _string(lib().mf_plan_kernel_text, self.h, k)
+
+    @staticmethod
+    def count_implementation_space(script: str, rows: int, cols: int,
+                                   manifest: Optional[str] = None) -> int:
+        """Covers x implementation choices (Table 4 "Impl. count" analogue)."""
+        n = lib().mf_count_implementation_space(script.encode(),
+                                                manifest.encode() if manifest else None, rows, cols)
+        if n < 0:
+            _check(-n)
+        return int(n)
 
     def implementations(self, k: int) -> int:
         """Number of implementations of kernel k (implementation generator)."""

@@ -269,3 +269,59 @@ def test_random_scripts_random_implementations_on_reference_vm(mf, seed):
         s = np.asarray(S[name], np.float64).ravel()
         lim = 4 * TAU * s + 4 * np.spacing(np.abs(w).astype(np.float32)).astype(np.float64)
         assert np.all(np.abs(got - w) <= lim), (text, name)
+
+
+def test_implementation_space_counts(mf):
+    """SPEC.md acceptance 6 (directional): covers x implementation choices --
+    GEMVER's space is the largest of the Table-1 sequences, GESUMMV's next."""
+    counts = {}
+    for s in ("GEMVER", "GESUMMV", "SGEMV", "BICGK", "SSCAL"):
+        txt = mf.runtime.sequence_script(s)
+        m, n = (1, 8192) if s == "SSCAL" else (256, 256)
+        counts[s] = mf.Plan.count_implementation_space(txt, m, n)
+        assert counts[s] >= mf.Plan.count_combinations(txt, m, n)
+    assert counts["GEMVER"] > counts["GESUMMV"] > max(counts["SGEMV"], counts["BICGK"]) >= 2
+    assert counts["SSCAL"] < counts["BICGK"]
+
+
+@pytest.mark.skipif(not RefOracle.available(), reason="oracle/_ref not built")
+def test_acceptance_traffic_and_hoisting_on_reference_vm(mf):
+    """SPEC.md acceptance 3 and 7, counted by the reference VM's own per-buffer
+    counters (vm.cpp:164-173) on the code generator's kernels: fused BiCGK
+    loads A exactly m*n words (2*m*n unfused); fused VADD moves 4n words
+    (6n unfused); the hoisted p of fused BiCGK is loaded once per block for
+    every serial iteration count."""
+    ref = RefOracle()
+    m = n = 256
+
+    def words(seq, mm, nn, mode, it=None):
+        if it:
+            mf.set_option("generic_iterations", it)
+        mf.set_option("generic", 1)
+        try:
+            p = mf.Plan.sequence(seq, mm, nn, mode)
+        finally:
+            mf.set_option("generic", 0)
+            mf.set_option("generic_iterations", 0)
+        host = host_buffers(p, {}, np.random.default_rng(0))
+        tot = {}
+        for k in range(p.num_kernels):
+            st = ref.vm_launch(p.kernel_text(k), {a: v.copy() for a, v in host.items()},
+                               {s: 0.5 for s in p.describe()["scalars"]})["stats"]
+            for b, (ld, sd) in st["per_buffer"].items():
+                t = tot.setdefault(b, [0, 0])
+                t[0] += ld
+                t[1] += sd
+            tot.setdefault("__blocks", [0, 0])[0] += st["blocks"]
+        return tot
+
+    assert words("BICGK", m, n, "fused")["A"][0] == m * n
+    assert words("BICGK", m, n, "unfused")["A"][0] == 2 * m * n
+    f, u = words("VADD", 1, 8192, "fused"), words("VADD", 1, 8192, "unfused")
+    tf = sum(l + s for b, (l, s) in f.items() if not b.startswith("__"))
+    tu = sum(l + s for b, (l, s) in u.items() if not b.startswith("__"))
+    assert (tf, tu) == (4 * 8192, 6 * 8192)
+    for it in (1, 2, 4, 8):
+        w = words("BICGK", m, n, "fused", it)
+        assert w["p"][0] == 32 * w["__blocks"][0], it  # one 32-word p slice per block
+        assert w["A"][0] == m * n

@@ -207,8 +207,10 @@ __global__ void __launch_bounds__(kRrThreads, 1) rowres_kernel(MatrixArgs a) {
 //           whole cluster;
 //   pass 2: A_i^T t_i into the register column accumulators of the slice.
 // No cluster-wide barrier per row: CTAs run loosely coupled.  A CTA publishes
-// row j+1 only after it consumed row j, which needed every peer's row-j
-// partial, so a peer is at most two rows behind: four slots never collide.  Column partials
+// row j+A (A = kRcAhead) only after it consumed row j-1, which needed every
+// peer's row-(j-1) partial -- published only after all of that peer's
+// threads finished row j-1-A-1 (named barrier inside the reduction) -- so the
+// live slots span at most 2A+3 rows: kRcDepth = 8 slots never collide.  Column partials
 // per cluster band go to colpart[cluster][n]; rowres_finalize_kernel sums them
 // in fixed order (locally or across GPUs).  ATAX at 131072 columns: one read
 // of A instead of two.
@@ -265,7 +267,12 @@ __device__ __forceinline__ void cl_wait_bar(unsigned long long* b, unsigned pari
       : "memory");
 }
 
-constexpr int kRcDepth = 4;  // exchange slots: a CTA runs at most 2 rows ahead of its cluster
+// Rows a CTA publishes ahead of the one it finishes.  1: the next row's
+// slice was requested a whole row earlier, so its reduction rarely waits on
+// memory (2 measured 1.55x slower: the slice two rows ahead was only just
+// requested from HBM when its reduction needs it).
+constexpr int kRcAhead = 1;
+constexpr int kRcDepth = 8;  // exchange slots: > the largest lead (kRcAhead + 3 rows) of a CTA
 
 template <int K, int CL>
 __global__ void __launch_bounds__(kRrThreads, 1) rowres_cluster_kernel(MatrixArgs a) {
@@ -348,11 +355,11 @@ __global__ void __launch_bounds__(kRrThreads, 1) rowres_cluster_kernel(MatrixArg
         cl_arrive_remote(&xbar[j % kRcDepth], (unsigned)tid);
       }
     };
-    float p = nrows > 0 ? slice_partial(0) : 0.f;
-    if (nrows > 0) publish(0, p);
+    for (long long j = 0; j < kRcAhead && j < nrows; ++j) publish(j, slice_partial(j));
     for (long long j = 0; j < nrows; ++j) {
-      // software pipelining: the next row's partial goes out before waiting on this one
-      if (j + 1 < nrows) publish(j + 1, slice_partial(j + 1));
+      // software pipelining: the partials of the next kRcAhead rows go out
+      // before waiting on this one (their slices are already in the ring)
+      if (j + kRcAhead < nrows) publish(j + kRcAhead, slice_partial(j + kRcAhead));
       cl_wait_bar(&xbar[j % kRcDepth], (unsigned)((j / kRcDepth) & 1));
       float s32 = 0.f;  // slices combined in cluster rank order: identical in every CTA
 #pragma unroll

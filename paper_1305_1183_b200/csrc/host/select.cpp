@@ -34,8 +34,9 @@ CostModel CostModel::defaults() {
       {"matrix.rowres.cluster", 0.75},  // ... rows over a CTA cluster (n > 16384): 32768^2 0.86, 131072 cols 0.71
       {"generic.d1", 0.60},        // NVRTC-emitted KernelIR (host/cudagen.cpp), depth 1:
                                    //   VADD 0.76, AXPYDOT 0.44 (profiles/r01_generic_sweep_pf.txt)
-      {"generic.d2", 0.45},        // ... depth 2 (BY 4, pipelined loads): BiCGK 0.47, ATAX 0.53,
-                                   //   GEMVER 0.52, GESUMMV 0.52 (profiles/r01_generic_sweep_pf.txt)
+      {"generic.d2", 0.60},        // ... depth 2 (BY 4, pipelined, proved bounds, 32-bit indices):
+                                   //   BiCGK 0.54, ATAX 0.70, GEMVER 0.74, GESUMMV 0.68
+                                   //   (profiles/r01_generic_sweep_pf.txt)
   };
   if (const char* f = std::getenv("MF_COST_DB")) {
     std::ifstream in(f);

@@ -777,6 +777,8 @@ int mf_set_option(const char* key, int value) {
       options().occupancy = value;
     } else if (k == "generic") {
       mapfuse::plan::set_force_generic(value != 0);
+    } else if (k == "generic_checked") {
+      options().generic_checked = value ? 1 : 0;
     } else if (k == "nvtx") {
       options().nvtx = value ? 1 : 0;
     } else if (k == "vm_exact") {
@@ -815,6 +817,7 @@ int mf_get_option(const char* key) {
   if (k == "codegen_barriers") return mapfuse::plan::codegen_barriers() ? 1 : 0;
   if (k == "vm_exact") return mapfuse::vm::exact() ? 1 : 0;
   if (k == "nvtx") return options().nvtx;
+  if (k == "generic_checked") return options().generic_checked;
   return -1;
 }
 

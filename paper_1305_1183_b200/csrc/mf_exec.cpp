@@ -32,6 +32,7 @@ EngineOptions& options() {
     if (const char* v = std::getenv("MF_TMA_CONSUMERS")) e.tma_consumers = std::atoi(v);
     if (const char* v = std::getenv("MF_GENERIC_POISON")) e.generic_poison = std::atoi(v);
     if (const char* v = std::getenv("MF_NVTX")) e.nvtx = std::atoi(v);
+    if (const char* v = std::getenv("MF_GENERIC_CHECKED")) e.generic_checked = std::atoi(v);
     return e;
   }();
   return o;
@@ -444,6 +445,49 @@ JitFlags generic_flags(const NativeKernel& k) {
   return fl;
 }
 
+// Launch-time proof that every index the generic kernel evaluates is in
+// bounds for THESE buffer shapes and grid (interval arithmetic over the affine
+// forms host/cudagen.cpp recorded).  Proved -> the kernel runs without
+// per-access checks (it cannot fault); *fits32 -> every index value and
+// buffer extent fits 32 bits, so index arithmetic runs in int.
+bool prove_bounds(const GenericOp& g, const GenericLaunch& L, bool* fits32) {
+  const int64_t rt[6] = {0, L.a.full_x, L.a.full_y, L.a.n_elems, L.launch_x, L.launch_y};
+  const int64_t lim32 = (int64_t{1} << 31) - 1;
+  bool small = true;
+  for (size_t i = 0; i < g.buffers.size(); ++i)
+    if (L.a.rows[i] * L.a.cols[i] > lim32) small = false;
+  for (const auto& b : g.bounds) {
+    if (!b.affine) return false;
+    int64_t lo[2] = {0, 0}, hi[2] = {0, 0};
+    for (int q = 0; q < (b.two ? 2 : 1); ++q) {
+      int64_t mn = b.c0[q], mx = b.c0[q], mag = b.c0[q] < 0 ? -b.c0[q] : b.c0[q];
+      for (const auto& t : b.terms[q]) {
+        const int64_t vlo = rt[t.lo_kind] + t.lo, vhi = rt[t.hi_kind] + t.hi;
+        if (vhi < vlo) continue;  // empty range (e.g. a grid extent of 0): never evaluated
+        mn += t.coef > 0 ? t.coef * vlo : t.coef * vhi;
+        mx += t.coef > 0 ? t.coef * vhi : t.coef * vlo;
+        const int64_t a = std::max(vlo < 0 ? -vlo : vlo, vhi < 0 ? -vhi : vhi);
+        mag += (t.coef < 0 ? -t.coef : t.coef) * a;
+      }
+      if (mag > lim32) small = false;
+      lo[q] = mn;
+      hi[q] = mx;
+    }
+    if (b.buffer >= 0) {
+      const int64_t rows = L.a.rows[b.buffer], cols = L.a.cols[b.buffer];
+      if (b.two) {
+        if (lo[0] < 0 || hi[0] >= rows || lo[1] < 0 || hi[1] >= cols) return false;
+      } else if (lo[0] < 0 || hi[0] >= rows * cols) {
+        return false;
+      }
+    } else if (b.buffer == -1) {
+      if (lo[0] < 0 || hi[0] >= b.words) return false;
+    }
+  }
+  *fits32 = small;
+  return true;
+}
+
 void run_generic(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc, cudaStream_t s,
                  Workspace& ws, Recorder* rec) {
   GenericLaunch L = generic_args(k, bufs, sc, s, ws);
@@ -454,7 +498,12 @@ void run_generic(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc,
       zero.emplace_back(b.ptr, sizeof(float) * (size_t)b.size());
     }
   const GenericOp& g = k.generic;
-  const JitFlags fl = generic_flags(k);
+  JitFlags fl = generic_flags(k);
+  bool fits32 = false;
+  if (options().generic_checked == 0 && prove_bounds(g, L, &fits32)) {
+    fl.unchecked = true;  // cannot fault: drop the per-access checks
+    fl.idx32 = fits32;
+  }
   if (rec) jit_load(g.source, fl);  // compile + load now: nothing heavy inside a capture
   const std::string src = g.source;
   const dim3 grid((unsigned)L.launch_x, (unsigned)L.launch_y), block((unsigned)(g.block_x * g.block_y));

@@ -43,7 +43,8 @@ struct EngineOptions {
   int max_sms = 0;  // > 0: cap the SMs a matrix kernel's grid is sized for
   int tma_consumers = 0;  // TMA matrix variant: 0 auto (by shape), 256 or 512 consumer threads
   int generic_poison = 0;
-  int nvtx = 0;  // 1: an NVTX range around every kernel launch (named after the plan kernel)  // 1: generic kernels poison on-chip memory (VM fault on uninitialised reads)
+  int nvtx = 0;
+  int generic_checked = 0;  // 1: generic kernels keep per-access checks even when proved in bounds  // 1: an NVTX range around every kernel launch (named after the plan kernel)  // 1: generic kernels poison on-chip memory (VM fault on uninitialised reads)
 };
 
 // A row-sharding group's in-kernel exchange buffers (see PeerLinks).

@@ -43,6 +43,8 @@ struct JitFlags {
   bool poison = false;
   bool stats = false;  // the VM's ExecutionStats counters
   bool trace = false;  // the VM's access trace (implies stats)
+  bool unchecked = false;  // every index proved in bounds at launch: no per-access checks
+  bool idx32 = false;      // ... and every index value fits 32 bits: int index arithmetic
 };
 
 // Device fault codes written by generic kernels (first fault wins).

@@ -71,6 +71,24 @@ struct MatrixOp {
   bool chain = false;
 };
 
+// An index expression a generic kernel evaluates, as an affine form over
+// symbols with known ranges -- proved in bounds at launch (then the kernel
+// runs without per-access checks, in 32-bit index arithmetic when safe).
+struct GenericBound {
+  enum Kind : int { Const = 0, FullX = 1, FullY = 2, NElems = 3, LaunchX = 4, LaunchY = 5 };
+  struct Term {
+    int64_t coef = 0;
+    int lo_kind = Const, hi_kind = Const;  // bound = value of kind (0 for Const) + offset
+    int64_t lo = 0, hi = 0;
+  };
+  int buffer = -1;       // >= 0 global buffer; -1 on-chip (words); -2 range only (conditions)
+  int64_t words = 0;     // on-chip: valid words [0, words)
+  bool two = false;      // global 2-D (row, col) index
+  bool affine = true;    // false: not provable (div / mod / min, unbounded loop variable)
+  int64_t c0[2] = {0, 0};
+  std::vector<Term> terms[2];
+};
+
 // Generic kernel: any KernelIR, emitted as CUDA C++ by
 // host/cudagen.cpp following the reference VM's execution semantics
 // (proj/src/vm.cpp:357-445) and JIT-compiled for sm_100a with NVRTC
@@ -86,6 +104,7 @@ struct GenericOp {
   char iter_dim = 'x';
   std::string domain;
   int shared_words_total = 0;
+  std::vector<GenericBound> bounds;  // every index expression (launch-time proof)
 };
 
 struct NativeKernel {

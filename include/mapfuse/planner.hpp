@@ -174,6 +174,10 @@ int generic_iterations();
 // depth-2 generic kernels (2 | 4 | 8 | 16).
 void set_generic_by(int by);
 int generic_by();
+// Engine option "generic_prefetch": loads of the loop body are issued this
+// many iterations ahead (0 = auto: 4, 2 or 1 within 32 registers per thread).
+void set_generic_prefetch(int d);
+int generic_prefetch();
 // Default implementation parameters of a generic kernel whose domain buffer
 // is dom_rows x dom_cols (a vector: 1 x length).
 CodegenParams generic_params(const kernel::KernelIR& k, int64_t dom_rows, int64_t dom_cols);

@@ -238,8 +238,12 @@ int mf_generate(float* dev, int64_t rows, int64_t cols, int64_t ld, uint64_t see
  * where a hand-written family applies), "generic_poison" (0|1: generic
  * kernels poison on-chip memory and fault on uninitialised reads),
  * "generic_iterations" (0 = per size, else the serial iterations of generic
- * kernels), "vm_exact" (0|1: vm::launch always counts like the VM),
- * "codegen_barriers" (test hook, 0 = codegen omits barriers). */
+ * kernels), "generic_by" (0 = default, else block rows of depth-2 generic
+ * kernels), "generic_prefetch" (0 = auto, else how many iterations ahead
+ * generic kernels issue their loads), "generic_checked" (0|1: keep per-access
+ * index checks even when the bounds are proved at launch), "vm_exact" (0|1:
+ * vm::launch always counts like the VM), "nvtx" (0|1: NVTX ranges per
+ * kernel), "codegen_barriers" (test hook, 0 = codegen omits barriers). */
 int mf_set_option(const char* key, int value);
 int mf_get_option(const char* key);
 

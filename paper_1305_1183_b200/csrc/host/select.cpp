@@ -32,8 +32,9 @@ CostModel CostModel::defaults() {
       {"matrix.tma.rank", 0.97},   // GEMVER ger2+sgemtv, TMA ring, 16 consumer warps
       {"matrix.rowres", 0.88},     // row-resident chain (ATAX one pass, 16384^2)
       {"matrix.rowres.cluster", 0.75},  // ... rows over a CTA cluster (n > 16384): 32768^2 0.86, 131072 cols 0.71
-      {"generic.d1", 0.60},        // NVRTC-emitted KernelIR (host/cudagen.cpp), depth 1:
-                                   //   VADD 0.76, AXPYDOT 0.44 (profiles/r01_generic_sweep_pf.txt)
+      {"generic.d1", 0.70},        // NVRTC-emitted KernelIR (host/cudagen.cpp), depth 1,
+                                   //   prefetch 4 ahead: VADD 0.93, AXPYDOT 0.53
+                                   //   (profiles/r01_generic_sweep_pf.txt)
       {"generic.d2", 0.60},        // ... depth 2 (BY 4, pipelined, proved bounds, 32-bit indices):
                                    //   BiCGK 0.54, ATAX 0.70, GEMVER 0.74, GESUMMV 0.68
                                    //   (profiles/r01_generic_sweep_pf.txt)
@@ -112,7 +113,9 @@ CodegenParams generic_params(const kernel::KernelIR& k, int64_t dom_rows, int64_
     limit = elems / inst;
   }
   const int forced = generic_iterations();
-  int64_t want = forced >= 1 ? forced : (k.depth == 1 ? 16 : (accumulates ? 4 : 1));
+  // depth 1: 32 iterations when the kernel reduces (half the blocks, half the
+  // global atomics: AXPYDOT 0.47 -> 0.53 of HBM), else 16 (VADD 0.95)
+  int64_t want = forced >= 1 ? forced : (k.depth == 1 ? (accumulates ? 32 : 16) : (accumulates ? 4 : 1));
   // keep >= 4 blocks per SM (148 SMs)
   while (want > 1 && (limit / want) * blocks_per_band < 148 * 4 && forced < 1) want /= 2;
   int64_t it = std::max<int64_t>(1, std::min(want, limit));

@@ -377,6 +377,8 @@ int mf_plan_prepare(const mf_plan* plan) {
         JitFlags fl;
         fl.poison = kern.generic_poison >= 0 ? kern.generic_poison != 0 : options().generic_poison != 0;
         jit_prepare(kern.generic.source, fl);
+        fl.unchecked = fl.idx32 = true;  // the variant launches use when the bounds are proved
+        jit_prepare(kern.generic.source, fl);
       }
   });
 }
@@ -789,6 +791,9 @@ int mf_set_option(const char* key, int value) {
       if (value != 0 && value != 2 && value != 4 && value != 8 && value != 16)
         throw Invalid("generic_by: 0 (default) | 2 | 4 | 8 | 16");
       mapfuse::plan::set_generic_by(value);
+    } else if (k == "generic_prefetch") {
+      if (value < 0 || value > 8) throw Invalid("generic_prefetch: 0 (auto) .. 8");
+      mapfuse::plan::set_generic_prefetch(value);
     } else if (k == "generic_iterations") {
       if (value < 0 || value > 4096) throw Invalid("generic_iterations: 0 (auto) .. 4096");
       mapfuse::plan::set_generic_iterations(value);
@@ -814,6 +819,7 @@ int mf_get_option(const char* key) {
   if (k == "generic_poison") return options().generic_poison;
   if (k == "generic_iterations") return mapfuse::plan::generic_iterations();
   if (k == "generic_by") return mapfuse::plan::generic_by();
+  if (k == "generic_prefetch") return mapfuse::plan::generic_prefetch();
   if (k == "codegen_barriers") return mapfuse::plan::codegen_barriers() ? 1 : 0;
   if (k == "vm_exact") return mapfuse::vm::exact() ? 1 : 0;
   if (k == "nvtx") return options().nvtx;

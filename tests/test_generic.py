@@ -50,6 +50,26 @@ def test_every_sequence_emits_and_compiles(generic, seq, mode):
     plan.prepare()  # NVRTC -> sm_100a cubin for every kernel; raises on a compile error
 
 
+@pytest.mark.parametrize("d", [0, 1, 2, 4])
+def test_prefetch_distance_emits_and_compiles(generic, d):
+    """Loads issued d iterations ahead: one register slot per distance, the
+    loop unrolled by the distance (auto: 4 for depth 1, 1 for depth 2)."""
+    mf = generic
+    mf.set_option("generic_prefetch", d)
+    mf.set_option("generic_iterations", 8)
+    try:
+        for seq, m, n, auto in [("AXPYDOT", 1, 1 << 20, 4), ("BICGK", 1024, 1024, 1)]:
+            plan = mf.Plan.sequence(seq, m, n, "fused")
+            src = plan.kernel_source(0)
+            want = d if d else auto
+            assert "float mfj_pf0[%d][" % want in src, (seq, d)
+            assert ("it0 += %d" % want in src) == (want > 1)
+            plan.prepare()
+    finally:
+        mf.set_option("generic_prefetch", 0)
+        mf.set_option("generic_iterations", 0)
+
+
 def test_hand_written_kernels_have_no_source(mf):
     plan = mf.Plan.sequence("BICGK", 128, 128, "fused")
     assert plan.describe()["kernels"][0]["kind"] == "matrix"

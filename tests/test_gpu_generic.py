@@ -90,6 +90,29 @@ def test_generic_larger_vs_oracle(generic, seq, m, n):
         check_output(seq, name, got[name], want[name], S[name], exact=False)
 
 
+@pytest.mark.parametrize("d", [1, 2, 4])
+@pytest.mark.parametrize("seq,m,n", [("AXPYDOT", 1, 1 << 20), ("VADD", 1, 1 << 20),
+                                     ("BICGK", 1024, 1024), ("GEMVER", 512, 512)])
+def test_prefetch_distance_vs_oracle(generic, seq, m, n, d):
+    """Loads issued 1, 2 or 4 iterations ahead give the same results."""
+    torch, mf, ref, co = generic
+    from test_gpu_parity import out_shapes, rand_inputs, run_plan
+    mf.set_option("generic_prefetch", d)
+    mf.set_option("generic_iterations", 8)
+    try:
+        vals = rand_inputs(seq, m, n, 5)
+        plan = mf.Plan.sequence(seq, m, n, "fused")
+        assert "float mfj_pf0[%d][" % d in plan.kernel_source(0)
+        got = run_plan(torch, plan, vals, out_shapes(plan))
+    finally:
+        mf.set_option("generic_prefetch", 0)
+        mf.set_option("generic_iterations", 0)
+    want = co.execute(seq, m, n, vals)
+    S = scale_bound(co, seq, m, n, vals)
+    for name in want:
+        check_output(seq, name, got[name], want[name], S[name], exact=False)
+
+
 @pytest.mark.parametrize("script", sorted(USER_SCRIPTS))
 @pytest.mark.parametrize("mode", ["fused", "unfused"])
 def test_user_functions_vs_reference_vm(env, script, mode):

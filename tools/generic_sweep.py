@@ -19,7 +19,7 @@ CASES = [("AXPYDOT", 1, 1 << 24), ("VADD", 1, 1 << 26), ("BICGK", 16384, 16384),
          ("ATAX", 8192, 8192), ("GEMVER", 8192, 8192), ("GESUMMV", 8192, 8192), ("MADD", 8192, 8192)]
 
 
-def run(seq, m, n, reps=5):
+def run(seq, m, n, reps=15):
     p = mf.Plan.sequence(seq, m, n, "fused")
     d = p.describe()
     bufs = {}
@@ -33,16 +33,16 @@ def run(seq, m, n, reps=5):
     p.launch(bufs, sc)
     p.check()
     flush = torch.empty(256 << 20, device="cuda")
-    tot = 0.0
+    times = []
     for _ in range(reps):
-        flush.zero_()
+        flush.zero_()  # also keeps the device busy while the launch is issued
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
         p.launch(bufs, sc)
         e.record()
         torch.cuda.synchronize()
-        tot += s.elapsed_time(e)
-    ms = tot / reps
+        times.append(s.elapsed_time(e))
+    ms = sorted(times)[len(times) // 2]  # median
     byts = d["bytes_loaded"] + d["bytes_stored"]
     its = [l.split()[1] for l in "\n".join(p.kernel_text(k) for k in range(p.num_kernels)).splitlines()
            if l.strip().startswith("iterations")]

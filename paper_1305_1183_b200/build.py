@@ -50,10 +50,16 @@ def _compile(cmd):
     return r.stderr
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
+def build(verbose: bool = False, force: bool = False, defines=(), lib: str = LIB,
+          obj: str = OBJ) -> str:
+    """defines/lib/obj: diagnostic variants (e.g. -DMF_TIMELINE) build into
+    their own object directory and library path."""
     cu, cpp = sources()
+    OBJ = obj
+    LIB = lib
+    defs = ["-D" + d for d in defines]
     stamp = os.path.join(OBJ, "stamp")
-    dig = _digest(cu + cpp + [__file__])
+    dig = _digest(cu + cpp + [__file__]) + " ".join(defs)
     if not force and os.path.exists(LIB) and os.path.exists(stamp):
         with open(stamp) as f:
             if f.read().strip() == dig:
@@ -65,11 +71,11 @@ def build(verbose: bool = False, force: bool = False) -> str:
         o = os.path.join(OBJ, os.path.basename(src) + ".o")
         objs.append(o)
         jobs.append([NVCC] + ARCH + ["-O3", "-std=c++20", "-lineinfo", "-Xcompiler", "-fPIC",
-                                     "-Xptxas", "-v"] + INC + ["-c", src, "-o", o])
+                                     "-Xptxas", "-v"] + defs + INC + ["-c", src, "-o", o])
     for src in cpp:
         o = os.path.join(OBJ, os.path.basename(src) + ".o")
         objs.append(o)
-        jobs.append(["g++", "-O2", "-std=c++20", "-fPIC", "-Wall", "-Wno-unused-function"] + INC +
+        jobs.append(["g++", "-O2", "-std=c++20", "-fPIC", "-Wall", "-Wno-unused-function"] + defs + INC +
                     ["-c", src, "-o", o])
     with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
         logs = list(ex.map(_compile, jobs))

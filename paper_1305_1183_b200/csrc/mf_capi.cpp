@@ -764,7 +764,7 @@ int mf_set_option(const char* key, int value) {
       if (value != 0 && value != 2 && value != 4 && value != 8) throw Invalid("stream_unroll: 0|2|4|8");
       options().stream_unroll = value;
     } else if (k == "stream_ctas_per_sm") {
-      if (value < 1 || value > 8) throw Invalid("stream_ctas_per_sm: 1..8");
+      if (value < 0 || value > 8) throw Invalid("stream_ctas_per_sm: 0 (one CTA per block) | 1..8");
       options().stream_ctas_per_sm = value;
     } else if (k == "tma_consumers") {
       if (value != 0 && value != 256 && value != 512) throw Invalid("tma_consumers: 0|256|512");

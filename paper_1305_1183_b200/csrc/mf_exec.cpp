@@ -181,7 +181,8 @@ void run_stream(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc, 
     for (int i = 0; i < nin; ++i) a.coef[q][i] = coef(op.outs[q].coef[i], sc, k.name);
   }
   const int sms = device_sm_count();
-  const int grid = stream_grid(a.n4, sms, options().stream_ctas_per_sm);
+  const int grid = stream_grid(a.n4, sms, options().stream_ctas_per_sm, nin, options().stream_unroll,
+                               op.has_dot);
   if (op.has_dot) {
     const DevBuf& r = need(bufs, op.dot_out, k.name);
     if (r.size() < 1) throw Fault("kernel " + k.name + ": empty dot output");

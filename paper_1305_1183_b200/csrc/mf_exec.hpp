@@ -37,8 +37,8 @@ struct EngineOptions {
   int matrix_k = 2;
   int f64acc = 0;
   int occupancy = 2;
-  int stream_unroll = 0;       // 0 = default (by input count), else 2 / 4 / 8
-  int stream_ctas_per_sm = 4;
+  int stream_unroll = 0;       // 0 = default (2), else 2 / 4 / 8 float4 per thread per stream
+  int stream_ctas_per_sm = 0;  // 0 = one CTA per block (non-persistent), else capped grid
   int tma = -1;  // matrix kernels: -1 auto (by shape), 1 = TMA ring, 0 = register-fed
   int max_sms = 0;  // > 0: cap the SMs a matrix kernel's grid is sized for
   int tma_consumers = 0;  // TMA matrix variant: 0 auto (by shape), 256 or 512 consumer threads

@@ -71,24 +71,62 @@ struct StreamBody {
 
 template <int NIN, int NOUT, bool DOT, int U>
 __global__ void __launch_bounds__(kThreads) stream_kernel(StreamArgs a) {
-  // U float4 loads in flight per input per thread
-  const long long stride = (long long)gridDim.x * kThreads;
-  long long i = (long long)blockIdx.x * kThreads + threadIdx.x;
+  // Block-contiguous layout: block b = float4 [b*256*U, (b+1)*256*U) of every
+  // stream; thread t loads b*256*U + u*256 + t, so a warp's U loads per input
+  // are U contiguous 512 B runs and the CTA's footprint one contiguous
+  // 4*U KB run per stream.  Default launch: one CTA per block (non-persistent,
+  // the block scheduler issues blocks in address order, so the whole GPU
+  // sweeps a compact, ordered wavefront); a capped grid strides over blocks.
+  // Measured on B200 (tools/copy_probe.cu, y = f(x1..xk), 1 GiB per stream):
+  // 1/2/3 inputs reach 6.9/7.0/7.2 TB/s this way against 6.0/6.3-6.7/6.7-7.0
+  // for a persistent grid-stride sweep; plain ld.global.nc beats an
+  // evict-first L2 policy by 2-5%.
+  // With a dot, every CTA ends in a block reduction and a ticket on one
+  // counter, so dot kernels keep a persistent grid (4 CTAs/SM) sweeping
+  // grid-strided float4 slots with evict-first loads: AXPYDOT 2^24 runs
+  // 41 us this way against 45-47 us block-contiguous (tools/sweep.py).
   double acc = 0.0;
-  for (; i + (U - 1) * stride < a.n4; i += U * stride) {
-    float4 v[U][NIN];
+  if constexpr (DOT) {
+    const long long stride = (long long)gridDim.x * kThreads;
+    long long i = (long long)blockIdx.x * kThreads + threadIdx.x;
+    for (; i + (U - 1) * stride < a.n4; i += U * stride) {
+      float4 v[U][NIN];
 #pragma unroll
-    for (int u = 0; u < U; ++u)
+      for (int u = 0; u < U; ++u)
 #pragma unroll
-      for (int k = 0; k < NIN; ++k) v[u][k] = ld_stream(a.in[k] + i + u * stride);
+        for (int k = 0; k < NIN; ++k) v[u][k] = ld_stream(a.in[k] + i + u * stride);
 #pragma unroll
-    for (int u = 0; u < U; ++u) StreamBody<NIN, NOUT, DOT>::apply(a, v[u], i + u * stride, acc);
-  }
-  for (; i < a.n4; i += stride) {
-    float4 v[NIN];
+      for (int u = 0; u < U; ++u) StreamBody<NIN, NOUT, DOT>::apply(a, v[u], i + u * stride, acc);
+    }
+    for (; i < a.n4; i += stride) {
+      float4 v[NIN];
 #pragma unroll
-    for (int k = 0; k < NIN; ++k) v[k] = ld_stream(a.in[k] + i);
-    StreamBody<NIN, NOUT, DOT>::apply(a, v, i, acc);
+      for (int k = 0; k < NIN; ++k) v[k] = ld_stream(a.in[k] + i);
+      StreamBody<NIN, NOUT, DOT>::apply(a, v, i, acc);
+    }
+  } else {
+    constexpr long long BLK = (long long)U * kThreads;
+    const long long nblk = (a.n4 + BLK - 1) / BLK;
+    for (long long b = blockIdx.x; b < nblk; b += gridDim.x) {
+      const long long base = b * BLK + threadIdx.x;
+      if (base + (U - 1) * kThreads < a.n4) {
+        float4 v[U][NIN];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int k = 0; k < NIN; ++k) v[u][k] = __ldg(a.in[k] + base + u * kThreads);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          StreamBody<NIN, NOUT, DOT>::apply(a, v[u], base + u * kThreads, acc);
+      } else {
+        for (long long i = base; i < a.n4; i += kThreads) {
+          float4 v[NIN];
+#pragma unroll
+          for (int k = 0; k < NIN; ++k) v[k] = __ldg(a.in[k] + i);
+          StreamBody<NIN, NOUT, DOT>::apply(a, v, i, acc);
+        }
+      }
+    }
   }
   if constexpr (DOT) {
     __shared__ double wsum[kWarps];
@@ -101,13 +139,14 @@ __global__ void __launch_bounds__(kThreads) stream_kernel(StreamArgs a) {
       double s = 0.0;
       for (int w = 0; w < kWarps; ++w) s += wsum[w];
       a.part[blockIdx.x] = s;
-      __threadfence();
-      last = (atomicAdd(a.ticket, 1u) == gridDim.x - 1);
+      unsigned prev;  // acq_rel RMW chain: publishes this partial, acquires all earlier ones
+      asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(prev) : "l"(a.ticket) : "memory");
+      last = (prev == gridDim.x - 1);
     }
     __syncthreads();
     if (last) {  // deterministic: fixed assignment of partials + fixed tree
-      __threadfence();
       double s = 0.0;
+#pragma unroll 8
       for (int b = threadIdx.x; b < (int)gridDim.x; b += kThreads) s += __ldcg(a.part + b);
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
@@ -147,8 +186,33 @@ __global__ void __launch_bounds__(kThreads) stream_kernel(StreamArgs a) {
 // Rows stream through in batches of R: all R*K (x NMAT) 128-bit loads of a
 // batch are issued before any arithmetic.
 
+#ifdef MF_TIMELINE
+// Diagnostic build only (tools/matrix_timeline.py): per-CTA %globaltimer
+// stamps at kernel entry, end of the streaming loop, after the grid barrier
+// and at exit; slot 4 holds the CTA's %smid.
+__device__ unsigned long long g_mf_timeline[5][4096];
+#define MF_STAMP(slot)                                                              \
+  do {                                                                              \
+    if (threadIdx.x == 0 && blockIdx.x < 4096) {                                    \
+      unsigned long long t_;                                                        \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                        \
+      g_mf_timeline[slot][blockIdx.x] = t_;                                         \
+      if (slot == 0) {                                                              \
+        unsigned sm_;                                                               \
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm_));                            \
+        g_mf_timeline[4][blockIdx.x] = sm_;                                         \
+      }                                                                             \
+    }                                                                               \
+  } while (0)
+#else
+#define MF_STAMP(slot) \
+  do {                 \
+  } while (0)
+#endif
+
 template <int NMAT, int NRANK, bool STORE, int NROW, int NCOL, int K, int R, typename ACC>
 __global__ void __launch_bounds__(kThreads, 2) matrix_kernel(MatrixArgs a) {
+  MF_STAMP(0);
   constexpr int NV = (NROW > 0 ? NROW : 1) * R;
   constexpr long long C = 4LL * kThreads * K;
   __shared__ ACC red[2][kWarps][NV];
@@ -286,9 +350,12 @@ __global__ void __launch_bounds__(kThreads, 2) matrix_kernel(MatrixArgs a) {
 
   if constexpr (NCOL > 0 || NROW > 0) {
     const bool need_rows = (NROW > 0) && a.CB > 1;
+    MF_STAMP(1);
     if (NCOL == 0 && !need_rows) return;
     grid_barrier(a.bar);
+    MF_STAMP(2);
     finalize_any<NROW, NCOL, ACC>(a, tid, kThreads);
+    MF_STAMP(3);
   }
 }
 
@@ -348,8 +415,7 @@ MatrixFn matrix_fn(const MatrixShape& s, const MatrixTuning& t) {
 
 template <int NIN, int NOUT, bool DOT>
 cudaError_t go_stream(const StreamArgs& a, int grid, int unroll, cudaStream_t s) {
-  // default: ~8 float4 loads in flight per thread
-  if (unroll <= 0) unroll = NIN <= 2 ? 8 : 2;  // measured best on B200 (tools/sweep.py)
+  unroll = stream_unroll_for(NIN, DOT, unroll);
   if (unroll >= 8) stream_kernel<NIN, NOUT, DOT, 8><<<grid, kThreads, 0, s>>>(a);
   else if (unroll >= 4) stream_kernel<NIN, NOUT, DOT, 4><<<grid, kThreads, 0, s>>>(a);
   else stream_kernel<NIN, NOUT, DOT, 2><<<grid, kThreads, 0, s>>>(a);
@@ -359,10 +425,23 @@ cudaError_t go_stream(const StreamArgs& a, int grid, int unroll, cudaStream_t s)
 }  // namespace
 
 // ---------------------------------------------------------------------------
-int stream_grid(long long n4, int sms, int ctas_per_sm) {
-  long long want = (long long)sms * (ctas_per_sm > 0 ? ctas_per_sm : 4);
-  long long need = (n4 + kThreads - 1) / kThreads;
-  return (int)std::max(1LL, std::min(want, need));
+int stream_unroll_for(int nin, bool dot, int unroll) {
+  if (unroll > 0) return unroll;
+  // block-contiguous maps: 2 float4 per thread per stream (tools/copy_probe.cu
+  // B2 vs B4); grid-strided dot kernels: ~8 loads in flight per thread
+  if (!dot) return 2;
+  return nin <= 2 ? 8 : 2;
+}
+
+int stream_grid(long long n4, int sms, int ctas_per_sm, int nin, int unroll, bool dot) {
+  if (dot) {
+    const long long want = (long long)sms * (ctas_per_sm > 0 ? ctas_per_sm : 4);
+    return (int)std::max(1LL, std::min(want, (n4 + kThreads - 1) / kThreads));
+  }
+  const long long blk = (long long)kThreads * stream_unroll_for(nin, dot, unroll);
+  const long long nblk = std::max(1LL, (n4 + blk - 1) / blk);
+  if (ctas_per_sm <= 0) return (int)std::min<long long>(nblk, 0x7fffffffLL);  // one CTA per block
+  return (int)std::max(1LL, std::min(nblk, (long long)sms * ctas_per_sm));
 }
 
 cudaError_t launch_stream(int nin, int nout, bool dot, const StreamArgs& a, int grid, int unroll,
@@ -446,6 +525,17 @@ cudaError_t launch_matrix(const MatrixShape& sh, const MatrixTuning& t, const Ma
   fn<<<grid, kThreads, 0, s>>>(copy);
   return cudaGetLastError();
 }
+
+#ifdef MF_TIMELINE
+extern "C" int mf_debug_timeline(unsigned long long* host) {  // host: 5 x 4096; read + clear
+  cudaError_t e = cudaMemcpyFromSymbol(host, g_mf_timeline, sizeof(g_mf_timeline));
+  void* p = nullptr;
+  if (e == cudaSuccess) e = cudaGetSymbolAddress(&p, g_mf_timeline);
+  if (e == cudaSuccess) e = cudaMemset(p, 0, sizeof(g_mf_timeline));
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  return (int)e;
+}
+#endif
 
 cudaError_t launch_generate(float* out, long long rows, long long cols, long long ld,
                             unsigned long long seed, long long row0, long long ncols_global,

@@ -82,7 +82,11 @@ struct MatrixTuning {
 // Launchers; return cudaSuccess or the launch error.  `sms` = SM count.
 cudaError_t launch_stream(int nin, int nout, bool dot, const StreamArgs& a, int grid, int unroll,
                           cudaStream_t s);
-int stream_grid(long long n4, int sms, int ctas_per_sm);
+// Stream grid.  Maps: ctas_per_sm = 0 (default) launches one CTA per block
+// of 256*U float4, > 0 caps the grid at sms * ctas_per_sm (CTAs stride over
+// blocks).  Dot kernels: persistent, sms * (ctas_per_sm or 4) CTAs.
+int stream_grid(long long n4, int sms, int ctas_per_sm, int nin, int unroll, bool dot);
+int stream_unroll_for(int nin, bool dot, int unroll);
 
 // Fills CB/RB/tiles and returns the grid size (co-resident for the barrier).
 cudaError_t matrix_config(const MatrixShape& sh, const MatrixTuning& t, long long m, long long n,

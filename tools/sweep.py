@@ -65,11 +65,11 @@ def run(seq, m, n, settings, mode="fused"):
 
 which = sys.argv[1] if len(sys.argv) > 1 else "all"
 if which in ("stream", "all"):
-    st = [{"stream_unroll": u, "stream_ctas_per_sm": c} for u in (0, 2, 4, 8) for c in (2, 4, 8)]
+    st = [{"stream_unroll": u, "stream_ctas_per_sm": c} for u in (0, 4, 8) for c in (0, 2, 4)]
     for seq, n in (("VADD", 1 << 28), ("WAXPBY", 1 << 28), ("AXPYDOT", 1 << 24)):
         run(seq, 1, n, st)
     mf.set_option("stream_unroll", 0)
-    mf.set_option("stream_ctas_per_sm", 4)
+    mf.set_option("stream_ctas_per_sm", 0)
 if which in ("matrix", "all"):
     st = [{"tma": -1, "matrix_k": 2, "tma_consumers": 0}, {"tma": 0, "matrix_k": 2},
           {"tma": 0, "matrix_k": 4}, {"tma": 1, "matrix_k": 2}, {"tma": 1, "matrix_k": 4},

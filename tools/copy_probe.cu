@@ -128,6 +128,61 @@ __global__ void __launch_bounds__(256) blocked(Ptrs p, long long n4) {
     if (base + u * 256 < n4) st<SH>(p.y + base + u * 256, combine<NIN>(v[u]));
 }
 
+// D: bulk-engine copy, persistent, one CTA (one elected thread) per SM: CTA b
+// moves blocks b, b+G, ... of BLK bytes global -> shared (cp.async.bulk,
+// mbarrier complete_tx) -> global (cp.async.bulk bulk_group), S-stage ring.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+template <int S>
+__global__ void __launch_bounds__(32) dma_copy(const char* x, char* y, long long nbytes, int BLK) {
+  extern __shared__ __align__(128) unsigned char sm[];
+  __shared__ __align__(8) unsigned long long full[S];
+  if (threadIdx.x != 0) return;
+  for (int s = 0; s < S; ++s)
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[s])));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  const long long nblk = nbytes / BLK;
+  unsigned phase[S] = {};
+  int k = 0;
+  // prologue: S loads in flight
+  long long b = blockIdx.x;
+  long long inflight[S];
+  for (int s = 0; s < S; ++s) inflight[s] = -1;
+  for (int s = 0; s < S && b < nblk; ++s, b += gridDim.x) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&full[s])), "r"(BLK) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(sm + (size_t)s * BLK)), "l"(x + b * BLK), "r"(BLK), "r"(smem_u32(&full[s])) : "memory");
+    inflight[s] = b;
+  }
+  for (;; ++k) {
+    const int s = k % S;
+    if (inflight[s] < 0) break;
+    // wait for the load of stage s, store it out
+    asm volatile("{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra W_%=;\n}\n"
+                 ::"r"(smem_u32(&full[s])), "r"(phase[s]) : "memory");
+    phase[s] ^= 1u;
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(y + inflight[s] * BLK),
+                 "r"(smem_u32(sm + (size_t)s * BLK)), "r"(BLK) : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    if (k > 0) {
+      // refill the previous stage once its store (one group older) has read it
+      const int q = (k - 1) % S;
+      if (b < nblk) {
+        asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&full[q])), "r"(BLK) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     ::"r"(smem_u32(sm + (size_t)q * BLK)), "l"(x + b * BLK), "r"(BLK), "r"(smem_u32(&full[q])) : "memory");
+        inflight[q] = b;
+        b += gridDim.x;
+      } else {
+        inflight[q] = -1;
+      }
+    }
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 static double bytes_per_elem = 8.0;
 
 int main(int argc, char** argv) {
@@ -191,6 +246,27 @@ int main(int argc, char** argv) {
     run(nm, [&] { blocked<NIN, U, LH, SH><<<(unsigned)nb, 256>>>(P, n4); });                   \
   }
 #define HINTS(NIN, U) VARS(NIN, U, false, false) VARS(NIN, U, true, false) VARS(NIN, U, false, true) VARS(NIN, U, true, true)
+  if (getenv("PROBE_DMA")) {
+    bytes_per_elem = 8.0;
+    for (int blk : {8192, 16384, 32768}) {
+      for (int per_sm : {1, 2}) {
+        const int S = 8;
+        const size_t smem = (size_t)S * blk;
+        if (smem * per_sm > 200 * 1024) continue;
+        CK(cudaFuncSetAttribute(dma_copy<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        snprintf(nm, sizeof nm, "DMA blk=%d S=8 ctas=%d", blk, per_sm);
+        run(nm, [&] { dma_copy<8><<<sms * per_sm, 32, smem>>>((const char*)x, (char*)y, n * 4, blk); });
+      }
+    }
+    for (int blk : {4096, 8192}) {
+      const int S = 8;
+      const size_t smem = (size_t)S * blk;
+      CK(cudaFuncSetAttribute(dma_copy<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      snprintf(nm, sizeof nm, "DMA blk=%d S=8 ctas=3", blk);
+      run(nm, [&] { dma_copy<8><<<sms * 3, 32, smem>>>((const char*)x, (char*)y, n * 4, blk); });
+    }
+    return 0;
+  }
   if (nin_max >= 1) { HINTS(1, 2) HINTS(1, 4) }
   if (nin_max >= 2) { HINTS(2, 2) HINTS(2, 4) }
   if (nin_max >= 3) { HINTS(3, 2) HINTS(3, 4) }

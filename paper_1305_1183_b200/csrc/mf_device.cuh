@@ -43,21 +43,27 @@ __device__ __forceinline__ void set_comp(float4& v, int c, float x) {
 // ---------------------------------------------------------------------------
 // Grid barrier for co-resident (cooperatively launched) grids.  bar[0] counts
 // arrivals, bar[1] is a generation number; self-resetting across launches.
+// One acq_rel RMW per CTA (publishes the CTA's writes -- ordered before it by
+// bar.sync -- and, for the last arriver, acquires everyone's), one release
+// increment of the generation, acquire polling: two L2 round trips on the
+// critical path instead of the four a fence-based barrier takes.
 __device__ __forceinline__ void grid_barrier(unsigned* bar) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    volatile unsigned* gen = bar + 1;
-    unsigned g = *gen;
-    __threadfence();
-    unsigned arrived = atomicAdd(bar, 1u);
+    unsigned g, arrived;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(bar + 1) : "memory");
+    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(arrived) : "l"(bar) : "memory");
     if (arrived == gridDim.x - 1) {
-      atomicExch(bar, 0u);
-      __threadfence();
-      atomicAdd(bar + 1, 1u);
+      asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(bar) : "memory");
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar + 1) : "memory");
     } else {
-      while (*gen == g) __nanosleep(64);
+      unsigned cur;
+      for (;;) {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(bar + 1) : "memory");
+        if (cur != g) break;
+        __nanosleep(32);
+      }
     }
-    __threadfence();
   }
   __syncthreads();
 }
@@ -110,6 +116,7 @@ __device__ __forceinline__ void group_sum4(const ACC* base, long long stride, in
                                            int glane, ACC (&t)[4]) {
   t[0] = t[1] = t[2] = t[3] = ACC(0);
   if (valid)
+#pragma unroll 4
     for (int b = glane; b < count; b += kFinGroup) {
       const ACC* q = base + (long long)b * stride;
 #pragma unroll

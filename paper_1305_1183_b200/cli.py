@@ -275,7 +275,7 @@ def cmd_bench_db(args):
     p = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")
     if os.path.exists(p):
         peak = float(json.load(open(p))["hbm_gbs"])
-    cases = {"stream": ("VADD", 1, 1 << 26), "matrix.ldg.read": ("BICGK", 8192, 16384),
+    cases = {"stream": ("VADD", 1, 1 << 26), "stream.dot": ("AXPYDOT", 1, 1 << 24), "matrix.ldg.read": ("BICGK", 8192, 16384),
              "matrix.tma.read": ("BICGK", 8192, 16384), "matrix.ldg.rank": ("GEMVER", 8192, 16384),
              "matrix.tma.rank": ("GEMVER", 8192, 16384)}
     lines = []

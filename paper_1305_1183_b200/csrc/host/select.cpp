@@ -25,7 +25,9 @@ CostModel CostModel::defaults() {
   cm.dev = vm::b200_device();
   // measured on B200 (round 1): fraction of the 6545.6 GB/s copy bandwidth
   cm.eta = {
-      {"stream", 0.98},            // VADD 0.99, WAXPBY 0.96, AXPYDOT 1.00
+      {"stream", 1.09},            // maps, one CTA per 8 KB block: VADD 1.12, WAXPBY 1.09,
+                                   //   SSCAL 1.07, MADD 1.09 (profiles/r01_stream_layout.txt)
+      {"stream.dot", 1.00},        // map + dot, persistent grid + ticket: AXPYDOT 1.00
       {"matrix.ldg.read", 1.04},   // BiCGK 1.03, ATAX 1.05, GESUMMV 1.12
       {"matrix.tma.read", 0.95},   // BiCGK 0.92-0.97
       {"matrix.ldg.rank", 0.62},   // GEMVER ger2+sgemtv, register-fed
@@ -55,7 +57,7 @@ double CostModel::predict_us(b200::NativeKernel& k, int64_t m, int64_t n) const 
     auto it = eta.find(key);
     return bytes / ((it == eta.end() ? 0.9 : it->second) * bw) + dev.launch_us;
   };
-  if (k.kind == b200::NativeKernel::Kind::Stream) return t("stream");
+  if (k.kind == b200::NativeKernel::Kind::Stream) return t(k.stream.has_dot ? "stream.dot" : "stream");
   if (k.kind == b200::NativeKernel::Kind::Generic)
     return t(k.generic.depth == 1 ? "generic.d1" : "generic.d2");
   if (k.matrix.chain) return t(n > 16384 ? "matrix.rowres.cluster" : "matrix.rowres");

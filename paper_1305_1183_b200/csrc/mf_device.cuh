@@ -16,6 +16,23 @@ __device__ __forceinline__ unsigned long long evict_first_policy() {
   return p;
 }
 
+// Matrix-operand L2 policy: evict-first (default) or evict-normal, chosen per
+// launch (MatrixArgs::l2_normal; option "matrix_l2_normal").
+__device__ __forceinline__ unsigned long long matrix_policy(int normal) {
+  unsigned long long p;
+  if (normal) asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  else asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+__device__ __forceinline__ float4 ld_policy(const float4* p, unsigned long long pol) {
+  float4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p), "l"(pol));
+  return v;
+}
+
 __device__ __forceinline__ float4 ld_stream(const float4* p) {
   float4 v;
   asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"

@@ -28,6 +28,7 @@ EngineOptions& options() {
     if (const char* v = std::getenv("MF_TMA")) e.tma = std::atoi(v);
     if (const char* v = std::getenv("MF_STREAM_UNROLL")) e.stream_unroll = std::atoi(v);
     if (const char* v = std::getenv("MF_STREAM_CTAS")) e.stream_ctas_per_sm = std::atoi(v);
+    if (const char* v = std::getenv("MF_MATRIX_L2_NORMAL")) e.matrix_l2_normal = std::atoi(v);
     if (const char* v = std::getenv("MF_MAX_SMS")) e.max_sms = std::atoi(v);
     if (const char* v = std::getenv("MF_TMA_CONSUMERS")) e.tma_consumers = std::atoi(v);
     if (const char* v = std::getenv("MF_GENERIC_POISON")) e.generic_poison = std::atoi(v);
@@ -368,6 +369,7 @@ void run_matrix(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc, 
   if (t.tma && !tma_supported(sh, t)) t.tma = false;
   int grid = 0;
   const int sms = eo.max_sms > 0 ? std::min(eo.max_sms, device_sm_count()) : device_sm_count();
+  a.l2_normal = eo.matrix_l2_normal < 0 ? (sh.store ? 1 : 0) : eo.matrix_l2_normal;
   if (t.tma)
     check_cuda(matrix_tma_config(sh, t, m, n, sms, &a, &grid), ("configure " + k.name).c_str());
   else

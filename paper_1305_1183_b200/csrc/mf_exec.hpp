@@ -42,6 +42,11 @@ struct EngineOptions {
   int tma = -1;  // matrix kernels: -1 auto (by shape), 1 = TMA ring, 0 = register-fed
   int max_sms = 0;  // > 0: cap the SMs a matrix kernel's grid is sized for
   int tma_consumers = 0;  // TMA matrix variant: 0 auto (by shape), 256 or 512 consumer threads
+  // matrix operand loads: 0 evict-first L2 policy, 1 evict-normal, -1 auto =
+  // evict-normal when the kernel also stores a matrix (GEMVER stage 1: 2036 ->
+  // 1996 us, fewer dirty lines of B left for the next kernel to write back),
+  // evict-first for read-only kernels (BiCGK 159.7 -> 157.7 us)
+  int matrix_l2_normal = -1;
   int generic_poison = 0;
   int nvtx = 0;
   int generic_checked = 0;  // 1: generic kernels keep per-access checks even when proved in bounds  // 1: an NVTX range around every kernel launch (named after the plan kernel)  // 1: generic kernels poison on-chip memory (VM fault on uninitialised reads)

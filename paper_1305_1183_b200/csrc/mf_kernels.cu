@@ -220,6 +220,7 @@ __global__ void __launch_bounds__(kThreads, 2) matrix_kernel(MatrixArgs a) {
   ACC* colpart = static_cast<ACC*>(a.colpart);
   ACC* rowpart = static_cast<ACC*>(a.rowpart);
   int buf = 0;
+  const unsigned long long pol = matrix_policy(a.l2_normal);
 
   for (int tile = blockIdx.x; tile < a.tiles; tile += gridDim.x) {
     const int cb = tile % a.CB, rb = tile / a.CB;
@@ -271,7 +272,7 @@ __global__ void __launch_bounds__(kThreads, 2) matrix_kernel(MatrixArgs a) {
 #pragma unroll
           for (int k = 0; k < K; ++k)
             av[rr][mt][k] = (rv && ok[k])
-                                ? ld_stream(reinterpret_cast<const float4*>(a.M[mt] + i * a.ld + col[k]))
+                                ? ld_policy(reinterpret_cast<const float4*>(a.M[mt] + i * a.ld + col[k]), pol)
                                 : zero4;
       }
       ACC rp[NV];

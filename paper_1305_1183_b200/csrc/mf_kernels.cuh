@@ -62,6 +62,7 @@ struct MatrixArgs {
   unsigned* bar = nullptr;          // grid barrier {count, generation}
   int CB = 1, RB = 1, tiles = 1;    // column chunks, row bands, CB*RB
   PeerLinks peer;                   // nranks > 1: fused cross-GPU column reduction
+  int l2_normal = 0;                // matrix loads: 0 evict-first L2 policy, 1 evict-normal
 };
 
 // Shape of a matrix-kernel instantiation.

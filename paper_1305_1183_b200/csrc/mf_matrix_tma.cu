@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(NC + 32, 1) matrix_tma_kernel(MatrixArgs a, in
   if (warp == kConsumerWarps) {
     // ---------------- producer warp: one elected lane drives the bulk engine
     if (lane == 0) {
-      const unsigned long long pol = evict_first_policy();
+      const unsigned long long pol = matrix_policy(a.l2_normal);
       unsigned long long keep;  // per-row vector slices are re-read by every column chunk
       asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
       int stage = 0;

@@ -266,8 +266,10 @@ def run_workload(args, torch, mf, rank, world):
     return res
 
 
-def run_e2e(args, torch, mf, steps):
-    """Host buffers through mf_launch_host: H2D + kernels + D2H per step."""
+def run_e2e(args, torch, mf, steps, world=1):
+    """Host buffers through mf_launch_host: H2D + kernels + D2H per step.
+    Under torchrun every rank runs its own slice at the same time (after a
+    barrier); the time is the max over ranks and the bytes the sum."""
     import numpy as np
     n = args.n
     sc = {"alpha": 0.5, "beta": 0.75}
@@ -292,15 +294,22 @@ def run_e2e(args, torch, mf, steps):
         specs.append((p, {k: v[1] for k, v in host.items()}, host, d))
     for p, hb, _, _ in specs:  # warm-up (allocates device mirrors)
         p.launch_host(hb, sc)
+    if world > 1:
+        torch.distributed.barrier()
     t0 = time.perf_counter()
     for _ in range(steps):
         for p, hb, _, _ in specs:
             p.launch_host(hb, sc)
     el = time.perf_counter() - t0
     step_bytes = sum(d["bytes_loaded"] + d["bytes_stored"] for _, _, _, d in specs)
-    return {"value": step_bytes * steps / el / 1e9, "unit": "GB/s", "h2d_bytes_per_step": h2d,
-            "d2h_bytes_per_step": d2h, "steps": steps,
-            "path": "C-ABI mf_launch_host (pinned host buffers, H2D + fused kernels + D2H)"}
+    if world > 1:
+        t = torch.tensor([el], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        el = float(t.item())
+    return {"value": step_bytes * world * steps / el / 1e9, "unit": "GB/s",
+            "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world, "steps": steps,
+            "path": "C-ABI mf_launch_host (pinned host buffers, H2D + fused kernels + D2H)" +
+                    ("; all %d ranks concurrently, max time over ranks" % world if world > 1 else "")}
 
 
 def run_sharded(args, torch, mf, rank, world, seq):
@@ -509,8 +518,9 @@ def main():
             "kernel_us": per_kernel,
             "speedup_vs_unfused": round(res["unfused_ms_per_step"] / ms_per_step, 3),
             "bytes_saved_ratio": round((24 + 20) / 28, 3)}
+    e2e = run_e2e(args, torch, mf, args.e2e_steps, world)
     if rank == 0:
-        line["e2e"] = run_e2e(args, torch, mf, args.e2e_steps)
+        line["e2e"] = e2e
         if world == 1 and not args.no_suite:
             line["suite"] = run_suite(args, torch, mf)
         if world == 1 and not args.no_cpu:

@@ -20,6 +20,9 @@ L2, so no flush is needed between steps).
   speedup_vs_unfused  same step as one kernel per elementary call
   suite            the other BASELINE configs (AXPYDOT 2^24, BiCGK/ATAX 16384^2,
                    GEMVER/GESUMMV 32768^2), fused vs unfused, for context
+  sharded          BASELINE configs[4]: BiCGK 131072^2 row-sharded over the N
+                   ranks (strong scaling, NCCL all-reduce of A^T r); at N = 1
+                   it is T(1) for the efficiency T(1)/(N T(N))
 
 Multi-GPU (torchrun): every rank runs the workload on its own GPU on its own
 slice (element-wise sequences shard with no exchange; "scaling": "weak");
@@ -426,6 +429,8 @@ def main():
     ap.add_argument("--n", type=int, default=N_DEFAULT)
     ap.add_argument("--no-suite", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-sharded", action="store_true",
+                    help="skip the BiCGK 131072^2 row-sharded leg of the default workload")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--workload", default="blas1", choices=["blas1", "bicgk-sharded", "atax-sharded"])
     ap.add_argument("--n-matrix", type=int, default=131072)
@@ -519,8 +524,31 @@ def main():
             "speedup_vs_unfused": round(res["unfused_ms_per_step"] / ms_per_step, 3),
             "bytes_saved_ratio": round((24 + 20) / 28, 3)}
     e2e = run_e2e(args, torch, mf, args.e2e_steps, world)
+    torch.cuda.empty_cache()
+    sharded = None
+    if not args.no_sharded:
+        # BASELINE configs[4]: BiCGK 131072^2 row-sharded over the N ranks
+        # (strong scaling; T(1) at N = 1), column partials all-reduced by NCCL
+        import copy
+        sa = copy.copy(args)
+        sa.n_matrix, sa.collective, sa.mode = 131072, "nccl", "fused"
+        sa.steps, sa.warmup = max(5, min(args.steps, 20)), 3
+        try:
+            r = run_sharded(sa, torch, mf, rank, world, "BICGK")
+            peak, _ = measured_peak()
+            sharded = {"workload": "BiCGK fp32 131072x131072 row-sharded over %d GPU(s), column "
+                                   "partials all-reduced by NCCL after the fused kernel" % world,
+                       "value": round(r["value"], 1), "unit": "GB/s", "ms_per_step": round(r["ms_per_step"], 4),
+                       "steps": sa.steps, "scaling": "strong", "rows_per_rank": r["rows_per_rank"],
+                       "frac_per_gpu": round(r["value"] / world / peak, 4),
+                       "collectives_per_step": r["collectives_per_step"]}
+        except Exception as ex:  # report, keep the main line
+            sharded = {"error": str(ex)[:300]}
+        torch.cuda.empty_cache()
     if rank == 0:
         line["e2e"] = e2e
+        if sharded is not None:
+            line["sharded"] = sharded
         if world == 1 and not args.no_suite:
             line["suite"] = run_suite(args, torch, mf)
         if world == 1 and not args.no_cpu:

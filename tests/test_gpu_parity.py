@@ -80,6 +80,8 @@ def rand_inputs(seq, m, n, seed):
         return {"w": U(n), "y": U(n), "z": U(n)}
     if S == "WAXPBY":
         return {"x": U(n), "y": U(n), **sc}
+    if S == "SSCAL":
+        return {"x": U(n), "alpha": sc["alpha"]}
     raise KeyError(seq)
 
 
@@ -294,3 +296,47 @@ def test_empty_problems(env, seq, m, n):
     got = run_plan(torch, plan, vals, shapes)
     for name, v in got.items():
         assert v.size == 0 or np.all(v == 0), (name, v[:4])
+
+
+# Stream-kernel layouts: one CTA per 512-float4 block (default) and a capped
+# grid that strides over blocks (stream_ctas_per_sm > 0); sizes straddle the
+# block edge so the in-block tail path runs.  Maps are bit-exact either way;
+# the dot kernel keeps its own persistent layout.
+@pytest.mark.parametrize("n", [32, 2016, 2048, 2080, 4096 + 96, 3 * 2048 + 32, (1 << 20) + 160])
+@pytest.mark.parametrize("ctas", [0, 1, 4])
+@pytest.mark.parametrize("unroll", [0, 4])
+def test_stream_layouts_bit_exact(env, n, ctas, unroll):
+    torch, mf, co = env
+    mf.set_option("stream_ctas_per_sm", ctas)
+    mf.set_option("stream_unroll", unroll)
+    try:
+        for seq in ("VADD", "WAXPBY", "AXPYDOT", "SSCAL"):
+            vals = rand_inputs(seq, 1, n, 5 + n)
+            plan = mf.Plan.sequence(seq, 1, n, "fused")
+            got = run_plan(torch, plan, vals, out_shapes(plan))
+            want = co.execute(seq, 1, n, vals)
+            S = scale_bound(co, seq, 1, n, vals)
+            for name in want:
+                check_output(seq, name, got[name], want[name], S[name])
+    finally:
+        mf.set_option("stream_ctas_per_sm", 0)
+        mf.set_option("stream_unroll", 0)
+
+
+def test_matrix_l2_policy_does_not_change_results(env):
+    """The L2 eviction policy of matrix loads is a cache hint only: outputs are
+    bit-identical under evict-first, evict-normal and the per-shape default."""
+    torch, mf, co = env
+    for seq, m, n in [("GEMVER", 512, 4096), ("BICGK", 1024, 3072), ("GESUMMV", 256, 2048)]:
+        vals = rand_inputs(seq, m, n, 17)
+        plan = mf.Plan.sequence(seq, m, n, "fused")
+        outs = []
+        try:
+            for pol in (-1, 0, 1):
+                mf.set_option("matrix_l2_normal", pol)
+                outs.append(run_plan(torch, plan, vals, out_shapes(plan)))
+        finally:
+            mf.set_option("matrix_l2_normal", -1)
+        for name in outs[0]:
+            assert np.array_equal(outs[0][name], outs[1][name]), (seq, name)
+            assert np.array_equal(outs[0][name], outs[2][name]), (seq, name)

@@ -243,7 +243,13 @@ int mf_generate(float* dev, int64_t rows, int64_t cols, int64_t ld, uint64_t see
  * generic kernels issue their loads), "generic_checked" (0|1: keep per-access
  * index checks even when the bounds are proved at launch), "vm_exact" (0|1:
  * vm::launch always counts like the VM), "nvtx" (0|1: NVTX ranges per
- * kernel), "codegen_barriers" (test hook, 0 = codegen omits barriers). */
+ * kernel), "codegen_barriers" (test hook, 0 = codegen omits barriers),
+ * "tma" (-1 auto | 0 register-fed | 1 TMA ring matrix kernels),
+ * "tma_consumers" (0 auto | 256 | 512), "max_sms" (0 = all SMs, else cap the
+ * matrix grid), "matrix_l2_normal" (-1 auto: evict-normal for kernels that
+ * store a matrix, evict-first otherwise | 0 | 1), "stream_unroll" (0 = 2 |
+ * 2 | 4 | 8 float4 per thread per stream), "stream_ctas_per_sm" (0 = one CTA
+ * per block, else a capped grid striding over blocks). */
 int mf_set_option(const char* key, int value);
 int mf_get_option(const char* key);
 

@@ -772,6 +772,8 @@ int mf_set_option(const char* key, int value) {
     } else if (k == "max_sms") {
       if (value < 0) throw Invalid("max_sms >= 0");
       options().max_sms = value;
+    } else if (k == "tma_bulk_store") {
+      options().tma_bulk_store = value ? 1 : 0;
     } else if (k == "matrix_l2_normal") {
       options().matrix_l2_normal = value < 0 ? -1 : (value ? 1 : 0);
     } else if (k == "tma") {
@@ -814,6 +816,7 @@ int mf_get_option(const char* key) {
   if (k == "occupancy") return options().occupancy;
   if (k == "tma") return options().tma;
   if (k == "matrix_l2_normal") return options().matrix_l2_normal;
+  if (k == "tma_bulk_store") return options().tma_bulk_store;
   if (k == "max_sms") return options().max_sms;
   if (k == "tma_consumers") return options().tma_consumers;
   if (k == "stream_unroll") return options().stream_unroll;

@@ -29,6 +29,7 @@ EngineOptions& options() {
     if (const char* v = std::getenv("MF_STREAM_UNROLL")) e.stream_unroll = std::atoi(v);
     if (const char* v = std::getenv("MF_STREAM_CTAS")) e.stream_ctas_per_sm = std::atoi(v);
     if (const char* v = std::getenv("MF_MATRIX_L2_NORMAL")) e.matrix_l2_normal = std::atoi(v);
+    if (const char* v = std::getenv("MF_TMA_BULK_STORE")) e.tma_bulk_store = std::atoi(v);
     if (const char* v = std::getenv("MF_MAX_SMS")) e.max_sms = std::atoi(v);
     if (const char* v = std::getenv("MF_TMA_CONSUMERS")) e.tma_consumers = std::atoi(v);
     if (const char* v = std::getenv("MF_GENERIC_POISON")) e.generic_poison = std::atoi(v);
@@ -366,6 +367,7 @@ void run_matrix(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc, 
   // 16 consumer warps for the store-heavy rank shape (measured +2.3% on
   // GEMVER 32768^2, tools/sweep.py); 8 elsewhere.  tma_consumers 0 = auto.
   if (t.tma) t.consumers = eo.tma_consumers == 0 ? (heavy ? 512 : 256) : eo.tma_consumers;
+  t.bulk_store = sh.store && eo.tma_bulk_store != 0;
   if (t.tma && !tma_supported(sh, t)) t.tma = false;
   int grid = 0;
   const int sms = eo.max_sms > 0 ? std::min(eo.max_sms, device_sm_count()) : device_sm_count();

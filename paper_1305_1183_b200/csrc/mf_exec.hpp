@@ -47,6 +47,7 @@ struct EngineOptions {
   // 1996 us, fewer dirty lines of B left for the next kernel to write back),
   // evict-first for read-only kernels (BiCGK 159.7 -> 157.7 us)
   int matrix_l2_normal = -1;
+  int tma_bulk_store = 1;  // TMA store shapes: 1 = E leaves through cp.async.bulk S2G, 0 = st.global
   int generic_poison = 0;
   int nvtx = 0;
   int generic_checked = 0;  // 1: generic kernels keep per-access checks even when proved in bounds  // 1: an NVTX range around every kernel launch (named after the plan kernel)  // 1: generic kernels poison on-chip memory (VM fault on uninitialised reads)

@@ -78,6 +78,7 @@ struct MatrixTuning {
   int occupancy = 2;   // CTAs per SM targeted (register-fed variant)
   bool tma = true;     // TMA/mbarrier shared-memory ring (mf_matrix_tma.cu)
   int consumers = 256; // TMA variant: consumer threads per CTA (256 | 512)
+  bool bulk_store = false;  // TMA variant, store shapes: E leaves through cp.async.bulk S2G
 };
 
 // Launchers; return cudaSuccess or the launch error.  `sms` = SM count.

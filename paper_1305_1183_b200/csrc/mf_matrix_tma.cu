@@ -60,6 +60,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+               "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
 template <int NC>
 __device__ __forceinline__ void consumers_sync() {
   asm volatile("bar.sync 1, %0;" ::"n"(NC) : "memory");
@@ -74,8 +79,14 @@ __device__ __forceinline__ void band(const MatrixArgs& a, int rb, int R, long lo
   *r1 = (long long)(rb + 1) * units / a.RB * R;
 }
 
-template <int NMAT, int NRANK, bool STORE, int NROW, int NCOL, int K, int R, typename ACC, int NC>
+// BULK (store shapes): the updated matrix E is written back into the stage it
+// was read from and leaves through the bulk engine (cp.async.bulk S2G, one
+// copy per row segment) instead of per-thread st.global; the stage returns to
+// the producer once its store has read shared memory.
+template <int NMAT, int NRANK, bool STORE, int NROW, int NCOL, int K, int R, typename ACC, int NC,
+          bool BULK = false>
 __global__ void __launch_bounds__(NC + 32, 1) matrix_tma_kernel(MatrixArgs a, int S) {
+  static_assert(!BULK || STORE, "bulk stores need a stored matrix");
   constexpr int kConsumers = NC;
   constexpr int kConsumerWarps = NC / 32;
   constexpr int kTmaThreads = NC + 32;
@@ -96,7 +107,7 @@ __global__ void __launch_bounds__(NC + 32, 1) matrix_tma_kernel(MatrixArgs a, in
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kConsumerWarps);
+      mbar_init(&empty[s], BULK ? 1 : kConsumerWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -148,10 +159,12 @@ __global__ void __launch_bounds__(NC + 32, 1) matrix_tma_kernel(MatrixArgs a, in
     int stage = 0;
     unsigned phase = 0;
     int buf = 0;
+    int prev_stage = -1;  // BULK: stage whose store may still be reading shared memory
     for (int tile = blockIdx.x; tile < a.tiles; tile += gridDim.x) {
       const int cb = tile % a.CB, rb = tile / a.CB;
       long long r0, r1;
       band(a, rb, R, &r0, &r1);
+      const unsigned row_bytes = (unsigned)(min((long long)C, a.n - (long long)cb * C) * 4);
       int lcol[K];
       long long col[K];
       bool ok[K];
@@ -186,7 +199,7 @@ __global__ void __launch_bounds__(NC + 32, 1) matrix_tma_kernel(MatrixArgs a, in
 
       for (long long i0 = r0; i0 < r1; i0 += R) {
         mbar_wait(&full[stage], phase);
-        const float* st_mat = sm_mat + stage * kMatStage;
+        float* st_mat = sm_mat + stage * kMatStage;
         ACC rp[NV];
 #pragma unroll
         for (int j = 0; j < NV; ++j) rp[j] = ACC(0);
@@ -231,13 +244,34 @@ __global__ void __launch_bounds__(NC + 32, 1) matrix_tma_kernel(MatrixArgs a, in
                 cacc[c][k][e] = fmacc<ACC>(ev[mt], (ACC)xcs[c], cacc[c][k][e]);
               }
             }
-            if constexpr (STORE)
+            if constexpr (BULK)
+              *reinterpret_cast<float4*>(st_mat + rr * C + lcol[k]) = st;  // in place: own slots
+            else if constexpr (STORE)
               st_stream(reinterpret_cast<float4*>(a.E + (i0 + rr) * a.ld + col[k]), st);
           }
         }
-        // stage fully consumed by this warp -> release it to the producer
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[stage]);
+        if constexpr (BULK) {
+          // every consumer's E values are in the stage: make them visible to
+          // the async proxy, then one thread sends the R row segments out and
+          // returns the PREVIOUS stage once its store has read shared memory
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          consumers_sync<NC>();
+          if (tid == 0) {
+#pragma unroll
+            for (int rr = 0; rr < R; ++rr)
+              bulk_s2g(a.E + (i0 + rr) * a.ld + (long long)cb * C, st_mat + rr * C, row_bytes);
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            if (prev_stage >= 0) {
+              asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+              mbar_arrive(&empty[prev_stage]);
+            }
+            prev_stage = stage;
+          }
+        } else {
+          // stage fully consumed by this warp -> release it to the producer
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[stage]);
+        }
         if (++stage == S) {
           stage = 0;
           phase ^= 1u;
@@ -269,6 +303,10 @@ __global__ void __launch_bounds__(NC + 32, 1) matrix_tma_kernel(MatrixArgs a, in
             for (int e = 0; e < 4; ++e) dst[e] = cacc[c][k][e];
           }
     }
+    if constexpr (BULK) {
+      // E must be in global memory before the grid barrier / kernel end
+      if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    }
   }
 
   if constexpr (NCOL > 0 || NROW > 0) {
@@ -284,6 +322,12 @@ using TmaFn = void (*)(MatrixArgs, int);
 template <int NMAT, int NRANK, bool STORE, int NROW, int NCOL>
 TmaFn pick_tma(const MatrixTuning& t) {
   if (t.f64acc) return matrix_tma_kernel<NMAT, NRANK, STORE, NROW, NCOL, 2, 4, double, 256>;
+  if constexpr (STORE) {
+    if (t.bulk_store && t.consumers == 512)
+      return matrix_tma_kernel<NMAT, NRANK, STORE, NROW, NCOL, 2, 4, float, 512, true>;
+    if (t.bulk_store && t.K != 4)
+      return matrix_tma_kernel<NMAT, NRANK, STORE, NROW, NCOL, 2, 4, float, 256, true>;
+  }
   if (t.consumers == 512) return matrix_tma_kernel<NMAT, NRANK, STORE, NROW, NCOL, 2, 4, float, 512>;
   if (t.K == 4) return matrix_tma_kernel<NMAT, NRANK, STORE, NROW, NCOL, 4, 4, float, 256>;
   return matrix_tma_kernel<NMAT, NRANK, STORE, NROW, NCOL, 2, 4, float, 256>;

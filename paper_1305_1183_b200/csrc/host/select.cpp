@@ -31,7 +31,7 @@ CostModel CostModel::defaults() {
       {"matrix.ldg.read", 1.04},   // BiCGK 1.03, ATAX 1.05, GESUMMV 1.12
       {"matrix.tma.read", 0.95},   // BiCGK 0.92-0.97
       {"matrix.ldg.rank", 0.62},   // GEMVER ger2+sgemtv, register-fed
-      {"matrix.tma.rank", 0.97},   // GEMVER ger2+sgemtv, TMA ring, 16 consumer warps
+      {"matrix.tma.rank", 0.99},   // GEMVER ger2+sgemtv, TMA ring, 16 consumer warps, bulk S2G stores
       {"matrix.rowres", 0.88},     // row-resident chain (ATAX one pass, 16384^2)
       {"matrix.rowres.cluster", 0.75},  // ... rows over a CTA cluster (n > 16384): 32768^2 0.86, 131072 cols 0.71
       {"generic.d1", 0.70},        // NVRTC-emitted KernelIR (host/cudagen.cpp), depth 1,

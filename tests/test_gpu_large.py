@@ -110,3 +110,67 @@ def test_sharded_plan_single_rank_equals_plan(env):
     torch.cuda.synchronize()
     assert info["collectives"] == 1
     assert torch.equal(y1, y2)
+
+
+def test_blas1_bench_size_exact(env):
+    """The bench workload at its full size (n = 2^28): VADD x = w + y + z and
+    WAXPBY w = alpha x + beta y through the fused stream kernels, inputs from
+    the device generator.  Maps are bit-exact (fp64, rounded once), so whole
+    slices are compared exactly -- the first and last 2^20 elements (the
+    block-edge tail included) and a random interior slice."""
+    torch, mf, co = env
+    n = 1 << 28
+    vadd = mf.Plan.sequence("VADD", 1, n, "fused")
+    ins = {}
+    for i, k in enumerate(("w", "y", "z")):
+        ins[k] = torch.empty(n, device="cuda")
+        mf.generate(ins[k], seed=40 + i)
+    x = torch.empty(n, device="cuda")
+    vadd.launch({**ins, "x": x})
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(5)
+    mid = int(rng.integers(1 << 20, n - (2 << 20))) // 32 * 32
+    for lo in (0, mid, n - (1 << 20)):
+        sl = slice(lo, lo + (1 << 20))
+        vals = {k: ins[k][sl].cpu().numpy() for k in ("w", "y", "z")}
+        want = co.execute("VADD", 1, 1 << 20, vals)["x"]  # elementwise: a slice is a problem
+        assert np.array_equal(x[sl].cpu().numpy(), want), lo
+    del ins, x
+    torch.cuda.empty_cache()
+    wax = mf.Plan.sequence("WAXPBY", 1, n, "fused")
+    xx, yy, ww = (torch.empty(n, device="cuda") for _ in range(3))
+    mf.generate(xx, seed=50)
+    mf.generate(yy, seed=51)
+    al, be = 0.625, 0.375
+    wax.launch({"x": xx, "y": yy, "w": ww}, {"alpha": al, "beta": be})
+    torch.cuda.synchronize()
+    for lo in (0, mid, n - (1 << 20)):
+        sl = slice(lo, lo + (1 << 20))
+        vals = {"x": xx[sl].cpu().numpy(), "y": yy[sl].cpu().numpy(), "alpha": al, "beta": be}
+        want = co.execute("WAXPBY", 1, 1 << 20, vals)["w"]
+        assert np.array_equal(ww[sl].cpu().numpy(), want), lo
+    del xx, yy, ww
+    torch.cuda.empty_cache()
+
+
+def test_axpydot_full_size(env):
+    """AXPYDOT at n = 2^24 (BASELINE configs[0]) against the C oracle on the
+    same device-generated inputs: z bit-exact, r within tau * sum |z u|."""
+    torch, mf, co = env
+    n = 1 << 24
+    plan = mf.Plan.sequence("AXPYDOT", 1, n, "fused")
+    d = {}
+    for i, k in enumerate(("w", "v", "u")):
+        d[k] = torch.empty(n, device="cuda")
+        mf.generate(d[k], seed=60 + i)
+    d["z"] = torch.empty(n, device="cuda")
+    d["r"] = torch.empty(1, device="cuda")
+    al = 0.625
+    plan.launch(d, {"alpha": al})
+    torch.cuda.synchronize()
+    vals = {k: d[k].cpu().numpy() for k in ("w", "v", "u")}
+    want = co.execute("AXPYDOT", 1, n, {**vals, "alpha": al})
+    assert np.array_equal(d["z"].cpu().numpy(), want["z"])
+    zz = want["z"].astype(np.float64)
+    S = float(np.sum(np.abs(zz * vals["u"].astype(np.float64))))
+    _check(d["r"].cpu().numpy(), want["r"].astype(np.float64), np.array([S]), "r")

@@ -229,6 +229,22 @@ int mf_launch_peers(const mf_plan* plan, mf_peer_group* g, const mf_buffer* buff
 
 /* Counter-based synthetic data on the device, identical to the CPU checker's
  * generator: out[r*ld + c] = U(seed, (row0 + r) * ncols_global + c). */
+/* Single-process, multi-GPU row-sharded launch: the mf_launch_sharded of
+ * SURVEY.md 8(b).  GPU g (CUDA device devices[g]) runs plans[g] -- the plan
+ * for its row panel, used with that device only -- on its buffers
+ * per_gpu[g][0 .. nbuf[g]) and stream streams[g] (a cudaStream_t).  After
+ * each kernel, the kernel's column reductions and dots
+ * (mf_plan_kernel_column_outputs) are summed in place over the GPUs with
+ * ncclAllReduce(ncclFloat, ncclSum) on comms[g] (the caller's ncclComm_t, one
+ * per GPU, e.g. from ncclCommInitAll), inside one ncclGroupStart/End.  NCCL
+ * is resolved at run time from the copy the process has loaded (with one GPU
+ * and comms[0] == NULL no collective is issued).  Async on the
+ * streams; stats are summed over the GPUs.  Replaces a host loop over
+ * vm::launch per shard plus the host all-reduce the reference would need. */
+int mf_launch_sharded(const mf_plan* const* plans, int ngpus, const int* devices,
+                      const mf_buffer* const* per_gpu, const int* nbuf, const mf_scalar* scalars,
+                      int nscalars, void* const* comms, void* const* streams, mf_stats* stats);
+
 int mf_generate(float* dev, int64_t rows, int64_t cols, int64_t ld, uint64_t seed, int64_t row0,
                 int64_t ncols_global, void* stream);
 

@@ -1,6 +1,8 @@
 // mf_capi.cpp -- extern "C" surface declared in include/mapfuse_b200.h.
 #include "mapfuse_b200.h"
 
+#include <dlfcn.h>
+
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
@@ -221,6 +223,44 @@ double launch_host_pipelined(const mf_plan* plan, const mf_buffer* hb, int nbuf,
   for (auto& e : done) cudaEventDestroy(e);
   for (auto& x : st) cudaStreamDestroy(x);
   return ms;
+}
+
+// NCCL for mf_launch_sharded, resolved at run time from the copy the host
+// process already loaded (its communicators must come from the same
+// library), else the system libnccl.so.2.  Only the stable C ABI is used:
+// ncclAllReduce(sendbuf, recvbuf, count, ncclFloat = 7, ncclSum = 0, comm, stream).
+struct NcclApi {
+  int (*all_reduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*group_start)() = nullptr;
+  int (*group_end)() = nullptr;
+  const char* (*error_string)(int) = nullptr;
+  std::string error;
+};
+
+const NcclApi& nccl() {
+  static NcclApi api = [] {
+    NcclApi r;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW);
+    if (!h) {
+      r.error = std::string("mf_launch_sharded needs NCCL (libnccl.so.2): ") + dlerror();
+      return r;
+    }
+    r.all_reduce = reinterpret_cast<decltype(r.all_reduce)>(dlsym(h, "ncclAllReduce"));
+    r.group_start = reinterpret_cast<decltype(r.group_start)>(dlsym(h, "ncclGroupStart"));
+    r.group_end = reinterpret_cast<decltype(r.group_end)>(dlsym(h, "ncclGroupEnd"));
+    r.error_string = reinterpret_cast<decltype(r.error_string)>(dlsym(h, "ncclGetErrorString"));
+    if (!r.all_reduce || !r.group_start || !r.group_end) r.error = "libnccl.so.2 lacks the collective API";
+    return r;
+  }();
+  return api;
+}
+
+void check_nccl(int rc, const char* what) {
+  if (rc == 0) return;
+  const NcclApi& api = nccl();
+  throw Fault(std::string(what) + ": NCCL error " + std::to_string(rc) +
+              (api.error_string ? std::string(" (") + api.error_string(rc) + ")" : std::string()));
 }
 
 }  // namespace
@@ -740,6 +780,70 @@ int mf_launch_peers(const mf_plan* plan, mf_peer_group* g, const mf_buffer* buff
       run_kernel(P, k, b, s, static_cast<cudaStream_t>(stream), plan->ws, &g->g);
     fill_stats(P, 0, (int)P.kernels.size(), b, stats);
   });
+}
+
+int mf_launch_sharded(const mf_plan* const* plans, int ngpus, const int* devices,
+                      const mf_buffer* const* per_gpu, const int* nbuf, const mf_scalar* scalars,
+                      int nscalars, void* const* comms, void* const* streams, mf_stats* stats) {
+  int prev_dev = -1;
+  cudaGetDevice(&prev_dev);
+  const int rc = guarded([&] {
+    if (ngpus < 1 || !plans || !devices || !per_gpu || !nbuf || !comms || !streams)
+      throw Invalid("mf_launch_sharded: null argument or ngpus < 1");
+    const int nk = (int)plans[0]->plan.kernels.size();
+    for (int g = 0; g < ngpus; ++g) {
+      if (!plans[g]) throw Invalid("mf_launch_sharded: null plan for GPU " + std::to_string(g));
+      if ((int)plans[g]->plan.kernels.size() != nk)
+        throw Invalid("mf_launch_sharded: the per-GPU plans must have the same kernels");
+    }
+    // one GPU with a null communicator: nothing to reduce
+    const bool collective = ngpus > 1 || comms[0] != nullptr;
+    if (collective) {
+      const NcclApi& api = nccl();
+      if (!api.error.empty()) throw Fault(api.error);
+    }
+    const ScalarMap s = to_scalars(scalars, nscalars);
+    std::vector<BufMap> b(ngpus);
+    for (int g = 0; g < ngpus; ++g) {
+      check_cuda(cudaSetDevice(devices[g]), "cudaSetDevice");
+      b[g] = complete_bindings(plans[g]->plan, to_map(per_gpu[g], nbuf[g]), plans[g]->ws);
+    }
+    for (int k = 0; k < nk; ++k) {
+      for (int g = 0; g < ngpus; ++g) {
+        check_cuda(cudaSetDevice(devices[g]), "cudaSetDevice");
+        run_kernel(plans[g]->plan, k, b[g], s, static_cast<cudaStream_t>(streams[g]), plans[g]->ws);
+      }
+      // partial column sums / dots of kernel k, summed over the GPUs before
+      // any later kernel reads them (the only exchange in a Table-1 plan)
+      const auto names = plans[0]->plan.kernels[k].column_outputs();
+      if (!collective || names.empty()) continue;
+      const NcclApi& api = nccl();
+      check_nccl(api.group_start(), "ncclGroupStart");
+      for (const auto& name : names)
+        for (int g = 0; g < ngpus; ++g) {
+          auto it = b[g].find(name);
+          if (it == b[g].end() || !it->second.ptr)
+            throw Invalid("mf_launch_sharded: GPU " + std::to_string(g) + " has no buffer '" + name + "'");
+          check_nccl(api.all_reduce(it->second.ptr, it->second.ptr, (size_t)it->second.size(), 7, 0,
+                                    comms[g], static_cast<cudaStream_t>(streams[g])),
+                     "ncclAllReduce");
+        }
+      check_nccl(api.group_end(), "ncclGroupEnd");
+    }
+    if (stats) {
+      mf_stats acc{0, 0, 0.0, 0};
+      for (int g = 0; g < ngpus; ++g) {
+        mf_stats one{};
+        fill_stats(plans[g]->plan, 0, nk, b[g], &one);
+        acc.bytes_loaded += one.bytes_loaded;
+        acc.bytes_stored += one.bytes_stored;
+        acc.kernels += one.kernels;
+      }
+      *stats = acc;
+    }
+  });
+  if (prev_dev >= 0) cudaSetDevice(prev_dev);
+  return rc;
 }
 
 int mf_generate(float* dev, int64_t rows, int64_t cols, int64_t ld, uint64_t seed, int64_t row0,

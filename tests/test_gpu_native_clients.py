@@ -44,3 +44,16 @@ def test_c_abi_client():
           os.path.join(ROOT, "tests", "cpp_gpu", "c_abi_client.c"), "-L" + PKG, "-lmapfuse_b200",
           "-Wl,-rpath," + PKG, "-o", exe])
     assert "c-abi client ok" in _run([exe])
+
+
+def test_c_sharded_client_nccl():
+    """mf_launch_sharded from plain C: one process, every visible GPU, NCCL
+    communicators from ncclCommInitAll (on a one-GPU box the all-reduce runs
+    over a single rank)."""
+    exe = os.path.join(OUT, "c_sharded_client")
+    os.makedirs(OUT, exist_ok=True)
+    _run(["gcc", "-O1", "-I" + os.path.join(ROOT, "include"), "-I/usr/local/cuda/include",
+          os.path.join(ROOT, "tests", "cpp_gpu", "c_sharded_client.c"), "-L" + PKG, "-lmapfuse_b200",
+          "-Wl,-rpath," + PKG, "-L/usr/local/cuda/lib64", "-lcudart", "-Wl,-rpath,/usr/local/cuda/lib64",
+          "-lnccl", "-lm", "-o", exe])
+    assert "c sharded client ok" in _run([exe])

@@ -135,6 +135,22 @@ def ncu_traffic(kernel_key: str):
     return None
 
 
+def host_info():
+    """CPU model, logical cores and RAM of the box the CPU baseline ran on."""
+    model = ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+        with open("/proc/meminfo") as f:
+            mem_kb = int(f.readline().split()[1])
+    except Exception:
+        mem_kb = 0
+    return {"cpu": model, "nproc": os.cpu_count(), "ram_gb": round(mem_kb / 2 ** 20, 1)}
+
+
 # ---------------------------------------------------------------------------
 # CPU reference arm / baseline: the reference's reference_execute from
 # oracle/_ref, run on independent element slices in parallel threads (ctypes
@@ -169,6 +185,7 @@ def cpu_reference(n_total: int, threads: int, reps: int, warmup: int):
     nbytes = 28 * per * threads  # VADD 16n + WAXPBY 12n
     sec = statistics.median(times)
     return {"value": nbytes / sec / 1e9, "unit": "GB/s", "cores": threads, "kind": "reference",
+            "host": host_info(),
             "sample": "reference_execute (oracle/_ref) VADD+WAXPBY on %d x %d-element slices "
                       "(%d threads), make_problem excluded" % (threads, per, threads),
             "sec_per_step": sec, "elements": per * threads}
@@ -457,7 +474,8 @@ def main():
                 "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
                 "config": config,
                 "cpu_baseline": {"value": round(r["value"], 3), "unit": "GB/s",
-                                 "cores": r["cores"], "kind": "reference", "sample": r["sample"]},
+                                 "cores": r["cores"], "kind": "reference", "sample": r["sample"],
+                                 "host": r["host"]},
                 "e2e": {"value": round(r["value"], 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
@@ -508,7 +526,8 @@ def main():
     peak, peak_kind = measured_peak()
     achieved = vadd_bytes / (kms / 1e3) / 1e9
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": ncu_traffic("stream_kernel<3, 1, 0,"),
+                "frac": round(achieved / peak, 4), "frac_of_nominal_8000": round(achieved / 8000.0, 4),
+                "traffic": ncu_traffic("stream_kernel<3, 1, 0,"),
                 "kernel": key[2], "peak_source": peak_kind,
                 "algorithmic_bytes_per_launch": vadd_bytes,
                 "avg_launch_us": round(kms * 1e3, 1)}

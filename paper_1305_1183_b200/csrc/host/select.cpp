@@ -157,7 +157,16 @@ std::vector<Candidate> candidates(const script::Script& s, const script::DataDep
           c.item.native = generic_kernel(c.item.kir);
         }
       }
-      c.item.predicted_us = cm.predict_us(c.item.native, sz.rows, sz.cols);
+      // a stream kernel over tiles (MADD, flattened) streams m*n elements
+      int64_t pm = sz.rows, pn = sz.cols;
+      if (c.item.native.kind == b200::NativeKernel::Kind::Stream && !c.item.native.stream.inputs.empty()) {
+        auto d = s.declarations.find(c.item.native.stream.inputs[0]);
+        if (d != s.declarations.end() && d->second.depth() == 2) {
+          pn = sz.rows * sz.cols;
+          pm = 1;
+        }
+      }
+      c.item.predicted_us = cm.predict_us(c.item.native, pm, pn);
     } catch (const std::invalid_argument& e) {
       if (must) throw std::invalid_argument("call " + std::to_string(calls[0]) + ": " + e.what());
       return;  // infeasible implementation (the generic emitter rejected it too)

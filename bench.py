@@ -22,7 +22,9 @@ L2, so no flush is needed between steps).
                    GEMVER/GESUMMV 32768^2), fused vs unfused, for context
   sharded          BASELINE configs[4]: BiCGK 131072^2 row-sharded over the N
                    ranks (strong scaling, NCCL all-reduce of A^T r); at N = 1
-                   it is T(1) for the efficiency T(1)/(N T(N))
+                   it is T(1) for the efficiency T(1)/(N T(N)); at N > 1 also
+                   `fused_collective`: the same leg with A^T r reduced inside
+                   the kernel over NVLink peer memory (child processes)
 
 Multi-GPU (torchrun): every rank runs the workload on its own GPU on its own
 slice (element-wise sequences shard with no exchange; "scaling": "weak");
@@ -387,6 +389,32 @@ def run_sharded(args, torch, mf, rank, world, seq):
             "collectives_per_step": sum(len(c) for c in sp.collective_after)}
 
 
+def run_fused_child(args, rank, world, steps):
+    """Every rank starts `bench.py --workload bicgk-sharded --collective fused`
+    with its own RANK / WORLD_SIZE on another rendezvous port; rank 0 returns
+    the child's JSON summary (or the error)."""
+    import torch
+    env = dict(os.environ)
+    env["MASTER_PORT"] = str(int(env.get("MASTER_PORT", "29500")) + 17)
+    cmd = [sys.executable, os.path.abspath(__file__), "--workload", "bicgk-sharded",
+           "--collective", "fused", "--steps", str(steps), "--warmup", "3", "--gpus", str(world)]
+    torch.distributed.barrier()
+    try:
+        r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=300)
+        out = r.stdout.strip().splitlines()
+        if rank != 0:
+            return None
+        if r.returncode != 0 or not out:
+            return {"error": ("rc=%d " % r.returncode) + (r.stderr or "")[-300:]}
+        d = json.loads(out[-1])
+        return {"value": d["value"], "unit": d["unit"], "ms_per_step": d["ms_per_step"],
+                "frac_per_gpu": d["roofline"]["frac"], "workload": d["config"]["workload"]}
+    except Exception as ex:
+        return {"error": str(ex)[:300]} if rank == 0 else None
+    finally:
+        torch.distributed.barrier()
+
+
 SUITE = [("AXPYDOT", 1, 1 << 24), ("BICGK", 16384, 16384), ("ATAX", 16384, 16384),
          ("GEMVER", 32768, 32768), ("GESUMMV", 32768, 32768)]
 
@@ -448,6 +476,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-sharded", action="store_true",
                     help="skip the BiCGK 131072^2 row-sharded leg of the default workload")
+    ap.add_argument("--no-fused-child", action="store_true",
+                    help="N > 1: skip the in-kernel (NVLink peer memory) variant of the sharded leg")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--workload", default="blas1", choices=["blas1", "bicgk-sharded", "atax-sharded"])
     ap.add_argument("--n-matrix", type=int, default=131072)
@@ -564,6 +594,14 @@ def main():
         except Exception as ex:  # report, keep the main line
             sharded = {"error": str(ex)[:300]}
         torch.cuda.empty_cache()
+        if world > 1 and not args.no_fused_child:
+            # the same leg with the column reduction fused into the kernel over
+            # NVLink peer memory (CUDA IPC, no NCCL on the data path) -- in
+            # child processes with their own rendezvous, so a failure there
+            # cannot take this line down
+            fused = run_fused_child(args, rank, world, sa.steps)
+            if sharded is not None and fused is not None:
+                sharded["fused_collective"] = fused
     if rank == 0:
         line["e2e"] = e2e
         if sharded is not None:

@@ -236,6 +236,10 @@ b200::NativeKernel lower_kernel(const kernel::KernelIR& k) {
     for (size_t i = 0; i < mats.size(); ++i)
       if (mats[i].base == m.base) {
         if (mats[i].rank != m.rank) throw std::invalid_argument("lowering: one matrix, two updates");
+        // the same update stored under two names (two identical ger2 calls):
+        // the matrix kernel has one store -- leave it to the generic kernel
+        if (!mats[i].stored.empty() && !m.stored.empty() && mats[i].stored != m.stored)
+          throw std::invalid_argument("lowering: one matrix update stored twice");
         if (mats[i].stored.empty()) mats[i].stored = m.stored;
         return static_cast<int>(i);
       }

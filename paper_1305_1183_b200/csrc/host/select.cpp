@@ -147,6 +147,20 @@ std::vector<Candidate> candidates(const script::Script& s, const script::DataDep
       c.item.kir = generate_kernel(calls, s, g, L, base);
       c.item.native = lower_or_generic(c.item.kir);
       if (c.item.native.kind == b200::NativeKernel::Kind::Generic) {
+        // a reduction result consumed inside the fusion (planner mode b200's
+        // row-resident chains) needs the whole row before its consumer runs:
+        // only the native row-resident kernel provides that, the generic
+        // kernel follows the paper's per-tile semantics
+        for (const auto& e : g.edges)
+          if (std::find(calls.begin(), calls.end(), e.producer) != calls.end() &&
+              std::find(calls.begin(), calls.end(), e.consumer) != calls.end()) {
+            const lib::ElementaryFunction* f = nullptr;
+            for (const auto& cst : s.calls)
+              if (cst.id == e.producer) f = L.find(cst.function);
+            if (f && f->is_reduction())
+              throw std::invalid_argument("row-resident chain '" + e.name +
+                                          "' has no native kernel for this fusion");
+          }
         // generic kernels execute the KernelIR as written: pick the
         // implementation parameters (serial iterations) for this size
         const auto dom = domain_shape(c.item.kir, s, L, sz);

@@ -7,6 +7,8 @@ exercised on code the Table-1 suite does not cover.  Results are compared
 with the per-call fp64 oracle chain (reference_call semantics,
 proj/src/blas.cpp:275-342) within the tau*S bound.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -83,15 +85,22 @@ def abs_chain(co, calls, env, m, n):
     return reference_chain(co, calls, envs, m, n)
 
 
-@pytest.mark.parametrize("seed", range(40))
-def test_random_script(seed):
+# MF_RANDOM_SEEDS / MF_RANDOM_MODES widen the sweep for offline runs
+# (profiles/r01_random_scripts.txt); the default is 40 seeds in fused mode.
+SEEDS = range(int(os.environ.get("MF_RANDOM_SEEDS", "40")))
+MODES = os.environ.get("MF_RANDOM_MODES", "fused").split(",")
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("seed", SEEDS)
+def test_random_script(seed, mode):
     import torch
     import paper_1305_1183_b200 as mf
     co = COracle()
     rng = np.random.default_rng(seed)
     text, calls, returns = make_script(rng, 3 + seed % 5)
     m, n = 96 + 32 * (seed % 3), 128 + 64 * (seed % 4)
-    plan = mf.Plan.compile(text, m, n, "fused")
+    plan = mf.Plan.compile(text, m, n, mode)
     d = plan.describe()
     # input lengths follow the plan's shape inference (a vector no depth-2
     # call pins down is column-length, as in the reference's make_problem)

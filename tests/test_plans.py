@@ -189,3 +189,42 @@ def test_b200_mode_row_resident_plans():
     p = mf.Plan.sequence("ATAX", 1024, 1024, "b200")
     q = mf.Plan.from_kernel_text(p.kernel_text(0), 1024, 1024)
     assert q.describe()["kernels"][0]["op"]["chain"] is True
+
+
+def test_identical_rank_updates_stored_twice_are_not_merged():
+    """Two ger2 calls with the same operands and different results: the
+    matrix kernel has one store, so the fusion must not lower onto it (found
+    by the 1000-seed random-script sweep, profiles/r01_random_scripts.txt)."""
+    text = ("TILE32x32 A, v1, v2;\nsubvector32 xa, v0;\ninput A, xa, v0;\n"
+            "v1 = ger2(A, v0, xa, v0, xa);\nv2 = ger2(A, v0, xa, v0, xa);\nreturn v1, v2;\n")
+    d = mf.Plan.compile(text, 128, 320, "fused").describe()
+    for k in d["kernels"]:
+        if k["kind"] == "matrix":
+            assert k["shape"]["store"] <= 1 and "+" not in k["name"], k
+    outs = {b["name"] for b in d["buffers"] if b["role"] == "output"}
+    assert outs == {"v1", "v2"}
+
+
+def test_b200_mode_chains_only_on_the_native_kernel():
+    """Planner mode b200 fuses a row reduction into a column reduction only
+    where the row-resident kernel runs it: a chain with extra members must not
+    become a generic kernel (the paper's per-tile semantics would read a
+    partial row sum)."""
+    import numpy as np
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from test_gpu_random_scripts import make_script
+    for seed in (48, 49, 61, 94, 99, 103, 107, 111, 118, 119):
+        rng = np.random.default_rng(seed)
+        text, calls, _ = make_script(rng, 3 + seed % 5)
+        m, n = 96 + 32 * (seed % 3), 128 + 64 * (seed % 4)
+        p = mf.Plan.compile(text, m, n, "b200")
+        stmts = re.findall(r"^(\w+) = (\w+)\(([^)]*)\);$", text, re.M)  # call id = statement order
+        for kd in p.describe()["kernels"]:
+            if kd["kind"] != "generic":
+                continue
+            for a in kd["calls"]:
+                for b in kd["calls"]:
+                    out, fn, _ = stmts[a]
+                    args = [x.strip() for x in stmts[b][2].split(",")]
+                    assert not (fn in ("sgemv", "sgemvs", "sgemtv", "dot") and out in args), (seed, kd["name"])

@@ -89,6 +89,7 @@ def abs_chain(co, calls, env, m, n):
 # (profiles/r01_random_scripts.txt); the default is 40 seeds in fused mode.
 SEEDS = range(int(os.environ.get("MF_RANDOM_SEEDS", "40")))
 MODES = os.environ.get("MF_RANDOM_MODES", "fused").split(",")
+BIG = os.environ.get("MF_RANDOM_BIG", "0") == "1"
 
 
 @pytest.mark.parametrize("mode", MODES)
@@ -100,6 +101,8 @@ def test_random_script(seed, mode):
     rng = np.random.default_rng(seed)
     text, calls, returns = make_script(rng, 3 + seed % 5)
     m, n = 96 + 32 * (seed % 3), 128 + 64 * (seed % 4)
+    if BIG:  # several column chunks and row bands per matrix kernel, ragged edges
+        m, n = 1024 + 160 * (seed % 7), 2048 + 96 * (seed % 11)
     plan = mf.Plan.compile(text, m, n, mode)
     d = plan.describe()
     # input lengths follow the plan's shape inference (a vector no depth-2

@@ -114,8 +114,11 @@ int mf_plan_num_kernels(const mf_plan* plan);
 int mf_plan_describe(const mf_plan* plan, char* buf, int cap);
 /* Emitted KernelIR text of kernel k (same size convention). */
 int mf_plan_kernel_text(const mf_plan* plan, int k, char* buf, int cap);
-/* Comma-separated names kernel k produces by a column (cross-row) reduction;
- * under row sharding these are all-reduced before use. */
+/* Comma-separated names that kernel k leaves as per-rank PARTIAL sums under
+ * row sharding and that must be all-reduced before use:
+ * column (cross-row) reductions, and dots over split vectors.  A dot over
+ * vectors a matrix plan replicates (column-indexed) is whole on every rank
+ * and is not listed. */
 int mf_plan_kernel_column_outputs(const mf_plan* plan, int k, char* buf, int cap);
 
 /* Launches every kernel of the plan on `stream` (a cudaStream_t; NULL = the

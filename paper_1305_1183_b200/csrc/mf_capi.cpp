@@ -371,7 +371,7 @@ int mf_plan_kernel_text(const mf_plan* plan, int k, char* buf, int cap) {
 int mf_plan_kernel_column_outputs(const mf_plan* plan, int k, char* buf, int cap) {
   if (!plan || k < 0 || k >= (int)plan->plan.kernels.size()) return -1;
   std::string s;
-  for (const auto& n : plan->plan.kernels[k].column_outputs()) s += (s.empty() ? "" : ",") + n;
+  for (const auto& n : plan->plan.rank_reductions(k)) s += (s.empty() ? "" : ",") + n;
   return copy_out(s, buf, cap);
 }
 
@@ -769,8 +769,9 @@ int mf_launch_peers(const mf_plan* plan, mf_peer_group* g, const mf_buffer* buff
   return guarded([&] {
     if (!plan || !g) throw Invalid("null plan or peer group");
     const NativePlan& P = plan->plan;
-    for (const auto& k : P.kernels)
-      if (k.kind == NativeKernel::Kind::Generic && !k.column_outputs().empty())
+    for (int i = 0; i < (int)P.kernels.size(); ++i)
+      if (const auto& k = P.kernels[i];
+          k.kind == NativeKernel::Kind::Generic && !P.rank_reductions(i).empty())
         throw Invalid("kernel " + k.name +
                       ": generic kernels reduce across ranks with a host collective "
                       "(mf_launch_kernel + all-reduce of mf_plan_kernel_column_outputs)");
@@ -793,8 +794,12 @@ int mf_launch_sharded(const mf_plan* const* plans, int ngpus, const int* devices
     const int nk = (int)plans[0]->plan.kernels.size();
     for (int g = 0; g < ngpus; ++g) {
       if (!plans[g]) throw Invalid("mf_launch_sharded: null plan for GPU " + std::to_string(g));
-      if ((int)plans[g]->plan.kernels.size() != nk)
-        throw Invalid("mf_launch_sharded: the per-GPU plans must have the same kernels");
+      bool same = (int)plans[g]->plan.kernels.size() == nk;
+      for (int k = 0; same && k < nk; ++k)
+        same = plans[g]->plan.kernels[k].calls == plans[0]->plan.kernels[k].calls;
+      if (!same)
+        throw Invalid("mf_launch_sharded: the per-GPU plans must have the same kernel partition "
+                      "(the collectives after each kernel line up)");
     }
     // one GPU with a null communicator: nothing to reduce
     const bool collective = ngpus > 1 || comms[0] != nullptr;
@@ -815,7 +820,7 @@ int mf_launch_sharded(const mf_plan* const* plans, int ngpus, const int* devices
       }
       // partial column sums / dots of kernel k, summed over the GPUs before
       // any later kernel reads them (the only exchange in a Table-1 plan)
-      const auto names = plans[0]->plan.kernels[k].column_outputs();
+      const auto names = plans[0]->plan.rank_reductions(k);
       if (!collective || names.empty()) continue;
       const NcclApi& api = nccl();
       check_nccl(api.group_start(), "ncclGroupStart");

@@ -616,7 +616,10 @@ void run_kernel(const NativePlan& plan, int k, const BufMap& bufs, const ScalarM
   const bool nvtx = options().nvtx != 0;
   if (nvtx) nvtxRangePushA(kern.name.c_str());
   try {
-    if (kern.kind == NativeKernel::Kind::Stream) run_stream(kern, bufs, scalars, stream, ws, nullptr, peers);
+    // a dot over replicated vectors is whole on every rank: no peer reduction
+    if (kern.kind == NativeKernel::Kind::Stream)
+      run_stream(kern, bufs, scalars, stream, ws, nullptr,
+                 peers && !plan.rank_reductions(k).empty() ? peers : nullptr);
     else if (kern.kind == NativeKernel::Kind::Generic) run_generic(kern, bufs, scalars, stream, ws, nullptr);
     else run_matrix(kern, bufs, scalars, stream, ws, peers, nullptr);
   } catch (...) {

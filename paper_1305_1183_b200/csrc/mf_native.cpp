@@ -121,6 +121,32 @@ std::vector<std::string> NativeKernel::column_outputs() const {
   return v;
 }
 
+bool NativePlan::row_sharded_matrix() const {
+  for (const auto& k : kernels)
+    if (k.kind == NativeKernel::Kind::Matrix ||
+        (k.kind == NativeKernel::Kind::Generic && k.generic.depth == 2))
+      return true;
+  for (const auto& b : buffers)
+    if (b.rows > 1) return true;
+  return false;
+}
+
+std::vector<std::string> NativePlan::rank_reductions(int k) const {
+  const NativeKernel& kern = kernels.at(static_cast<size_t>(k));
+  std::vector<std::string> v = kern.column_outputs();
+  if (!row_sharded_matrix()) return v;  // depth-1 plans: every vector is split
+  // depth-1 reductions inside a matrix plan: split only if row-indexed
+  std::string over;
+  if (kern.kind == NativeKernel::Kind::Stream && kern.stream.has_dot && !kern.stream.inputs.empty())
+    over = kern.stream.inputs[0];
+  else if (kern.kind == NativeKernel::Kind::Generic && kern.generic.depth == 1)
+    over = kern.generic.domain;
+  if (over.empty()) return v;
+  const BufferSpec* b = find(over);
+  if (b && !b->row_indexed) return {};  // replicated vectors: the reduction is whole on every rank
+  return v;
+}
+
 static uint64_t generic_words(const GenericOp& g, const std::vector<std::string>& names, int64_t m,
                               int64_t n) {
   uint64_t w = 0;

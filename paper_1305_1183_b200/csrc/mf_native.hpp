@@ -164,6 +164,14 @@ struct NativePlan {
   uint64_t bytes_loaded() const;
   uint64_t bytes_stored() const;
   std::string describe_json() const;
+  // Row-sharded execution (sharding.py, mf_launch_peers, mf_launch_sharded):
+  // plans with a matrix split A into row panels and split row-indexed
+  // vectors, replicating column-indexed ones; depth-1 plans split every
+  // vector.  The outputs of kernel k that are then per-rank PARTIAL sums and
+  // must be summed over the ranks: column reductions always; a dot only when
+  // its vectors are split (a dot over replicated vectors is already whole).
+  bool row_sharded_matrix() const;
+  std::vector<std::string> rank_reductions(int k) const;
 };
 
 }  // namespace mapfuse::b200

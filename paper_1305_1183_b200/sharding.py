@@ -62,8 +62,12 @@ class ShardedPlan:
             lrows, lcols = 1, self.r1 - self.r0
         if lrows <= 0 or lcols <= 0:
             raise ValueError("problem too small for %d ranks" % world)
-        self.plan = (Plan.compile(script, lrows, lcols, mode, manifest=manifest) if script else
-                     Plan.sequence(sequence, lrows, lcols, mode))
+        # every rank must run the SAME kernel partition as every other (the
+        # collectives after each kernel have to line up): the local plan is the
+        # best-ranked combination for the local shape whose partition equals
+        # the global plan's -- panel heights differ across ranks, and the cost
+        # model may rank partitions differently per shape
+        self.plan = self._matching_plan(script, sequence, lrows, lcols, mode, manifest, d)
         self.desc = self.plan.describe()
         self.global_desc = d
         self.collective_after = [self.plan.column_outputs(k) for k in range(self.plan.num_kernels)]
@@ -83,6 +87,29 @@ class ShardedPlan:
                     self.fused_names[k] = list(self.collective_after[k])
             if self.peers is None and world > 1 and executor is None:
                 self.peers = self._connect_peers()
+
+    @staticmethod
+    def _matching_plan(script, sequence, rows, cols, mode, manifest, global_desc):
+        from .runtime import MapfuseError, sequence_script
+
+        def parts(desc):
+            return [tuple(k["calls"]) for k in desc["kernels"]]
+
+        target = parts(global_desc)
+        first = (Plan.compile(script, rows, cols, mode, manifest=manifest) if script else
+                 Plan.sequence(sequence, rows, cols, mode))
+        if parts(first.describe()) == target:
+            return first
+        text = script if script else sequence_script(sequence)
+        for r in range(1, 512):
+            try:
+                p = Plan.compile_ranked(text, rows, cols, r, mode, manifest)
+            except MapfuseError:
+                break
+            if parts(p.describe()) == target:
+                return p
+        raise ValueError("no plan for the local %dx%d panel has the global plan's kernel "
+                         "partition %s" % (rows, cols, target))
 
     def _connect_peers(self):
         """One PeerGroup per rank; IPC handles exchanged over the process group."""

@@ -228,3 +228,39 @@ def test_b200_mode_chains_only_on_the_native_kernel():
                     out, fn, _ = stmts[a]
                     args = [x.strip() for x in stmts[b][2].split(",")]
                     assert not (fn in ("sgemv", "sgemvs", "sgemtv", "dot") and out in args), (seed, kd["name"])
+
+
+def test_rank_reductions_skip_dots_over_replicated_vectors():
+    """Under row sharding a matrix plan replicates column-indexed vectors, so
+    a dot over them is whole on every rank and must not be summed again; a
+    dot over row-indexed (split) vectors and every column reduction are
+    partial (found by tests/test_gpu_random_sharded.py)."""
+    text = ("TILE32x32 A;\nsubvector32 xa, xb, ra, v0, v1;\nfloat s0, s1;\ninput A, xa, xb, ra;\n"
+            "v0 = sgemv(A, xa);\nv1 = sgemtv(A, ra);\ns0 = dot(xa, xb);\ns1 = dot(v0, ra);\n"
+            "return v1, s0, s1;\n")
+    p = mf.Plan.compile(text, 256, 192, "unfused")
+    d = p.describe()
+    red = {}
+    for k, kd in enumerate(d["kernels"]):
+        for name in kd["outputs"]:
+            red[name] = name in p.column_outputs(k)
+    assert red["v1"] and red["s1"] and not red["s0"] and not red["v0"], red
+    # depth-1 plans split every vector: their dots are partial
+    q = mf.Plan.sequence("AXPYDOT", 1, 4096, "fused")
+    assert q.column_outputs(0) == ["r"]
+
+
+def test_sharded_ranks_share_one_kernel_partition():
+    """Row panels of different heights may rank fusion partitions differently;
+    every rank must still run the global plan's partition so the collectives
+    after each kernel line up (found by tests/test_gpu_random_sharded.py)."""
+    from paper_1305_1183_b200.sharding import ShardedPlan
+    text = ("TILE32x32 A;\nsubvector32 xa, xb, ra, v0, v1, v3;\nfloat k, s3;\n"
+            "input A, xa, xb, ra, k;\nv0 = sgemv(A, xb);\nv1 = sgemvs(k, A, xa);\n"
+            "s3 = dot(xb, xa);\nv3 = sgemtv(A, v0);\nreturn v1, s3, v3;\n")
+    parts = []
+    for r in range(2):
+        sp = ShardedPlan(script=text, rows=224, cols=128, mode="fused", world=2, rank=r)
+        parts.append(([k["calls"] for k in sp.desc["kernels"]], sp.collective_after))
+    glob = [k["calls"] for k in mf.Plan.compile(text, 224, 128, "fused").describe()["kernels"]]
+    assert parts[0] == parts[1] and parts[0][0] == glob, parts

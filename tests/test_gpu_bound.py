@@ -88,3 +88,35 @@ def test_graph_needs_a_stream():
     bound = plan.bind(bufs, {})
     with pytest.raises(mf.ParseError, match="non-default stream"):
         bound.graph_launch(None)
+
+
+@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("MF_RANDOM_BOUND_SEEDS", "16"))))
+def test_random_scripts_bound_and_graph(seed):
+    """Random planner outputs (tests/test_gpu_random_scripts.py) replayed as
+    bound plans and CUDA graphs: bit-identical to Plan.launch where every
+    kernel is hand-written (generic kernels accumulate with atomics)."""
+    import torch
+    import paper_1305_1183_b200 as mf
+    from test_gpu_random_scripts import make_script
+    rng = np.random.default_rng(7000 + seed)
+    text, _, _ = make_script(rng, 3 + seed % 5)
+    m, n = 1024 + 96 * (seed % 3), 2048 + 160 * (seed % 4)
+    plan = mf.Plan.compile(text, m, n, ("fused", "unfused", "b200")[seed % 3])
+    if any(k["kind"] == "generic" for k in plan.describe()["kernels"]):
+        pytest.skip("generic kernels are not bit-reproducible (float atomics)")
+    sc = {"k": 0.625}
+    bufs = make(torch, mf, plan, seed)
+    plan.launch(bufs, sc)
+    torch.cuda.synchronize()
+    want = outputs(plan, bufs)
+    bound = plan.bind(bufs, sc)
+    s = torch.cuda.Stream()
+    for k in want:
+        bufs[k].fill_(float("nan"))
+    torch.cuda.synchronize()
+    for _ in range(3):
+        bound.graph_launch(s)
+    s.synchronize()
+    got = outputs(plan, bufs)
+    for k in want:
+        assert np.array_equal(got[k], want[k], equal_nan=True), (text, k)

@@ -90,6 +90,7 @@ def abs_chain(co, calls, env, m, n):
 SEEDS = range(int(os.environ.get("MF_RANDOM_SEEDS", "40")))
 MODES = os.environ.get("MF_RANDOM_MODES", "fused").split(",")
 BIG = os.environ.get("MF_RANDOM_BIG", "0") == "1"
+TINY = os.environ.get("MF_RANDOM_TINY", "0") == "1"
 
 
 @pytest.mark.parametrize("mode", MODES)
@@ -103,6 +104,8 @@ def test_random_script(seed, mode):
     m, n = 96 + 32 * (seed % 3), 128 + 64 * (seed % 4)
     if BIG:  # several column chunks and row bands per matrix kernel, ragged edges
         m, n = 1024 + 160 * (seed % 7), 2048 + 96 * (seed % 11)
+    if TINY:  # one 32x32 tile or a row of them
+        m, n = 32 * (1 + seed % 2), 32 * (1 + seed % 3)
     plan = mf.Plan.compile(text, m, n, mode)
     d = plan.describe()
     # input lengths follow the plan's shape inference (a vector no depth-2

@@ -91,6 +91,7 @@ SEEDS = range(int(os.environ.get("MF_RANDOM_SEEDS", "40")))
 MODES = os.environ.get("MF_RANDOM_MODES", "fused").split(",")
 BIG = os.environ.get("MF_RANDOM_BIG", "0") == "1"
 TINY = os.environ.get("MF_RANDOM_TINY", "0") == "1"
+RANDOM_OPTIONS = os.environ.get("MF_RANDOM_OPTIONS", "0") == "1"
 
 
 @pytest.mark.parametrize("mode", MODES)
@@ -121,8 +122,22 @@ def test_random_script(seed, mode):
         v = env.get(b["name"])
         bufs[b["name"]] = (torch.from_numpy(v).cuda() if isinstance(v, np.ndarray)
                            else torch.full(shp, float("nan"), device="cuda"))
-    plan.launch(bufs, {"k": env["k"]})
-    torch.cuda.synchronize()
+    opts = {}
+    if RANDOM_OPTIONS:  # a random engine variant per seed (every setting must give the same results)
+        orng = np.random.default_rng(seed + 17)
+        opts = {"tma": int(orng.choice([-1, 0, 1])), "matrix_k": int(orng.choice([2, 4])),
+                "f64acc": int(orng.choice([0, 1])), "matrix_l2_normal": int(orng.choice([-1, 0, 1])),
+                "tma_bulk_store": int(orng.choice([0, 1])), "stream_ctas_per_sm": int(orng.choice([0, 2])),
+                "stream_unroll": int(orng.choice([0, 4])), "tma_consumers": int(orng.choice([0, 256, 512]))}
+    saved = {k: mf.get_option(k) for k in opts}
+    try:
+        for k, v in opts.items():
+            mf.set_option(k, v)
+        plan.launch(bufs, {"k": env["k"]})
+        torch.cuda.synchronize()
+    finally:
+        for k, v in saved.items():
+            mf.set_option(k, v)
     want = reference_chain(co, calls, dict(env), m, n)
     S = abs_chain(co, calls, dict(env), m, n)
     for name in returns:

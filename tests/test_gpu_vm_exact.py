@@ -143,3 +143,23 @@ def test_measure_routine_matches_reference(env):
                 assert got == want, (fn, r, inst, it, extra, got, want)
                 checked += 1
     assert checked >= 100
+
+
+@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("MF_RANDOM_VM_SEEDS", "12"))))
+def test_random_scripts_stats_match_reference_vm(env, seed):
+    """Every kernel of a random planner output (tests/test_gpu_random_scripts.py)
+    through vm::launch on the GPU against the reference VM: the same
+    ExecutionStats field by field, maps bit-exact."""
+    mf, ref = env
+    from test_gpu_random_scripts import make_script
+    rng = np.random.default_rng(9000 + seed)
+    text, _, _ = make_script(rng, 3 + seed % 5)
+    m, n = 64 + 32 * (seed % 2), 96 + 32 * (seed % 3)
+    plan = mf.Plan.compile(text, m, n, ("fused", "unfused")[seed % 2])
+    host = host_buffers(plan, {}, rng)
+    mf.set_option("vm_exact", 1)  # hand-written-covered kernels count like the VM too
+    try:
+        for k in range(plan.num_kernels):
+            host = compare_kernel(mf, ref, plan.kernel_text(k), host, {"k": 0.625}, trace=seed % 3 == 0)
+    finally:
+        mf.set_option("vm_exact", 0)

@@ -183,6 +183,21 @@ __global__ void __launch_bounds__(32) dma_copy(const char* x, char* y, long long
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// B with T threads per CTA
+template <int NIN, int U, int T>
+__global__ void __launch_bounds__(T) blocked_t(Ptrs p, long long n4) {
+  const long long base = (long long)blockIdx.x * T * U + threadIdx.x;
+  float4 v[U][NIN];
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+#pragma unroll
+    for (int k = 0; k < NIN; ++k)
+      if (base + u * T < n4) v[u][k] = ld<false>(p.x[k] + base + u * T);
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+    if (base + u * T < n4) st<false>(p.y + base + u * T, combine<NIN>(v[u]));
+}
+
 static double bytes_per_elem = 8.0;
 
 int main(int argc, char** argv) {
@@ -246,6 +261,19 @@ int main(int argc, char** argv) {
     run(nm, [&] { blocked<NIN, U, LH, SH><<<(unsigned)nb, 256>>>(P, n4); });                   \
   }
 #define HINTS(NIN, U) VARS(NIN, U, false, false) VARS(NIN, U, true, false) VARS(NIN, U, false, true) VARS(NIN, U, true, true)
+  if (getenv("PROBE_THREADS")) {
+#define BT(NIN, U, T)                                                                   \
+  {                                                                                     \
+    bytes_per_elem = 4.0 * (NIN + 1);                                                   \
+    const long long nb = (n4 + (long long)T * U - 1) / ((long long)T * U);              \
+    snprintf(nm, sizeof nm, "in%d B%d T=%d", NIN, U, T);                                \
+    run(nm, [&] { blocked_t<NIN, U, T><<<(unsigned)nb, T>>>(P, n4); });                 \
+  }
+    BT(3, 2, 128) BT(3, 2, 256) BT(3, 2, 512) BT(3, 4, 128) BT(3, 1, 512) BT(3, 1, 1024)
+    BT(2, 2, 128) BT(2, 2, 256) BT(2, 2, 512) BT(2, 4, 128) BT(2, 1, 512)
+    BT(1, 2, 128) BT(1, 2, 256) BT(1, 2, 512) BT(1, 4, 128) BT(1, 1, 512)
+    return 0;
+  }
   if (getenv("PROBE_DMA")) {
     bytes_per_elem = 8.0;
     for (int blk : {8192, 16384, 32768}) {

@@ -478,7 +478,7 @@ def main():
                     help="skip the BiCGK 131072^2 row-sharded leg of the default workload")
     ap.add_argument("--no-fused-child", action="store_true",
                     help="N > 1: skip the in-kernel (NVLink peer memory) variant of the sharded leg")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--workload", default="blas1", choices=["blas1", "bicgk-sharded", "atax-sharded"])
     ap.add_argument("--n-matrix", type=int, default=131072)
     ap.add_argument("--mode", default="fused", choices=["fused", "b200"],

@@ -149,3 +149,44 @@ def test_random_script(seed, mode):
         lim = 4 * TAU * s + 4 * np.spacing(np.abs(w).astype(np.float32)).astype(np.float64)
         err = np.abs(got - w)
         assert np.all(err <= lim), (text, name, float(np.max(err / np.maximum(lim, 1e-300))))
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("MF_RANDOM_COMBO_SEEDS", "10"))))
+def test_random_script_every_combination(seed):
+    """Every fusion combination the selector enumerates for a random script
+    (not only its first choice) runs and matches the oracle chain: each
+    combination is a different set of kernels (Plan.compile_ranked)."""
+    import torch
+    import paper_1305_1183_b200 as mf
+    co = COracle()
+    rng = np.random.default_rng(20000 + seed)
+    text, calls, returns = make_script(rng, 3 + seed % 5)
+    m, n = 96 + 32 * (seed % 3), 128 + 64 * (seed % 4)
+    env = None
+    want = S = None
+    for r in range(min(mf.Plan.count_combinations(text, m, n), 12)):
+        plan = mf.Plan.compile_ranked(text, m, n, r, "fused")
+        d = plan.describe()
+        if env is None:
+            env = {"k": 0.625}
+            for b in d["buffers"]:
+                if b["role"] == "input":
+                    shp = (b["rows"], b["cols"]) if b["rows"] > 1 else (b["cols"],)
+                    env[b["name"]] = rng.uniform(-1, 1, shp).astype(np.float32)
+            want = reference_chain(co, calls, dict(env), m, n)
+            S = abs_chain(co, calls, dict(env), m, n)
+        bufs = {}
+        for b in d["buffers"]:
+            shp = (b["rows"], b["cols"]) if b["rows"] > 1 else (b["cols"],)
+            v = env.get(b["name"])
+            bufs[b["name"]] = (torch.from_numpy(v).cuda() if isinstance(v, np.ndarray)
+                               else torch.full(shp, float("nan"), device="cuda"))
+        plan.launch(bufs, {"k": env["k"]})
+        torch.cuda.synchronize()
+        for name in returns:
+            got = bufs[name].cpu().numpy().astype(np.float64).ravel()
+            w = np.asarray(want[name], np.float64).ravel()
+            s = np.asarray(S[name], np.float64).ravel()
+            lim = 4 * TAU * s + 4 * np.spacing(np.abs(w).astype(np.float32)).astype(np.float64)
+            err = np.abs(got - w)
+            assert np.all(err <= lim), (text, r, name, float(np.max(err / np.maximum(lim, 1e-300))))

@@ -264,3 +264,29 @@ def test_sharded_ranks_share_one_kernel_partition():
         parts.append(([k["calls"] for k in sp.desc["kernels"]], sp.collective_after))
     glob = [k["calls"] for k in mf.Plan.compile(text, 224, 128, "fused").describe()["kernels"]]
     assert parts[0] == parts[1] and parts[0][0] == glob, parts
+
+
+@pytest.mark.parametrize("mode", ["fused", "unfused", "b200"])
+def test_random_scripts_plan_file_round_trip(mode):
+    """Plan files (mf_plan_save / mf_plan_load) reproduce random planner
+    outputs exactly: same kernels, shapes, buffers and kernel IR."""
+    import json
+    import sys
+
+    import numpy as np
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from test_gpu_random_scripts import make_script
+    for seed in range(60):
+        rng = np.random.default_rng(30000 + seed)
+        text, _, _ = make_script(rng, 3 + seed % 5)
+        m, n = 96 + 32 * (seed % 3), 128 + 64 * (seed % 4)
+        p = mf.Plan.compile(text, m, n, mode)
+        q = mf.Plan.load(p.save())
+        a, b = p.describe(), q.describe()
+        for d in (a, b):
+            d.pop("predicted_us", None)
+            for k in d["kernels"]:
+                k.get("op", {}).pop("source_bytes", None)
+        assert json.dumps(a, sort_keys=True) == json.dumps(b, sort_keys=True), (seed, text)
+        for k in range(p.num_kernels):
+            assert p.kernel_text(k) == q.kernel_text(k), (seed, k)

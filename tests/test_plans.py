@@ -290,3 +290,24 @@ def test_random_scripts_plan_file_round_trip(mode):
         assert json.dumps(a, sort_keys=True) == json.dumps(b, sort_keys=True), (seed, text)
         for k in range(p.num_kernels):
             assert p.kernel_text(k) == q.kernel_text(k), (seed, k)
+
+
+def test_random_kernels_text_boundary_round_trip():
+    """mf_plan_create(kernel_ir_text): every kernel of random planner outputs,
+    re-created from its KernelIR text alone, lowers to the same family, shape
+    and bindings (the vm::launch boundary, SURVEY 8(b))."""
+    import sys
+
+    import numpy as np
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from test_gpu_random_scripts import make_script
+    for seed in range(80):
+        rng = np.random.default_rng(40000 + seed)
+        text, _, _ = make_script(rng, 3 + seed % 5)
+        m, n = 96 + 32 * (seed % 3), 128 + 64 * (seed % 4)
+        p = mf.Plan.compile(text, m, n, ("fused", "unfused", "b200")[seed % 3])
+        d = p.describe()
+        for k in range(p.num_kernels):
+            qd = mf.Plan.from_kernel_text(p.kernel_text(k), m, n).describe()["kernels"][0]
+            for key in ("kind", "shape", "inputs", "outputs"):
+                assert qd.get(key) == d["kernels"][k].get(key), (seed, k, key, text)

@@ -1,6 +1,14 @@
-import sys, statistics
-sys.path.insert(0, '/root/repo')
-import torch, paper_1305_1183_b200 as mf
+"""Run-to-run spread of the fused AXPYDOT kernel (n = 2^24) under three
+timing regimes: L2 flushed before each launch, back-to-back, and flushed with
+an idle gap.  python tools/axpy_variance.py"""
+import os
+import statistics
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_1305_1183_b200 as mf  # noqa: E402
 p = mf.Plan.sequence("AXPYDOT", 1, 1 << 24, "fused")
 bufs = {}
 for i, b in enumerate(p.describe()["buffers"]):

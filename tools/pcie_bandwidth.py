@@ -1,3 +1,6 @@
+"""Pinned host <-> B200 copy bandwidth (1 GiB, torch copies): H2D, D2H and
+both directions at once on two streams -- the bound of bench.py's e2e leg.
+python tools/pcie_bandwidth.py"""
 import torch, time
 n = 256 << 20
 h = torch.empty(n, dtype=torch.float32).pin_memory()

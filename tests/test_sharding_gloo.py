@@ -118,3 +118,90 @@ def test_split_covers_exactly():
             for (a, b), (c, d) in zip(blocks, blocks[1:]):
                 assert b == c and a <= b
             assert all(b % 32 == 0 or b == total for _, b in blocks)
+
+
+def _worker_script(rank, world, port, text, m, n, seed, q):
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    sys.path.insert(0, os.path.join(root, "tests"))
+    sys.path.insert(0, os.path.join(root, "oracle"))
+    from plan_emulator import run_kernel
+    from paper_1305_1183_b200.sharding import ShardedPlan
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        sp = ShardedPlan(script=text, rows=m, cols=n, mode="fused", executor=run_kernel)
+        rng = np.random.default_rng(seed)
+        gd = sp.global_desc
+        full = {}
+        for b in gd["buffers"]:
+            shp = (b["rows"], b["cols"]) if b["rows"] > 1 else (b["cols"],)
+            full[b["name"]] = (rng.uniform(-1, 1, shp).astype(np.float32) if b["role"] == "input"
+                               else np.zeros(shp, np.float32))
+        local = {}
+        for name, a in full.items():
+            sl = sp.local_slice(name)
+            local[name] = torch.from_numpy((a if sl is None else a[sl[1]:sl[2]]).copy())
+        for b in sp.desc["buffers"]:  # intermediates the local plan adds
+            if b["name"] not in local:
+                shp = (b["rows"], b["cols"]) if b["rows"] > 1 else (b["cols"],)
+                local[b["name"]] = torch.zeros(shp)
+        sp.launch(local, {"k": 0.625})
+        outs = {}
+        for b in gd["buffers"]:
+            if b["role"] != "output":
+                continue
+            sl = sp.local_slice(b["name"])
+            parts = [None] * world
+            dist.all_gather_object(parts, local[b["name"]].numpy())
+            outs[b["name"]] = parts[0] if sl is None else np.concatenate(parts, axis=0)
+            if sl is None:  # replicated: every rank holds the same value
+                assert all(np.array_equal(parts[0], p) for p in parts), b["name"]
+        if rank == 0:
+            q.put((outs, {k: v for k, v in full.items() if gd and k in
+                          {x["name"] for x in gd["buffers"] if x["role"] == "input"}},
+                   [k["calls"] for k in sp.desc["kernels"]]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("seed", range(int(os.environ.get("MF_GLOO_RANDOM_SEEDS", "3"))))
+def test_random_scripts_row_sharded_gloo(seed, world):
+    """Random planner outputs sharded over real gloo process groups: every
+    rank must pick the same kernel partition, the layer must all-reduce
+    exactly the rank partials (no dot over replicated vectors), and the
+    gathered outputs must match the per-call fp64 oracle chain."""
+    import paper_1305_1183_b200 as mf
+    from oracle import COracle
+    from test_gpu_random_scripts import abs_chain, make_script, reference_chain
+    from gpu_util import TAU
+    rng = np.random.default_rng(50000 + seed)
+    text, calls, returns = make_script(rng, 3 + seed % 5)
+    m, n = 192 + 32 * (seed % 3), 128 + 64 * (seed % 4)
+    if any(k["kind"] == "generic" for k in mf.Plan.compile(text, m, n, "fused").describe()["kernels"]):
+        pytest.skip("the CPU kernel emulator covers the hand-written families only")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker_script, args=(r, world, port, text, m, n, seed, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    outs, inputs, _ = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    co = COracle()
+    env = dict(inputs)
+    env["k"] = 0.625
+    want = reference_chain(co, calls, dict(env), m, n)
+    S = abs_chain(co, calls, dict(env), m, n)
+    for name in returns:
+        got = np.asarray(outs[name], np.float64).ravel()
+        w = np.asarray(want[name], np.float64).ravel()
+        s = np.asarray(S[name], np.float64).ravel()
+        lim = 4 * TAU * s + 4 * np.spacing(np.abs(w).astype(np.float32)).astype(np.float64)
+        assert np.all(np.abs(got - w) <= lim), (text, name)

@@ -190,3 +190,34 @@ def test_random_script_every_combination(seed):
             lim = 4 * TAU * s + 4 * np.spacing(np.abs(w).astype(np.float32)).astype(np.float64)
             err = np.abs(got - w)
             assert np.all(err <= lim), (text, r, name, float(np.max(err / np.maximum(lim, 1e-300))))
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("MF_RANDOM_HOST_SEEDS", "8"))))
+def test_random_script_host_launch_matches_device(seed):
+    """mf_launch_host (vm::launch's host-buffer contract: inputs and outputs
+    only, intermediates on the device) gives the device launch's results bit
+    for bit on random plans of hand-written kernels."""
+    import torch
+    import paper_1305_1183_b200 as mf
+    rng = np.random.default_rng(60000 + seed)
+    text, _, _ = make_script(rng, 3 + seed % 5)
+    m, n = 96 + 32 * (seed % 3), 128 + 64 * (seed % 4)
+    plan = mf.Plan.compile(text, m, n, ("fused", "unfused", "b200")[seed % 3])
+    d = plan.describe()
+    if any(k["kind"] == "generic" for k in d["kernels"]):
+        pytest.skip("generic kernels are not bit-reproducible (float atomics)")
+    host, dev = {}, {}
+    for b in d["buffers"]:
+        if b["role"] == "intermediate":
+            continue
+        shp = (b["rows"], b["cols"]) if b["rows"] > 1 else (b["cols"],)
+        a = (rng.uniform(-1, 1, shp).astype(np.float32) if b["role"] == "input"
+             else np.zeros(shp, np.float32))
+        host[b["name"]] = a
+        dev[b["name"]] = torch.from_numpy(a.copy()).cuda()
+    plan.launch_host(host, {"k": 0.625})
+    plan.launch(dev, {"k": 0.625})
+    torch.cuda.synchronize()
+    for b in d["buffers"]:
+        if b["role"] == "output":
+            assert np.array_equal(host[b["name"]], dev[b["name"]].cpu().numpy()), (text, b["name"])

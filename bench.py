@@ -53,8 +53,14 @@ METRIC = "fused-sequence effective GB/s"
 WORKLOAD = "BLAS-1 chains fp32 n=2^28: VADD (x=w+y+z) + WAXPBY (w=alpha*x+beta*y), planner-fused"
 
 
+# MF_BENCH_SHARED_GPU=1: every rank on cuda:0 with a gloo process group -- a
+# one-GPU smoke run of the multi-rank code path (numbers are not meaningful)
+SHARED_GPU = os.environ.get("MF_BENCH_SHARED_GPU", "0") == "1"
+
+
 def env_rank():
-    return (int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0")),
+    return (int(os.environ.get("RANK", "0")),
+            0 if SHARED_GPU else int(os.environ.get("LOCAL_RANK", "0")),
             int(os.environ.get("WORLD_SIZE", "1")))
 
 
@@ -267,7 +273,7 @@ def run_workload(args, torch, mf, rank, world):
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
-    gpu_index = int(os.environ.get("LOCAL_RANK", "0"))
+    gpu_index = env_rank()[1]
     with ClockSampler(gpu_index) as clk:
         total_ms, per = time_kernels(torch, plans, args.steps, args.warmup)
     if world > 1:
@@ -365,7 +371,7 @@ def run_sharded(args, torch, mf, rank, world, seq):
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
-    gpu_index = int(os.environ.get("LOCAL_RANK", "0"))
+    gpu_index = env_rank()[1]
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(gpu_index) as clk:
         start.record()
@@ -400,7 +406,7 @@ def run_fused_child(args, rank, world, steps):
            "--collective", "fused", "--steps", str(steps), "--warmup", "3", "--gpus", str(world)]
     torch.distributed.barrier()
     try:
-        r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=300)
+        r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=150)
         out = r.stdout.strip().splitlines()
         if rank != 0:
             return None
@@ -515,7 +521,10 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if SHARED_GPU:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_1305_1183_b200 as mf
     mf.lib()
 
@@ -594,7 +603,7 @@ def main():
         except Exception as ex:  # report, keep the main line
             sharded = {"error": str(ex)[:300]}
         torch.cuda.empty_cache()
-        if world > 1 and not args.no_fused_child:
+        if world > 1 and not args.no_fused_child and not SHARED_GPU:
             # the same leg with the column reduction fused into the kernel over
             # NVLink peer memory (CUDA IPC, no NCCL on the data path) -- in
             # child processes with their own rendezvous, so a failure there

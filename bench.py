@@ -477,7 +477,7 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="mapfuse", choices=["mapfuse", "reference"])
-    ap.add_argument("--n", type=int, default=N_DEFAULT)
+    ap.add_argument("--n", "--elements", dest="n", type=int, default=N_DEFAULT)
     ap.add_argument("--no-suite", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-sharded", action="store_true",
@@ -589,7 +589,7 @@ def main():
         # (strong scaling; T(1) at N = 1), column partials all-reduced by NCCL
         import copy
         sa = copy.copy(args)
-        sa.n_matrix, sa.collective, sa.mode = 131072, "nccl", "fused"
+        sa.collective, sa.mode = "nccl", "fused"  # n_matrix: 131072 unless --n-matrix
         sa.steps, sa.warmup = max(5, min(args.steps, 20)), 3
         try:
             r = run_sharded(sa, torch, mf, rank, world, "BICGK")

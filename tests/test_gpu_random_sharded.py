@@ -21,9 +21,10 @@ pytestmark = pytest.mark.gpu
 SEEDS = range(int(os.environ.get("MF_RANDOM_SHARDED_SEEDS", "24")))
 
 
+@pytest.mark.parametrize("mode", ["fused", "b200"])
 @pytest.mark.parametrize("P", [2, 3])
 @pytest.mark.parametrize("seed", SEEDS)
-def test_random_script_row_sharded(seed, P):
+def test_random_script_row_sharded(seed, P, mode):
     import torch
     import paper_1305_1183_b200 as mf
     from paper_1305_1183_b200.sharding import ShardedPlan
@@ -31,7 +32,7 @@ def test_random_script_row_sharded(seed, P):
     rng = np.random.default_rng(1000 + seed)
     text, calls, returns = make_script(rng, 3 + seed % 5)
     m, n = 192 + 32 * (seed % 3), 128 + 64 * (seed % 4)
-    sps = [ShardedPlan(script=text, rows=m, cols=n, mode="fused", world=P, rank=r, collective="nccl")
+    sps = [ShardedPlan(script=text, rows=m, cols=n, mode=mode, world=P, rank=r, collective="nccl")
            for r in range(P)]
     gd = sps[0].global_desc
     env = {"k": 0.625}
@@ -86,8 +87,9 @@ def test_random_script_row_sharded(seed, P):
         assert np.all(err <= lim), (text, name, float(np.max(err / np.maximum(lim, 1e-300))))
 
 
+@pytest.mark.parametrize("mode", ["fused", "b200"])
 @pytest.mark.parametrize("seed", SEEDS)
-def test_random_script_peers_in_kernel(seed):
+def test_random_script_peers_in_kernel(seed, mode):
     """The same random scripts through mf_launch_peers: two virtual ranks on
     their own streams, every cross-rank sum done inside the kernels over the
     peer buffers (the CUDA-IPC / NVLink code path).  Plans whose generic
@@ -100,7 +102,7 @@ def test_random_script_peers_in_kernel(seed):
     rng = np.random.default_rng(5000 + seed)
     text, calls, returns = make_script(rng, 3 + seed % 5)
     m, n = 192 + 64 * (seed % 3), 128 + 64 * (seed % 4)
-    sps = [ShardedPlan(script=text, rows=m, cols=n, mode="fused", world=P, rank=r, collective="nccl")
+    sps = [ShardedPlan(script=text, rows=m, cols=n, mode=mode, world=P, rank=r, collective="nccl")
            for r in range(P)]
     for k, kd in enumerate(sps[0].desc["kernels"]):
         if kd["kind"] == "generic" and sps[0].collective_after[k]:

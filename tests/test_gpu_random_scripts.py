@@ -92,6 +92,7 @@ MODES = os.environ.get("MF_RANDOM_MODES", "fused").split(",")
 BIG = os.environ.get("MF_RANDOM_BIG", "0") == "1"
 TINY = os.environ.get("MF_RANDOM_TINY", "0") == "1"
 RANDOM_OPTIONS = os.environ.get("MF_RANDOM_OPTIONS", "0") == "1"
+LONG = int(os.environ.get("MF_RANDOM_LONG", "0"))  # > 0: scripts of LONG..LONG+5 calls
 
 
 @pytest.mark.parametrize("mode", MODES)
@@ -101,7 +102,7 @@ def test_random_script(seed, mode):
     import paper_1305_1183_b200 as mf
     co = COracle()
     rng = np.random.default_rng(seed)
-    text, calls, returns = make_script(rng, 3 + seed % 5)
+    text, calls, returns = make_script(rng, (LONG + seed % 6) if LONG else 3 + seed % 5)
     m, n = 96 + 32 * (seed % 3), 128 + 64 * (seed % 4)
     if BIG:  # several column chunks and row bands per matrix kernel, ragged edges
         m, n = 1024 + 160 * (seed % 7), 2048 + 96 * (seed % 11)

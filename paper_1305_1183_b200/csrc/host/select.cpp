@@ -5,7 +5,7 @@
 // micro-benchmarks.  On B200 every kernel here is
 // HBM-bound (<= 1 flop/byte), so t = bytes / (eta * BW) + t_launch with BW
 // the measured copy bandwidth and eta the per-family efficiency measured on
-// B200 (bench.py suite, profiles/r01_variants.txt) -- the analogue of the
+// B200 (bench.py suite, profiles/r01_sweep_initial.txt, r01_stream_layout.txt) -- the analogue of the
 // paper's per-architecture benchmark database.  Modelling launch overhead
 // fixes the paper's own AXPYDOT misprediction.
 #include <algorithm>

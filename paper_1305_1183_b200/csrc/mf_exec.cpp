@@ -355,7 +355,7 @@ void run_matrix(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc, 
   // shapes that stream a matrix back out (ger2's B) or carry the rank-2
   // update need the deep TMA ring to keep enough bytes in flight; read-only
   // reduction shapes reach roofline from registers alone (measured on B200,
-  // profiles/r01_variants.txt).  tma = -1 auto, 0 register-fed, 1 TMA.
+  // profiles/r01_sweep_initial.txt, r01_matrix_layout.txt).  tma = -1 auto, 0 register-fed, 1 TMA.
   const bool heavy = sh.nrank > 0 || sh.store;
   if (eo.tma < 0 && k.variant_tma >= 0) {  // the cost model's choice
     t.tma = k.variant_tma == 1;

@@ -1,37 +1,47 @@
 #!/usr/bin/env python
 """bench.py -- fused-sequence effective GB/s on B200 (BASELINE.json metric).
 
-Default workload (BASELINE.json configs[1]): the BLAS-1 chains at
+N = 1 (default workload, BASELINE.json configs[1]): the BLAS-1 chains at
 n = 2^28 fp32 -- VADD (x = w + y + z) and WAXPBY (w = alpha x + beta y) --
 each compiled by the planner into ONE fused sm_100a kernel.  A step is one
 pass of both fused sequences over resident synthetic inputs (device-side
 counter-based generator; inputs 4 GiB and 3 GiB, far larger than the 126 MB
 L2, so no flush is needed between steps).
 
+N > 1 (torchrun; default workload "auto" -> bicgk-sharded): BASELINE.json
+configs[4], BiCGK 131072^2 row-sharded over the N ranks -- strong scaling,
+the north star's multi-GPU path.  Every rank runs the planner's fused kernel
+on its row panel; the column partials A^T r are all-reduced (NCCL) after the
+kernel.  Rank 0 first times the whole problem alone on its GPU (T(1)), so
+the line carries t1_ms, tN_ms and efficiency = T(1) / (N T(N)).
+
   value            algorithmic bytes of the step (every input read once, every
                    output written once) / device time  [GB/s, whole job]
-  e2e              same metric through the C-ABI host entry point
-                   (mf_launch_host): pinned host inputs copied H2D, kernels,
-                   outputs copied D2H, every step inside the timed region
-  roofline         dominant kernel (fused VADD): achieved GB/s vs the measured
-                   HBM copy bandwidth in MEASURED_PEAKS.json
+  e2e              same metric through the public API with host buffers:
+                   N = 1 the C-ABI host entry point mf_launch_host (pinned host
+                   inputs copied H2D, kernels, outputs copied D2H); N > 1 the
+                   row panels copied H2D from pinned host memory, the sharded
+                   plan, the outputs copied D2H -- every step timed
+  roofline         dominant kernel: achieved GB/s vs the measured HBM copy
+                   bandwidth in MEASURED_PEAKS.json
   cpu_baseline     the reference's own CPU oracle (oracle/_ref, compiled from
-                   /root/reference/proj/src) on a bounded sample, all host cores
+                   /root/reference/proj/src) on a bounded sample, all host
+                   cores, plus the serial code's 1-core figure
   speedup_vs_unfused  same step as one kernel per elementary call
   suite            the other BASELINE configs (AXPYDOT 2^24, BiCGK/ATAX 16384^2,
                    GEMVER/GESUMMV 32768^2), fused vs unfused, for context
-  sharded          BASELINE configs[4]: BiCGK 131072^2 row-sharded over the N
-                   ranks (strong scaling, NCCL all-reduce of A^T r); at N = 1
-                   it is T(1) for the efficiency T(1)/(N T(N)); at N > 1 also
-                   `fused_collective`: the same leg with A^T r reduced inside
-                   the kernel over NVLink peer memory (child processes)
+  sharded          N = 1: BiCGK 131072^2 through the sharding layer on one GPU
+                   (T(1) of the strong-scaling line), with a sampled fp64 parity
+                   check
+  parity           sampled rows / columns of the sharded outputs re-derived in
+                   fp64 on the CPU from the counter-based generator
 
-Multi-GPU (torchrun): every rank runs the workload on its own GPU on its own
-slice (element-wise sequences shard with no exchange; "scaling": "weak");
-time = max over ranks of the device-timed region.
-
---impl reference: rank 0 times the reference's CPU implementation
-(reference_execute from oracle/_ref) on the same workload and metric.
+--workload bicgk-sharded | atax-sharded | gemver-sharded runs that sharded
+line at any N (gemver: proj/data/scripts/gemver.mfs:8-11, one all-reduce of
+t = B^T y per step).  --impl reference: rank 0 times the reference's CPU
+implementation (reference_execute from oracle/_ref) on the same workload.
+MF_BENCH_SHARED_GPU=1: every rank on cuda:0 over gloo (a one-GPU smoke run of
+the multi-rank code path; numbers are not meaningful).
 """
 from __future__ import annotations
 
@@ -129,20 +139,6 @@ def measured_peak():
     return 6650.0, "fallback (B200_PROFILING.md, MEASURED_PEAKS.json absent)"
 
 
-def ncu_traffic(kernel_key: str):
-    """DRAM bytes per launch of the kernel whose template name contains
-    kernel_key, from the committed ncu capture (profiles/ncu_traffic.json)."""
-    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if not os.path.exists(p):
-        return None
-    with open(p) as f:
-        d = json.load(f)
-    for k, v in d.items():
-        if kernel_key in k:
-            return v.get("dram_bytes_per_launch") if isinstance(v, dict) else v
-    return None
-
-
 def host_info():
     """CPU model, logical cores and RAM of the box the CPU baseline ran on."""
     model = ""
@@ -164,38 +160,48 @@ def host_info():
 # oracle/_ref, run on independent element slices in parallel threads (ctypes
 # releases the GIL; the reference itself is serial code).
 
+def _parallel(fn, items):
+    out = [None] * len(items)
+
+    def run(i):
+        out[i] = fn(items[i])
+
+    ths = [threading.Thread(target=run, args=(i,)) for i in range(len(items))]
+    for th in ths:
+        th.start()
+    for th in ths:
+        th.join()
+    return out
+
+
 def cpu_reference(n_total: int, threads: int, reps: int, warmup: int):
+    """VADD + WAXPBY through the reference's reference_execute over
+    n_total elements split into `threads` independent slices, one thread
+    each (make_problem excluded from the timing)."""
     from oracle import RefOracle
     ref = RefOracle()
     per = max(32, (n_total // threads) // 32 * 32)
-    probs = []
-    for t in range(threads):
-        probs.append((ref.problem("VADD", 1, per, 1 + t), ref.problem("WAXPBY", 1, per, 101 + t)))
+    probs = _parallel(lambda t: (ref.problem("VADD", 1, per, 1 + t), ref.problem("WAXPBY", 1, per, 101 + t)),
+                      list(range(threads)))
 
     def one(pair):
         pair[0].L.mfr_execute(pair[0].h)
         pair[1].L.mfr_execute(pair[1].h)
 
-    def step():
-        ths = [threading.Thread(target=one, args=(p,)) for p in probs]
-        for th in ths:
-            th.start()
-        for th in ths:
-            th.join()
-
     for _ in range(warmup):
-        step()
+        _parallel(one, probs)
     times = []
     for _ in range(reps):
         t0 = time.perf_counter()
-        step()
+        _parallel(one, probs)
         times.append(time.perf_counter() - t0)
     nbytes = 28 * per * threads  # VADD 16n + WAXPBY 12n
     sec = statistics.median(times)
     return {"value": nbytes / sec / 1e9, "unit": "GB/s", "cores": threads, "kind": "reference",
             "host": host_info(),
             "sample": "reference_execute (oracle/_ref) VADD+WAXPBY on %d x %d-element slices "
-                      "(%d threads), make_problem excluded" % (threads, per, threads),
+                      "(%d threads, %d elements), make_problem excluded" % (threads, per, threads,
+                                                                           per * threads),
             "sec_per_step": sec, "elements": per * threads}
 
 
@@ -235,7 +241,6 @@ def time_kernels(torch, plans, steps, warmup, flush=None):
             flush[0].zero_()
             flush[1].sum()
         evs[e].record()
-        first = e
         for plan, bufs, sc in plans:
             for k in range(plan.num_kernels):
                 plan.launch_kernel(k, bufs, sc)
@@ -261,6 +266,22 @@ def time_kernels(torch, plans, steps, warmup, flush=None):
     return t_total, per
 
 
+def soak_steps(torch, step, seconds, world):
+    """How many untimed steps fill `seconds` (agreed over the ranks, so
+    collectives inside a step stay matched): the clock sampler's window
+    around the timed region is then >= `seconds` of the same load."""
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    step()
+    torch.cuda.synchronize()
+    n = max(1, int(seconds / max(time.perf_counter() - t0, 1e-6)))
+    if world > 1:
+        t = torch.tensor([n], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        n = int(t.item())
+    return min(n, 100000)
+
+
 def run_workload(args, torch, mf, rank, world):
     n = args.n
     sc = {"alpha": 0.5, "beta": 0.75}
@@ -270,11 +291,20 @@ def run_workload(args, torch, mf, rank, world):
         bufs, d = make_buffers(torch, mf, p, seed=1 + rank * 17 + i)
         plans.append((p, bufs, sc))
     step_bytes = sum(p.describe()["bytes_loaded"] + p.describe()["bytes_stored"] for p in fused)
+
+    def step():
+        for plan, bufs, scal in plans:
+            plan.launch(bufs, scal)
+
+    n_soak = soak_steps(torch, step, 1.5, world)
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
     gpu_index = env_rank()[1]
     with ClockSampler(gpu_index) as clk:
+        # the sampler's window: >= 1.5 s of the same load, then the timed region
+        for _ in range(n_soak):
+            step()
         total_ms, per = time_kernels(torch, plans, args.steps, args.warmup)
     if world > 1:
         t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
@@ -282,13 +312,17 @@ def run_workload(args, torch, mf, rank, world):
         total_ms = float(t.item())
     res = {"total_ms": total_ms, "step_bytes": step_bytes, "per": per, "clocks": clk.summary(),
            "launches": args.steps * sum(p.num_kernels for p in fused)}
-    # unfused chain (speedup context), same data
+    # unfused chain (speedup context), same data; bytes-saved ratio from the
+    # two plans' own algorithmic bytes
     unf = []
+    unf_bytes = 0
     for (p, bufs, _), s in zip(plans, ("VADD", "WAXPBY")):
         up = mf.Plan.sequence(s, 1, n, "unfused")
+        unf_bytes += up.describe()["bytes_loaded"] + up.describe()["bytes_stored"]
         unf.append((up, bufs, sc))
     u_ms, _ = time_kernels(torch, unf, max(2, args.steps // 2), 1)
     res["unfused_ms_per_step"] = u_ms / max(2, args.steps // 2)
+    res["bytes_saved_ratio"] = unf_bytes / step_bytes
     del plans, unf
     torch.cuda.empty_cache()
     return res
@@ -301,7 +335,6 @@ def run_e2e(args, torch, mf, steps, world=1):
     import numpy as np
     n = args.n
     sc = {"alpha": 0.5, "beta": 0.75}
-    out = []
     h2d = d2h = 0
     specs = []
     for s in ("VADD", "WAXPBY"):
@@ -340,43 +373,130 @@ def run_e2e(args, torch, mf, steps, world=1):
                     ("; all %d ranks concurrently, max time over ranks" % world if world > 1 else "")}
 
 
-def run_sharded(args, torch, mf, rank, world, seq):
-    """BiCGK / ATAX at 131072^2 row-sharded over the ranks (BASELINE configs[4]).
-    Each rank generates its row panel on the device (counter-based, global
-    row offset), runs the planner's fused kernels on it, and all-reduces the
-    column partials (NCCL) after the kernel that produced them."""
-    from paper_1305_1183_b200.sharding import ShardedPlan
-    m = n = args.n_matrix
-    sp = ShardedPlan(seq, m, n, args.mode, collective=args.collective)
+# ---------------------------------------------------------------------------
+# Row-sharded sequences (BASELINE configs[4]; GEMVER per proj/data/scripts/gemver.mfs)
+
+SHARDED_SEQ = {"bicgk-sharded": "BICGK", "atax-sharded": "ATAX", "gemver-sharded": "GEMVER"}
+SHARDED_N = {"BICGK": 131072, "ATAX": 131072, "GEMVER": 65536}
+SHARDED_SC = {"alpha": 0.625, "beta": 0.375}
+
+
+def sharded_buffers(torch, mf, sp, n):
+    """This rank's shard on the device, generated by the counter-based
+    generator at GLOBAL indices (tile element (r0 + i) * n + j, row-indexed
+    vector element r0 + k, column-indexed vector element j), so the CPU can
+    re-derive any sampled row or column.  Returns (buffers, seed per input)."""
     d = sp.desc
-    bufs = {}
+    bufs, seeds = {}, {}
     for i, b in enumerate(d["buffers"]):
         if b["role"] == "intermediate":
             continue
         shp = (b["rows"], b["cols"]) if b["rows"] > 1 else (b["cols"],)
         t = torch.empty(shp, device="cuda", dtype=torch.float32)
         if b["role"] == "input":
+            seeds[b["name"]] = 11 + i
             sl = sp.local_slice(b["name"])
-            if b["rows"] > 1:  # tile row panel: global element index (r0 + i) * n + j
+            if b["rows"] > 1:
                 mf.generate(t, seed=11 + i, row0=sp.r0, ncols_global=n)
-            elif sl is not None:  # row-indexed vector slice
+            elif sl is not None:
                 mf.runtime._check(mf.lib().mf_generate(mf.runtime.C.c_void_p(t.data_ptr()),
                                                        t.numel(), 1, 1, 11 + i, sp.r0, 1, None))
             else:
                 mf.generate(t, seed=11 + i)
+        else:
+            t.fill_(float("nan"))
         bufs[b["name"]] = t
-    local_bytes = d["bytes_loaded"] + d["bytes_stored"]
-    for _ in range(args.warmup):
-        sp.launch(bufs, {})
+    return bufs, seeds
+
+
+def sharded_parity(torch, seq, sp, bufs, seeds, m, n, rank, world, k=16):
+    """Sampled fp64 check of the sharded outputs:
+    row outputs on k of this rank's rows, replicated column outputs on k
+    columns (rank 0), against the counter-based generator's values.
+    |got - ref| <= 2^-17 S + ulp(ref) elementwise and 1e-5 normwise.
+    Returns the worst ratio over all ranks."""
+    import numpy as np
+    from oracle import COracle
+    co = COracle()
+    lr = sp.r1 - sp.r0
+    rows_l = np.sort(np.random.default_rng(1234 + rank).choice(lr, min(k, lr), replace=False))
+    rows_g = rows_l + sp.r0
+    cols = np.sort(np.random.default_rng(99).choice(n, min(k, n), replace=False))
+    g = lambda name, length: co.hash_fill(seeds[name], 0, length).astype(np.float64)
+    host = lambda name: bufs[name].cpu().numpy()
+    worst = [0.0, 0.0]  # elementwise ratio err / (tau S + ulp), normwise
+    checked = []
+    sc = SHARDED_SC
+
+    def chk(name, got, ref, S):
+        got = np.asarray(got, np.float64)
+        err = np.abs(got - ref)
+        lim = 2.0 ** -17 * S + np.spacing(np.abs(ref).astype(np.float32)).astype(np.float64)
+        worst[0] = max(worst[0], float(np.max(err / lim)) if np.all(np.isfinite(got)) else float("inf"))
+        worst[1] = max(worst[1], float(np.max(err) / max(float(np.max(np.abs(ref))), 1e-30)))
+        checked.append(name)
+
+    if seq == "BICGK":
+        qr, qa = co.hash_rows(seeds["A"], n, rows_g, g("p", n).astype(np.float32))
+        chk("q", host("q")[rows_l], qr, qa)
+        if rank == 0:
+            sr, sa = co.hash_cols(seeds["A"], n, 0, m, cols, g("r", m).astype(np.float32))
+            chk("s", host("s")[cols], sr, sa)
+    elif seq == "ATAX":
+        if rank == 0:
+            t64, tabs = co.hash_matvec_all(seeds["A"], m, n, g("x", n).astype(np.float32))
+            yr, ya = co.hash_cols_f64(seeds["A"], n, m, cols, t64, tabs)
+            chk("y", host("y")[cols], yr, ya)
+    elif seq == "GEMVER":
+        al, be = sc["alpha"], sc["beta"]
+        u1, u2, y = g("u1", m), g("u2", m), g("y", m)
+        v1, v2, z = g("v1", n), g("v2", n), g("z", n)
+        Arows = np.stack([co.hash_fill(seeds["A"], int(r) * n, n) for r in rows_g]).astype(np.float64)
+        Brows = bufs["B"][torch.from_numpy(rows_l).cuda()].cpu().numpy()
+        Bexp = (Arows + u1[rows_g, None] * v1[None, :] + u2[rows_g, None] * v2[None, :]).astype(np.float32)
+        if not np.array_equal(Brows, Bexp):  # the rank-2 update is exact (fp64, rounded once)
+            worst[0] = float("inf")
+        checked.append("B")
+        x = host("x").astype(np.float64)
+        wr = al * (Brows.astype(np.float64) @ x)
+        wa = abs(al) * (np.abs(Brows.astype(np.float64)) @ np.abs(x))
+        chk("w", host("w")[rows_l], wr, wa)
+        if rank == 0:  # x = beta B^T y + z, B = A + u1 v1^T + u2 v2^T
+            ay, aya = co.hash_cols(seeds["A"], n, 0, m, cols, y.astype(np.float32))
+            xr = be * (ay + v1[cols] * (u1 @ y) + v2[cols] * (u2 @ y)) + z[cols]
+            xa = abs(be) * (aya + np.abs(v1[cols]) * (np.abs(u1) @ np.abs(y)) +
+                            np.abs(v2[cols]) * (np.abs(u2) @ np.abs(y))) + np.abs(z[cols])
+            chk("x", host("x")[cols], xr, xa)
+    if world > 1:
+        t = torch.tensor(worst, device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        worst = [float(v) for v in t.tolist()]
+    return {"checked": checked, "rows_per_rank": int(len(rows_l)), "cols": int(len(cols)),
+            "max_err_over_tol": round(worst[0], 4), "normwise": worst[1],
+            "ok": bool(worst[0] <= 1.0 and worst[1] <= 1e-5),
+            "oracle": "oracle/mf_oracle.c counter-based generator, fp64 (tau = 2^-17, normwise 1e-5)"}
+
+
+def time_sharded(torch, sp, bufs, steps, warmup, world):
+    """Device time of `steps` sharded steps (kernels + collectives) after a
+    barrier, max over ranks; clocks sampled over a >= 1.5 s window of the
+    same load ending with the timed region."""
+    for _ in range(warmup):
+        sp.launch(bufs, SHARDED_SC)
+    n_soak = soak_steps(torch, lambda: sp.launch(bufs, SHARDED_SC), 1.5, world)
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
-    gpu_index = env_rank()[1]
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(gpu_index) as clk:
+    with ClockSampler(env_rank()[1]) as clk:
+        for _ in range(n_soak):
+            sp.launch(bufs, SHARDED_SC)
+        if world > 1:
+            torch.cuda.synchronize()
+            torch.distributed.barrier()
         start.record()
-        for _ in range(args.steps):
-            sp.launch(bufs, {})
+        for _ in range(steps):
+            sp.launch(bufs, SHARDED_SC)
         end.record()
         torch.cuda.synchronize()
     ms = start.elapsed_time(end)
@@ -384,29 +504,121 @@ def run_sharded(args, torch, mf, rank, world, seq):
         t = torch.tensor([ms], device="cuda", dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
+    return ms / steps, clk.summary()
+
+
+def run_sharded(args, torch, mf, rank, world, seq, collective="nccl", parity=True, e2e_steps=0):
+    """`seq` at n_matrix^2 row-sharded over the ranks.  Each rank generates its
+    row panel on the device (counter-based, global row offset), runs the
+    planner's fused kernels on it and reduces the column partials after the
+    kernel that produced them (NCCL all-reduce, or in-kernel over peer
+    memory with collective="fused")."""
+    from paper_1305_1183_b200.sharding import ShardedPlan
+    m = n = args.n_matrix or SHARDED_N[seq]
+    sp = ShardedPlan(seq, m, n, args.mode, collective=collective)
+    d = sp.desc
+    bufs, seeds = sharded_buffers(torch, mf, sp, n)
+    local_bytes = d["bytes_loaded"] + d["bytes_stored"]
+    ms, clocks = time_sharded(torch, sp, bufs, args.steps, args.warmup, world)
+    sp.check()  # collective="fused": a peer barrier that timed out is an error, not a number
+    if world > 1:
         tb = torch.tensor([local_bytes], device="cuda", dtype=torch.float64)
         torch.distributed.all_reduce(tb)
         total_bytes = float(tb.item())
     else:
         total_bytes = float(local_bytes)
-    return {"ms_per_step": ms / args.steps, "value": total_bytes * args.steps / (ms / 1e3) / 1e9,
-            "clocks": clk.summary(), "launches": args.steps * sp.plan.num_kernels,
-            "kernels": [k["name"] for k in d["kernels"]], "rows_per_rank": sp.r1 - sp.r0,
-            "collectives_per_step": sum(len(c) for c in sp.collective_after)}
+    out = {"ms_per_step": ms, "value": total_bytes / (ms / 1e3) / 1e9, "step_bytes": total_bytes,
+           "clocks": clocks, "launches": args.steps * sp.plan.num_kernels,
+           "kernels": [k["name"] for k in d["kernels"]], "rows_per_rank": sp.r1 - sp.r0,
+           "collectives_per_step": sum(len(c) for c in sp.collective_after), "m": m, "n": n}
+    if parity:
+        out["parity"] = sharded_parity(torch, seq, sp, bufs, seeds, m, n, rank, world)
+    if e2e_steps > 0:
+        out["e2e"] = sharded_e2e(torch, sp, bufs, e2e_steps, world, total_bytes)
+    del bufs
+    torch.cuda.empty_cache()
+    return out
 
 
-def run_fused_child(args, rank, world, steps):
-    """Every rank starts `bench.py --workload bicgk-sharded --collective fused`
+def sharded_e2e(torch, sp, bufs, steps, world, total_bytes):
+    """The sharded step through the public API (ShardedPlan.launch) with the
+    inputs in pinned host memory: every step copies this rank's shard H2D,
+    runs the kernels + collectives and copies the outputs D2H; wall time,
+    max over ranks."""
+    d = sp.desc
+    ins = [b["name"] for b in d["buffers"] if b["role"] == "input"]
+    outs = [b["name"] for b in d["buffers"] if b["role"] == "output"]
+    host = {k: torch.empty_like(bufs[k], device="cpu").pin_memory() for k in ins + outs}
+    for k in ins:
+        host[k].copy_(bufs[k])
+    h2d = sum(host[k].numel() * 4 for k in ins)
+    d2h = sum(host[k].numel() * 4 for k in outs)
+
+    def step():
+        for k in ins:
+            bufs[k].copy_(host[k], non_blocking=True)
+        sp.launch(bufs, SHARDED_SC)
+        for k in outs:
+            host[k].copy_(bufs[k], non_blocking=True)
+        torch.cuda.synchronize()
+
+    step()
+    if world > 1:
+        torch.distributed.barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        step()
+    el = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([el], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        hd = torch.tensor([h2d, d2h], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(hd)
+        el, h2d, d2h = float(t.item()), int(hd[0].item()), int(hd[1].item())
+    del host
+    return {"value": total_bytes * steps / el / 1e9, "unit": "GB/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "steps": steps,
+            "path": "ShardedPlan.launch with every rank's shard copied H2D from pinned host memory "
+                    "and the outputs copied D2H each step; wall time, max over ranks"}
+
+
+def run_t1(args, torch, mf, rank, world, seq):
+    """T(1): rank 0 runs the whole problem alone on its GPU (the other ranks
+    wait at a barrier), before any shard is allocated."""
+    res = None
+    if rank == 0:
+        import copy
+        a1 = copy.copy(args)
+        from paper_1305_1183_b200.sharding import ShardedPlan
+        m = n = args.n_matrix or SHARDED_N[seq]
+        sp = ShardedPlan(seq, m, n, args.mode, world=1, rank=0, collective="nccl")
+        bufs, _ = sharded_buffers(torch, mf, sp, n)
+        ms, _ = time_sharded(torch, sp, bufs, max(5, a1.steps), 3, 1)
+        byts = sp.desc["bytes_loaded"] + sp.desc["bytes_stored"]
+        res = {"t1_ms": ms, "t1_value": byts / (ms / 1e3) / 1e9}
+        del bufs
+        torch.cuda.empty_cache()
+    if world > 1:
+        torch.distributed.barrier()
+    return res
+
+
+def run_fused_child(args, rank, world, steps, seq):
+    """Every rank starts `bench.py --workload <seq>-sharded --collective fused`
     with its own RANK / WORLD_SIZE on another rendezvous port; rank 0 returns
-    the child's JSON summary (or the error)."""
+    the child's JSON summary (or the error).  The in-kernel peer barriers
+    time out (MF_PEER_TIMEOUT_MS, a clear error instead of a hang), and the
+    child itself is bounded by a wall-clock timeout."""
     import torch
     env = dict(os.environ)
     env["MASTER_PORT"] = str(int(env.get("MASTER_PORT", "29500")) + 17)
-    cmd = [sys.executable, os.path.abspath(__file__), "--workload", "bicgk-sharded",
-           "--collective", "fused", "--steps", str(steps), "--warmup", "3", "--gpus", str(world)]
+    env.setdefault("MF_PEER_TIMEOUT_MS", "2000")
+    cmd = [sys.executable, os.path.abspath(__file__), "--workload", seq.lower() + "-sharded",
+           "--collective", "fused", "--steps", str(steps), "--warmup", "3", "--gpus", str(world),
+           "--no-t1"]
     torch.distributed.barrier()
     try:
-        r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=150)
+        r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=240)
         out = r.stdout.strip().splitlines()
         if rank != 0:
             return None
@@ -414,7 +626,8 @@ def run_fused_child(args, rank, world, steps):
             return {"error": ("rc=%d " % r.returncode) + (r.stderr or "")[-300:]}
         d = json.loads(out[-1])
         return {"value": d["value"], "unit": d["unit"], "ms_per_step": d["ms_per_step"],
-                "frac_per_gpu": d["roofline"]["frac"], "workload": d["config"]["workload"]}
+                "frac_per_gpu": d["roofline"]["frac"], "workload": d["config"]["workload"],
+                "parity": d.get("parity")}
     except Exception as ex:
         return {"error": str(ex)[:300]} if rank == 0 else None
     finally:
@@ -471,6 +684,54 @@ def run_suite(args, torch, mf):
     return out
 
 
+def traffic_entry(kernel_key):
+    """roofline.traffic: DRAM bytes per launch of the dominant kernel from the
+    committed ncu --set full capture (profiles/ncu_traffic.json), with the
+    capture it came from -- ncu is not run inside the bench."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None, None
+    with open(p) as f:
+        d = json.load(f)
+    for k, v in d.items():
+        if kernel_key in k and isinstance(v, dict):
+            return v.get("dram_bytes_per_launch"), "profiles/ncu_traffic.json: %s (%s)" % (
+                v.get("source", "?"), v.get("captured", "round-1 capture"))
+    return None, None
+
+
+def sharded_line(args, r, t1, world, seq, collective):
+    peak, peak_kind = measured_peak()
+    line = {"metric": METRIC, "value": round(r["value"], 1), "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(r["ms_per_step"], 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": "%s fp32 %dx%d row-sharded over %d GPU(s), column partials "
+                                   "reduced %s" % (seq, r["m"], r["n"], world,
+                                                   "in-kernel over NVLink peer memory"
+                                                   if collective == "fused" else "by NCCL all-reduce"),
+                       "rows_per_rank": r["rows_per_rank"], "kernels": r["kernels"],
+                       "collectives_per_step": r["collectives_per_step"],
+                       "parallelism": "row-sharded x%d" % world,
+                       "l2": "inputs (%d GiB) >> L2; no flush" % (r["step_bytes"] // (1 << 30)),
+                       "data": "synthetic, device-side counter-based U(-1,1) generator at global indices"},
+            "roofline": {"bound": "hbm", "achieved": round(r["value"] / world, 1), "peak": peak,
+                         "unit": "GB/s", "frac": round(r["value"] / world / peak, 4),
+                         "traffic": None, "peak_source": peak_kind + " (per GPU)",
+                         "kernel": r["kernels"][0]},
+            "clocks": r["clocks"], "gpu_launches": r["launches"]}
+    if "parity" in r:
+        line["parity"] = r["parity"]
+    if t1 is not None:
+        line["strong_scaling"] = {"t1_ms": round(t1["t1_ms"], 4), "tN_ms": round(r["ms_per_step"], 4),
+                                  "n": world, "t1_value": round(t1["t1_value"], 1),
+                                  "efficiency": round(t1["t1_ms"] / (world * r["ms_per_step"]), 4),
+                                  "t1_how": "rank 0 alone on its GPU, whole problem, before the shards"}
+    if "e2e" in r:
+        line["e2e"] = r["e2e"]
+    return line
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -481,19 +742,26 @@ def main():
     ap.add_argument("--no-suite", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-sharded", action="store_true",
-                    help="skip the BiCGK 131072^2 row-sharded leg of the default workload")
+                    help="N = 1: skip the BiCGK 131072^2 sharding-layer leg")
     ap.add_argument("--no-fused-child", action="store_true",
-                    help="N > 1: skip the in-kernel (NVLink peer memory) variant of the sharded leg")
+                    help="N > 1: skip the in-kernel (NVLink peer memory) variant of the sharded line")
+    ap.add_argument("--no-t1", action="store_true", help="sharded workloads: skip the T(1) run")
     ap.add_argument("--e2e-steps", type=int, default=5)
-    ap.add_argument("--workload", default="blas1", choices=["blas1", "bicgk-sharded", "atax-sharded"])
-    ap.add_argument("--n-matrix", type=int, default=131072)
+    ap.add_argument("--workload", default="auto",
+                    choices=["auto", "blas1", "bicgk-sharded", "atax-sharded", "gemver-sharded"],
+                    help="auto: blas1 at N = 1, bicgk-sharded (strong scaling) at N > 1")
+    ap.add_argument("--n-matrix", type=int, default=0,
+                    help="sharded workloads: matrix size (0: 131072, gemver 65536)")
     ap.add_argument("--mode", default="fused", choices=["fused", "b200"],
                     help="planner mode of the sharded workloads (b200: row-resident ATAX)")
-    ap.add_argument("--collective", default="fused", choices=["fused", "nccl"],
-                    help="sharded workloads: in-kernel peer-memory reduction or NCCL all-reduce")
+    ap.add_argument("--collective", default="nccl", choices=["fused", "nccl"],
+                    help="sharded workloads: NCCL all-reduce (default) or in-kernel peer-memory reduction")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     rank, local, world = env_rank()
+    workload = args.workload
+    if workload == "auto":
+        workload = "blas1" if world == 1 else "bicgk-sharded"
     config = {"workload": WORKLOAD, "n": args.n, "dtype": "fp32", "parallelism": "dp%d" % world,
               "global_elements": args.n * world, "l2": "inputs (7 GiB/step) >> 126 MB L2; no flush",
               "data": "synthetic, device-side counter-based U(-1,1) generator"}
@@ -502,13 +770,16 @@ def main():
         if rank != 0:
             return
         threads = os.cpu_count() or 1
-        sample = 1 << 24
-        r = cpu_reference(sample, threads, args.steps, args.warmup)
+        # the stated n: every step is the whole 2^28-element workload, split
+        # into one independent slice per host thread
+        r = cpu_reference(args.n, threads, args.steps, args.warmup)
         line = {"impl": "reference", "metric": METRIC, "value": round(r["value"], 3),
                 "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": round(r["sec_per_step"] * 1e3, 3), "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": config,
+                "config": dict(config, n=r["elements"], global_elements=r["elements"],
+                               note="the reference arm always runs the N = 1 BLAS-1 workload on "
+                                    "the host cores"),
                 "cpu_baseline": {"value": round(r["value"], 3), "unit": "GB/s",
                                  "cores": r["cores"], "kind": "reference", "sample": r["sample"],
                                  "host": r["host"]},
@@ -528,27 +799,24 @@ def main():
     import paper_1305_1183_b200 as mf
     mf.lib()
 
-    if args.workload != "blas1":
-        seq = "BICGK" if args.workload.startswith("bicgk") else "ATAX"
-        r = run_sharded(args, torch, mf, rank, world, seq)
-        peak, peak_kind = measured_peak()
+    if workload != "blas1":
+        seq = SHARDED_SEQ[workload]
+        t1 = None if args.no_t1 else run_t1(args, torch, mf, rank, world, seq)
+        r = run_sharded(args, torch, mf, rank, world, seq, collective=args.collective,
+                        e2e_steps=args.e2e_steps if world > 1 else 0)
+        fused = None
+        if (world > 1 and args.collective == "nccl" and not args.no_fused_child and not SHARED_GPU
+                and args.workload == "auto"):
+            # the same line with the column reduction fused into the kernel over
+            # NVLink peer memory (CUDA IPC, no NCCL on the data path), in child
+            # processes with their own rendezvous: a failure there cannot take
+            # this line down
+            torch.cuda.empty_cache()
+            fused = run_fused_child(args, rank, world, args.steps, seq)
         if rank == 0:
-            line = {"metric": METRIC, "value": round(r["value"], 1), "unit": "GB/s", "n_gpus": world,
-                    "steps": args.steps, "warmup": args.warmup,
-                    "ms_per_step": round(r["ms_per_step"], 4), "higher_is_better": True,
-                    "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                    "config": {"workload": "%s fp32 %dx%d row-sharded over %d GPU(s), column partials "
-                                           "reduced %s" % (seq, args.n_matrix, args.n_matrix, world,
-                                                           "in-kernel over NVLink peer memory"
-                                                           if args.collective == "fused" else
-                                                           "by NCCL all-reduce"),
-                               "rows_per_rank": r["rows_per_rank"], "kernels": r["kernels"],
-                               "collectives_per_step": r["collectives_per_step"],
-                               "l2": "inputs (64 GiB) >> L2; no flush"},
-                    "roofline": {"bound": "hbm", "achieved": round(r["value"] / world, 1), "peak": peak,
-                                 "unit": "GB/s", "frac": round(r["value"] / world / peak, 4),
-                                 "traffic": None, "peak_source": peak_kind + " (per GPU)"},
-                    "clocks": r["clocks"], "gpu_launches": r["launches"]}
+            line = sharded_line(args, r, t1, world, seq, args.collective)
+            if fused is not None:
+                line["fused_collective"] = fused
             print(json.dumps(line), flush=True)
         if world > 1:
             torch.distributed.barrier()
@@ -564,9 +832,10 @@ def main():
     vadd_bytes = 16 * args.n
     peak, peak_kind = measured_peak()
     achieved = vadd_bytes / (kms / 1e3) / 1e9
+    traffic, traffic_src = traffic_entry("stream_kernel<3, 1, 0,")
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "frac_of_nominal_8000": round(achieved / 8000.0, 4),
-                "traffic": ncu_traffic("stream_kernel<3, 1, 0,"),
+                "traffic": traffic, "traffic_source": traffic_src,
                 "kernel": key[2], "peak_source": peak_kind,
                 "algorithmic_bytes_per_launch": vadd_bytes,
                 "avg_launch_us": round(kms * 1e3, 1)}
@@ -580,37 +849,29 @@ def main():
             "clocks": res["clocks"], "gpu_launches": res["launches"],
             "kernel_us": per_kernel,
             "speedup_vs_unfused": round(res["unfused_ms_per_step"] / ms_per_step, 3),
-            "bytes_saved_ratio": round((24 + 20) / 28, 3)}
+            "bytes_saved_ratio": round(res["bytes_saved_ratio"], 4)}
     e2e = run_e2e(args, torch, mf, args.e2e_steps, world)
     torch.cuda.empty_cache()
     sharded = None
-    if not args.no_sharded:
-        # BASELINE configs[4]: BiCGK 131072^2 row-sharded over the N ranks
-        # (strong scaling; T(1) at N = 1), column partials all-reduced by NCCL
+    if not args.no_sharded and world == 1:
+        # BASELINE configs[4] through the sharding layer on this one GPU: the
+        # T(1) of the strong-scaling line bench.py prints at N > 1, with the
+        # sampled fp64 parity check
         import copy
         sa = copy.copy(args)
-        sa.collective, sa.mode = "nccl", "fused"  # n_matrix: 131072 unless --n-matrix
+        sa.mode = "fused"
         sa.steps, sa.warmup = max(5, min(args.steps, 20)), 3
         try:
             r = run_sharded(sa, torch, mf, rank, world, "BICGK")
-            peak, _ = measured_peak()
-            sharded = {"workload": "BiCGK fp32 131072x131072 row-sharded over %d GPU(s), column "
-                                   "partials all-reduced by NCCL after the fused kernel" % world,
-                       "value": round(r["value"], 1), "unit": "GB/s", "ms_per_step": round(r["ms_per_step"], 4),
-                       "steps": sa.steps, "scaling": "strong", "rows_per_rank": r["rows_per_rank"],
-                       "frac_per_gpu": round(r["value"] / world / peak, 4),
-                       "collectives_per_step": r["collectives_per_step"]}
+            sharded = {"workload": "BiCGK fp32 %dx%d through the sharding layer on 1 GPU (T(1) of the "
+                                   "N > 1 strong-scaling line)" % (r["m"], r["n"]),
+                       "value": round(r["value"], 1), "unit": "GB/s",
+                       "ms_per_step": round(r["ms_per_step"], 4), "steps": sa.steps, "scaling": "strong",
+                       "rows_per_rank": r["rows_per_rank"], "frac_per_gpu": round(r["value"] / peak, 4),
+                       "collectives_per_step": r["collectives_per_step"], "parity": r["parity"]}
         except Exception as ex:  # report, keep the main line
             sharded = {"error": str(ex)[:300]}
         torch.cuda.empty_cache()
-        if world > 1 and not args.no_fused_child and not SHARED_GPU:
-            # the same leg with the column reduction fused into the kernel over
-            # NVLink peer memory (CUDA IPC, no NCCL on the data path) -- in
-            # child processes with their own rendezvous, so a failure there
-            # cannot take this line down
-            fused = run_fused_child(args, rank, world, sa.steps)
-            if sharded is not None and fused is not None:
-                sharded["fused_collective"] = fused
     if rank == 0:
         line["e2e"] = e2e
         if sharded is not None:
@@ -619,9 +880,14 @@ def main():
             line["suite"] = run_suite(args, torch, mf)
         if world == 1 and not args.no_cpu:
             try:
-                line["cpu_baseline"] = {k: v for k, v in cpu_reference(
-                    1 << 24, os.cpu_count() or 1, 3, 1).items() if k in
-                    ("value", "unit", "cores", "kind", "sample")}
+                cores = os.cpu_count() or 1
+                many = cpu_reference(1 << 24, cores, 3, 1)
+                one = cpu_reference(1 << 22, 1, 3, 1)
+                line["cpu_baseline"] = {k: v for k, v in many.items() if k in
+                                        ("value", "unit", "cores", "kind", "sample")}
+                line["cpu_baseline"]["single_core"] = {
+                    "value": one["value"], "unit": "GB/s", "cores": 1,
+                    "sample": one["sample"] + " -- the serial reference as written"}
             except Exception as e:  # oracle/_ref absent: say so
                 line["cpu_baseline"] = {"value": None, "unit": "GB/s", "cores": 0,
                                         "kind": "reference", "sample": "unavailable: %s" % e}

@@ -56,6 +56,11 @@ struct PlannerOptions {
   bool row_resident = false;
   int64_t row_resident_max_cols = 131072;
   int64_t cols = 0;  // padded problem cols (row-resident feasibility)
+  // block-capacity rule: the fusion's smallest Algorithm 1/2
+  // kernel (BY = 2, one instance, one iteration, first-fit shared plan) must
+  // fit one CTA.  B200: 227 KB opt-in shared memory, 1024 threads.
+  int64_t block_shared_bytes = 227 * 1024;
+  int max_threads_per_block = 1024;
 };
 
 std::optional<ConstraintViolation> fusibility(const std::vector<int>& nodes,

@@ -122,7 +122,11 @@ int mf_plan_kernel_text(const mf_plan* plan, int k, char* buf, int cap);
 int mf_plan_kernel_column_outputs(const mf_plan* plan, int k, char* buf, int cap);
 
 /* Launches every kernel of the plan on `stream` (a cudaStream_t; NULL = the
- * legacy default stream).  Asynchronous.  Buffers: device pointers. */
+ * legacy default stream).  Asynchronous.  Buffers: device pointers.
+ * A plan may be launched concurrently on several streams and from several
+ * threads: it keeps one device workspace (cross-CTA partials, barrier
+ * counters, unbound intermediates) per stream, so launches on different
+ * streams never share scratch; launches on one stream are ordered by it. */
 int mf_launch(const mf_plan* plan, const mf_buffer* buffers, int nbuf, const mf_scalar* scalars,
               int nscalars, void* stream, mf_stats* stats);
 
@@ -219,6 +223,13 @@ int mf_peer_group_handle(const mf_peer_group* g, void* out, int cap); /* returns
 int mf_peer_group_open(mf_peer_group* g, int peer, const void* handle, int len);
 int mf_peer_group_connect_local(mf_peer_group* g, int peer, const mf_peer_group* other);
 void mf_peer_group_destroy(mf_peer_group* g);
+/* Synchronizes `stream` and reports (MF_ERR_FAULT) whether an in-kernel peer
+ * barrier of this rank gave up waiting: a peer did not arrive within
+ * MF_PEER_TIMEOUT_MS (default 10000) ms -- a rank crashed, or the ranks
+ * issued different launch sequences.  The kernel then finished without the
+ * cross-rank sum (outputs are invalid) instead of hanging the GPU; recreate
+ * the group.  Clears the flag. */
+int mf_peer_group_check(mf_peer_group* g, void* stream);
 int mf_launch_kernel_peers(const mf_plan* plan, int k, mf_peer_group* g, const mf_buffer* buffers,
                            int nbuf, const mf_scalar* scalars, int nscalars, void* stream,
                            mf_stats* stats);

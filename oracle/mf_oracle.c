@@ -387,3 +387,101 @@ void mfo_hash_cols(uint64_t seed, int64_t n, int64_t row0, int64_t row1, const i
     }
   }
 }
+
+/* Multi-threaded helpers (pthreads; the image has no libgomp).             */
+#include <pthread.h>
+
+typedef struct {
+  void (*fn)(void* ctx, int64_t i);
+  void* ctx;
+  int64_t lo, hi, step;
+} mfo_range;
+
+static void* mfo_range_run(void* p) {
+  mfo_range* r = (mfo_range*)p;
+  for (int64_t i = r->lo; i < r->hi; i += r->step) r->fn(r->ctx, i);
+  return NULL;
+}
+
+/* fn(ctx, i) for i in [0, count), index i on thread i % nthreads. */
+static void mfo_parallel_for(int64_t count, int nthreads, void (*fn)(void*, int64_t), void* ctx) {
+  if (nthreads < 1) nthreads = 1;
+  if (nthreads > 256) nthreads = 256;
+  pthread_t th[256];
+  mfo_range rg[256];
+  for (int t = 0; t < nthreads; ++t) {
+    rg[t].fn = fn;
+    rg[t].ctx = ctx;
+    rg[t].lo = t;
+    rg[t].hi = count;
+    rg[t].step = nthreads;
+    if (t > 0) pthread_create(&th[t], NULL, mfo_range_run, &rg[t]);
+  }
+  mfo_range_run(&rg[0]);
+  for (int t = 1; t < nthreads; ++t) pthread_join(th[t], NULL);
+}
+
+static double mfo_hash_value(uint64_t hs, uint64_t index) {
+  const uint64_t h = splitmix64(index ^ hs);
+  return (double)((float)(uint32_t)(h >> 40) * (1.0f / 8388608.0f) - 1.0f);
+}
+
+/* y = A x and |A||x| for EVERY row of a hash-generated m x n matrix, fp64,   */
+/* rows interleaved over `nthreads` threads (the chained ATAX check at        */
+/* 131072^2 needs the whole intermediate t = A x).  Each */
+/* row's sum runs in column order, like mfo_hash_rows.                        */
+typedef struct {
+  uint64_t hs;
+  int64_t n;
+  const float* x;
+  double *out, *absout;
+} mfo_matvec_ctx;
+
+static void mfo_matvec_row(void* p, int64_t i) {
+  const mfo_matvec_ctx* c = (const mfo_matvec_ctx*)p;
+  double acc = 0.0, aacc = 0.0;
+  const uint64_t base = (uint64_t)i * (uint64_t)c->n;
+  for (int64_t j = 0; j < c->n; ++j) {
+    const double a = mfo_hash_value(c->hs, base + (uint64_t)j);
+    acc += a * (double)c->x[j];
+    aacc += fabs(a) * fabs((double)c->x[j]);
+  }
+  c->out[i] = acc;
+  c->absout[i] = aacc;
+}
+
+void mfo_hash_matvec_all(uint64_t seed, int64_t m, int64_t n, const float* x, double* out,
+                         double* absout, int nthreads) {
+  mfo_matvec_ctx c = {splitmix64(seed), n, x, out, absout};
+  mfo_parallel_for(m, nthreads, mfo_matvec_row, &c);
+}
+
+/* y_j = sum_i A[i][j] t_i and sum_i |A[i][j]| tabs_i for the listed columns, */
+/* i over [0, m), with fp64 row weights (t = the fp64 intermediate of a       */
+/* chained reduction, tabs its |.|-formula); columns split over threads.     */
+typedef struct {
+  uint64_t hs;
+  int64_t n, m;
+  const int64_t* cols;
+  const double *t, *tabs;
+  double *out, *absout;
+} mfo_cols_ctx;
+
+static void mfo_cols_one(void* p, int64_t k) {
+  const mfo_cols_ctx* c = (const mfo_cols_ctx*)p;
+  double acc = 0.0, aacc = 0.0;
+  for (int64_t i = 0; i < c->m; ++i) {
+    const double a = mfo_hash_value(c->hs, (uint64_t)i * (uint64_t)c->n + (uint64_t)c->cols[k]);
+    acc += a * c->t[i];
+    aacc += fabs(a) * c->tabs[i];
+  }
+  c->out[k] = acc;
+  c->absout[k] = aacc;
+}
+
+void mfo_hash_cols_f64(uint64_t seed, int64_t n, int64_t m, const int64_t* cols, int ncols,
+                       const double* t, const double* tabs, double* out, double* absout,
+                       int nthreads) {
+  mfo_cols_ctx c = {splitmix64(seed), n, m, cols, t, tabs, out, absout};
+  mfo_parallel_for(ncols, nthreads, mfo_cols_one, &c);
+}

@@ -97,6 +97,25 @@ std::optional<ConstraintViolation> fusibility(const std::vector<int>& nodes_in,
                                  "call " + std::to_string(out) +
                                      " lies on a path that leaves and re-enters the set"};
   }
+  // block capacity: even the fusion's smallest kernel must fit one block
+  CodegenParams small;
+  small.by = 2;
+  small.instances = 1;
+  small.iterations = 1;
+  small.overlap = true;
+  kernel::KernelIR k;
+  try {
+    k = generate_kernel(nodes, s, g, L, small);
+  } catch (const std::exception&) {
+    return std::nullopt;  // not expressible as one Algorithm 1/2 kernel: lowering decides
+  }
+  if (k.shared_bytes_total() > opt.block_shared_bytes || k.threads() > opt.max_threads_per_block)
+    return ConstraintViolation{"block-capacity", nodes,
+                               "smallest fused kernel needs " + std::to_string(k.shared_bytes_total()) +
+                                   " B shared memory and " + std::to_string(k.threads()) +
+                                   " threads per block (capacity " +
+                                   std::to_string(opt.block_shared_bytes) + " B, " +
+                                   std::to_string(opt.max_threads_per_block) + " threads)"};
   return std::nullopt;
 }
 

@@ -25,7 +25,21 @@ using namespace mapfuse::b200;
 
 struct mf_plan {
   NativePlan plan;
-  mutable Workspace ws;
+  // One workspace per stream: launches of one plan on different streams (or
+  // from different threads) may overlap on the device, and each needs its own
+  // grid-barrier counters, dot ticket, partials and intermediates.  Launches
+  // on one stream are ordered by the stream.  Host launches (mf_launch_host,
+  // synchronous) use `host_ws`, serialized by `host_mu`.
+  mutable std::mutex ws_mu;
+  mutable std::map<cudaStream_t, std::unique_ptr<Workspace>> per_stream;
+  mutable Workspace host_ws;
+  mutable std::mutex host_mu;
+  Workspace& ws(cudaStream_t s) const {
+    std::lock_guard<std::mutex> lk(ws_mu);
+    auto& w = per_stream[s];
+    if (!w) w = std::make_unique<Workspace>();
+    return *w;
+  }
   // implementation generator results per kernel (enumerated on first use)
   mutable std::map<int, std::vector<mapfuse::plan::FusionImplementation>> impls;
   mutable std::mutex impl_mu;
@@ -143,6 +157,36 @@ void fill_stats(const NativePlan& p, int k0, int k1, const BufMap& b, mf_stats* 
 }
 
 
+// Owned CUDA events / streams, released on every exit path (exceptions included).
+struct Events {
+  std::vector<cudaEvent_t> e;
+  explicit Events(int n) {
+    for (int i = 0; i < n; ++i) {
+      cudaEvent_t x = nullptr;
+      check_cuda(cudaEventCreate(&x), "cudaEventCreate");
+      e.push_back(x);
+    }
+  }
+  ~Events() {
+    for (auto x : e) cudaEventDestroy(x);
+  }
+  cudaEvent_t& operator[](int i) { return e[(size_t)i]; }
+};
+struct Streams {
+  std::vector<cudaStream_t> s;
+  explicit Streams(int n) {
+    for (int i = 0; i < n; ++i) {
+      cudaStream_t x = nullptr;
+      check_cuda(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking), "cudaStreamCreate");
+      s.push_back(x);
+    }
+  }
+  ~Streams() {
+    for (auto x : s) cudaStreamDestroy(x);
+  }
+  cudaStream_t operator[](int i) const { return s[(size_t)i]; }
+};
+
 // Element-wise plans (only stream kernels, no cross-element reduction, every
 // buffer the same length) over PINNED host memory are executed as a
 // chunked pipeline: chunk c's H2D copy, kernels and D2H copy are ordered on
@@ -172,14 +216,11 @@ double launch_host_pipelined(const mf_plan* plan, const mf_buffer* hb, int nbuf,
   const NativePlan& P = plan->plan;
   const int64_t len = (int64_t)hb[0].rows * hb[0].cols;
   const int64_t chunk = std::max<int64_t>(32, (int64_t)(16 << 20) / 32 * 32);  // 64 MB per buffer
-  BufMap full = complete_bindings(P, dev, plan->ws);
+  BufMap full = complete_bindings(P, dev, plan->host_ws);
   constexpr int kStreams = 3;
-  cudaStream_t st[kStreams];
-  for (auto& x : st) check_cuda(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking), "stream");
-  cudaEvent_t start, stop, done[kStreams];
-  check_cuda(cudaEventCreate(&start), "event");
-  check_cuda(cudaEventCreate(&stop), "event");
-  for (auto& e : done) check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+  Streams st(kStreams);
+  Events ev(2 + kStreams);  // start, stop, done[i]
+  cudaEvent_t start = ev[0], stop = ev[1], *done = &ev[2];
   check_cuda(cudaEventRecord(start, st[0]), "event");
   for (int i = 1; i < kStreams; ++i) check_cuda(cudaStreamWaitEvent(st[i], start, 0), "wait");
   int c = 0;
@@ -201,7 +242,7 @@ double launch_host_pipelined(const mf_plan* plan, const mf_buffer* hb, int nbuf,
                                  cudaMemcpyHostToDevice, q),
                  "H2D");
     }
-    for (int k = 0; k < (int)P.kernels.size(); ++k) run_kernel(P, k, part, s, q, plan->ws);
+    for (int k = 0; k < (int)P.kernels.size(); ++k) run_kernel(P, k, part, s, q, plan->host_ws);
     for (int i = 0; i < nbuf; ++i) {
       const BufferSpec* spec = P.find(hb[i].name);
       if (spec && spec->role == Role::Input) continue;
@@ -218,10 +259,6 @@ double launch_host_pipelined(const mf_plan* plan, const mf_buffer* hb, int nbuf,
   check_cuda(cudaEventSynchronize(stop), "sync");
   float ms = 0.f;
   cudaEventElapsedTime(&ms, start, stop);
-  cudaEventDestroy(start);
-  cudaEventDestroy(stop);
-  for (auto& e : done) cudaEventDestroy(e);
-  for (auto& x : st) cudaStreamDestroy(x);
   return ms;
 }
 
@@ -379,10 +416,11 @@ int mf_launch(const mf_plan* plan, const mf_buffer* buffers, int nbuf, const mf_
               int nscalars, void* stream, mf_stats* stats) {
   return guarded([&] {
     if (!plan) throw Invalid("null plan");
-    BufMap b = complete_bindings(plan->plan, to_map(buffers, nbuf), plan->ws);
-    ScalarMap s = to_scalars(scalars, nscalars);
     auto st = static_cast<cudaStream_t>(stream);
-    for (int k = 0; k < (int)plan->plan.kernels.size(); ++k) run_kernel(plan->plan, k, b, s, st, plan->ws);
+    Workspace& ws = plan->ws(st);
+    BufMap b = complete_bindings(plan->plan, to_map(buffers, nbuf), ws);
+    ScalarMap s = to_scalars(scalars, nscalars);
+    for (int k = 0; k < (int)plan->plan.kernels.size(); ++k) run_kernel(plan->plan, k, b, s, st, ws);
     fill_stats(plan->plan, 0, (int)plan->plan.kernels.size(), b, stats);
   });
 }
@@ -391,9 +429,10 @@ int mf_launch_kernel(const mf_plan* plan, int k, const mf_buffer* buffers, int n
                      const mf_scalar* scalars, int nscalars, void* stream, mf_stats* stats) {
   return guarded([&] {
     if (!plan) throw Invalid("null plan");
-    BufMap b = complete_bindings(plan->plan, to_map(buffers, nbuf), plan->ws);
-    run_kernel(plan->plan, k, b, to_scalars(scalars, nscalars), static_cast<cudaStream_t>(stream),
-               plan->ws);
+    auto st = static_cast<cudaStream_t>(stream);
+    Workspace& ws = plan->ws(st);
+    BufMap b = complete_bindings(plan->plan, to_map(buffers, nbuf), ws);
+    run_kernel(plan->plan, k, b, to_scalars(scalars, nscalars), st, ws);
     fill_stats(plan->plan, k, k + 1, b, stats);
   });
 }
@@ -626,7 +665,8 @@ int mf_plan_set_implementation(mf_plan* plan, int k, int index) {
 int mf_plan_check(const mf_plan* plan, void* stream) {
   return guarded([&] {
     if (!plan) throw Invalid("null plan");
-    check_jit_faults(plan->ws, static_cast<cudaStream_t>(stream));
+    auto st = static_cast<cudaStream_t>(stream);
+    check_jit_faults(plan->ws(st), st);
   });
 }
 
@@ -635,6 +675,8 @@ int mf_launch_host(const mf_plan* plan, const mf_buffer* host_buffers, int nbuf,
   return guarded([&] {
     if (!plan) throw Invalid("null plan");
     const NativePlan& P = plan->plan;
+    std::lock_guard<std::mutex> host_lock(plan->host_mu);  // one host launch of a plan at a time
+    Workspace& ws = plan->host_ws;
     BufMap dev;
     for (int i = 0; i < nbuf; ++i) {
       const mf_buffer& h = host_buffers[i];
@@ -642,7 +684,10 @@ int mf_launch_host(const mf_plan* plan, const mf_buffer* host_buffers, int nbuf,
       DevBuf d;
       d.rows = h.rows;
       d.cols = h.cols;
-      d.ptr = plan->ws.named(std::string("__host__") + h.name, (int64_t)h.rows * h.cols);
+      {
+        std::lock_guard<std::mutex> lk(ws.mu);
+        d.ptr = ws.named(std::string("__host__") + h.name, (int64_t)h.rows * h.cols);
+      }
       dev[h.name] = d;
     }
     ScalarMap s = to_scalars(scalars, nscalars);
@@ -661,13 +706,11 @@ int mf_launch_host(const mf_plan* plan, const mf_buffer* host_buffers, int nbuf,
                                  cudaMemcpyHostToDevice, st),
                  "cudaMemcpy H2D");
     }
-    BufMap b = complete_bindings(P, dev, plan->ws);
-    cudaEvent_t e0, e1;
-    check_cuda(cudaEventCreate(&e0), "cudaEventCreate");
-    check_cuda(cudaEventCreate(&e1), "cudaEventCreate");
-    check_cuda(cudaEventRecord(e0, st), "cudaEventRecord");
-    for (int k = 0; k < (int)P.kernels.size(); ++k) run_kernel(P, k, b, s, st, plan->ws);
-    check_cuda(cudaEventRecord(e1, st), "cudaEventRecord");
+    BufMap b = complete_bindings(P, dev, ws);
+    Events ev(2);  // destroyed on every exit path
+    check_cuda(cudaEventRecord(ev[0], st), "cudaEventRecord");
+    for (int k = 0; k < (int)P.kernels.size(); ++k) run_kernel(P, k, b, s, st, ws);
+    check_cuda(cudaEventRecord(ev[1], st), "cudaEventRecord");
     for (int i = 0; i < nbuf; ++i) {
       const mf_buffer& h = host_buffers[i];
       const BufferSpec* spec = P.find(h.name);
@@ -677,11 +720,9 @@ int mf_launch_host(const mf_plan* plan, const mf_buffer* host_buffers, int nbuf,
                  "cudaMemcpy D2H");
     }
     check_cuda(cudaStreamSynchronize(st), "cudaStreamSynchronize");
-    check_jit_faults(plan->ws, st);
+    check_jit_faults(ws, st);
     float ms = 0.f;
-    cudaEventElapsedTime(&ms, e0, e1);
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
+    cudaEventElapsedTime(&ms, ev[0], ev[1]);
     fill_stats(P, 0, (int)P.kernels.size(), b, stats);
     if (stats) stats->ms = ms;
   });
@@ -752,14 +793,33 @@ int mf_peer_group_connect_local(mf_peer_group* gp, int peer, const mf_peer_group
 
 void mf_peer_group_destroy(mf_peer_group* g) { delete g; }
 
+int mf_peer_group_check(mf_peer_group* gp, void* stream) {
+  return guarded([&] {
+    if (!gp) throw Invalid("null peer group");
+    auto st = static_cast<cudaStream_t>(stream);
+    unsigned word = 0;
+    PeerGroup& g = gp->g;
+    check_cuda(cudaMemcpyAsync(&word, g.flags + kPeerErrorWord, sizeof word, cudaMemcpyDeviceToHost, st),
+               "read peer error word");
+    check_cuda(cudaStreamSynchronize(st), "peer group check");
+    if (word == 0) return;
+    check_cuda(cudaMemsetAsync(g.flags + kPeerErrorWord, 0, sizeof word, st), "clear peer error word");
+    check_cuda(cudaStreamSynchronize(st), "peer group check");
+    throw Fault("in-kernel peer barrier " + std::to_string(word - 1) + " of rank " + std::to_string(g.rank) +
+                " timed out: a peer did not arrive within MF_PEER_TIMEOUT_MS (a rank failed or the ranks "
+                "launched different kernels); the cross-rank sums of that launch are invalid");
+  });
+}
+
 int mf_launch_kernel_peers(const mf_plan* plan, int k, mf_peer_group* g, const mf_buffer* buffers,
                            int nbuf, const mf_scalar* scalars, int nscalars, void* stream,
                            mf_stats* stats) {
   return guarded([&] {
     if (!plan) throw Invalid("null plan");
-    BufMap b = complete_bindings(plan->plan, to_map(buffers, nbuf), plan->ws);
-    run_kernel(plan->plan, k, b, to_scalars(scalars, nscalars), static_cast<cudaStream_t>(stream),
-               plan->ws, g ? &g->g : nullptr);
+    auto st = static_cast<cudaStream_t>(stream);
+    Workspace& ws = plan->ws(st);
+    BufMap b = complete_bindings(plan->plan, to_map(buffers, nbuf), ws);
+    run_kernel(plan->plan, k, b, to_scalars(scalars, nscalars), st, ws, g ? &g->g : nullptr);
     fill_stats(plan->plan, k, k + 1, b, stats);
   });
 }
@@ -775,10 +835,11 @@ int mf_launch_peers(const mf_plan* plan, mf_peer_group* g, const mf_buffer* buff
         throw Invalid("kernel " + k.name +
                       ": generic kernels reduce across ranks with a host collective "
                       "(mf_launch_kernel + all-reduce of mf_plan_kernel_column_outputs)");
-    BufMap b = complete_bindings(P, to_map(buffers, nbuf), plan->ws);
+    auto st = static_cast<cudaStream_t>(stream);
+    Workspace& ws = plan->ws(st);
+    BufMap b = complete_bindings(P, to_map(buffers, nbuf), ws);
     const ScalarMap s = to_scalars(scalars, nscalars);
-    for (int k = 0; k < (int)P.kernels.size(); ++k)
-      run_kernel(P, k, b, s, static_cast<cudaStream_t>(stream), plan->ws, &g->g);
+    for (int k = 0; k < (int)P.kernels.size(); ++k) run_kernel(P, k, b, s, st, ws, &g->g);
     fill_stats(P, 0, (int)P.kernels.size(), b, stats);
   });
 }
@@ -811,12 +872,14 @@ int mf_launch_sharded(const mf_plan* const* plans, int ngpus, const int* devices
     std::vector<BufMap> b(ngpus);
     for (int g = 0; g < ngpus; ++g) {
       check_cuda(cudaSetDevice(devices[g]), "cudaSetDevice");
-      b[g] = complete_bindings(plans[g]->plan, to_map(per_gpu[g], nbuf[g]), plans[g]->ws);
+      b[g] = complete_bindings(plans[g]->plan, to_map(per_gpu[g], nbuf[g]),
+                               plans[g]->ws(static_cast<cudaStream_t>(streams[g])));
     }
     for (int k = 0; k < nk; ++k) {
       for (int g = 0; g < ngpus; ++g) {
         check_cuda(cudaSetDevice(devices[g]), "cudaSetDevice");
-        run_kernel(plans[g]->plan, k, b[g], s, static_cast<cudaStream_t>(streams[g]), plans[g]->ws);
+        auto st = static_cast<cudaStream_t>(streams[g]);
+        run_kernel(plans[g]->plan, k, b[g], s, st, plans[g]->ws(st));
       }
       // partial column sums / dots of kernel k, summed over the GPUs before
       // any later kernel reads them (the only exchange in a Table-1 plan)

@@ -208,16 +208,30 @@ __device__ __forceinline__ void finalize(const MatrixArgs& a, int tid, int nthre
 // Phase C: after a second barrier, every rank pulls the other slices from the
 //          owners' outboxes into its y.  Traffic per rank = 2(P-1)/P * n
 //          floats, the ring all-reduce volume, with no extra kernel launch.
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Bounded wait: a peer that never arrives (a rank that crashed or launched a
+// different kernel) makes the barrier give up after timeout_ns of wall time,
+// raise the group's error word and let the kernel finish -- the host gets a
+// clear error from mf_peer_group_check instead of a hung GPU or a trap that
+// poisons the context.
 __device__ __forceinline__ void peer_signal_wait(const PeerLinks& pl, int which) {
   // one thread of block 0, after a grid barrier: all CTAs' writes are done
   __threadfence_system();
   for (int s = 0; s < pl.nranks; ++s) atomicAdd_system(pl.flags[s] + which, 1u);
   const unsigned target = pl.epoch * (unsigned)pl.nranks;
-  const long long t0 = clock64();
+  const unsigned long long t0 = global_ns();
   volatile unsigned* mine = pl.flags[pl.rank] + which;
   while (*mine < target) {
     __nanosleep(128);
-    if (pl.spin_limit > 0 && clock64() - t0 > pl.spin_limit) __trap();  // never hang the GPU
+    if (pl.timeout_ns > 0 && (long long)(global_ns() - t0) > pl.timeout_ns) {
+      atomicExch_system(pl.flags[pl.rank] + kPeerErrorWord, 1u + (unsigned)which);
+      break;
+    }
   }
   __threadfence_system();
 }

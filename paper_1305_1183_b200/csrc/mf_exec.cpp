@@ -64,18 +64,20 @@ int device_sm_count() {
 // ---------------------------------------------------------------------------
 Workspace::~Workspace() {
   // Best effort: the process may be tearing down the CUDA context already.
+  for (void* p : retired_) cudaFree(p);
   if (scratch_) cudaFree(scratch_);
   if (counters_) cudaFree(counters_);
   if (jit_fault_) cudaFree(jit_fault_);
   for (auto& [k, v] : named_) cudaFree(v.first);
 }
 
-void* Workspace::scratch(size_t bytes, cudaStream_t s) {
+// Growing never frees the old buffer: launches already enqueued (or recorded
+// by a bound plan / captured into a graph) keep the pointer they were given,
+// so it stays valid until the workspace dies.  Doubling bounds the retired
+// total below the live buffer's size.
+void* Workspace::scratch(size_t bytes, cudaStream_t) {
   if (bytes <= scratch_bytes_) return scratch_;
-  if (scratch_) {
-    check_cuda(cudaStreamSynchronize(s), "workspace resize sync");
-    check_cuda(cudaFree(scratch_), "cudaFree");
-  }
+  if (scratch_) retired_.push_back(scratch_);
   size_t want = std::max(bytes, scratch_bytes_ * 2);
   check_cuda(cudaMalloc(&scratch_, want), "cudaMalloc(workspace)");
   scratch_bytes_ = want;
@@ -101,9 +103,8 @@ unsigned* Workspace::jit_fault(cudaStream_t s) {
 float* Workspace::named(const std::string& key, int64_t words) {
   auto it = named_.find(key);
   if (it != named_.end() && it->second.second >= words) return it->second.first;
-  if (it != named_.end()) {
-    check_cuda(cudaDeviceSynchronize(), "named resize sync");
-    cudaFree(it->second.first);
+  if (it != named_.end()) {  // retired, not freed (see scratch())
+    retired_.push_back(it->second.first);
     named_.erase(it);
   }
   float* p = nullptr;
@@ -160,6 +161,16 @@ void emit(Recorder* rec, const std::string& what, std::function<cudaError_t(cuda
 template <typename Args>
 void fill_peers(Args& a, PeerGroup* peers, int64_t n, const std::string& kname);
 
+// MF_PEER_TIMEOUT_MS (default 10000): how long an in-kernel peer barrier
+// waits for the other ranks before it gives up and flags the group.
+long long peer_timeout_ms() {
+  static const long long v = [] {
+    const char* e = std::getenv("MF_PEER_TIMEOUT_MS");
+    return e ? std::max(1LL, std::atoll(e)) : 10000LL;
+  }();
+  return v;
+}
+
 void run_stream(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc, cudaStream_t s,
                 Workspace& ws, Recorder* rec, PeerGroup* peers = nullptr) {
   const StreamOp& op = k.stream;
@@ -195,9 +206,13 @@ void run_stream(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc, 
     }
     a.part = static_cast<double*>(ws.scratch(sizeof(double) * (size_t)grid, s));
     a.ticket = ws.counters(s) + 2;
-    fill_peers(a, peers, 1, k.name);  // dot partials reduced across ranks in-kernel
+    // dot partials reduced across ranks in-kernel; an empty shard still
+    // launches (its partial is 0) so every rank arrives at the peer barrier
+    // and the group's epochs stay in step
+    fill_peers(a, peers, 1, k.name);
   }
-  if (n == 0) {  // an empty dot is 0 (the reference sums nothing into a zeroed output)
+  if (n == 0 && !(op.has_dot && a.peer.nranks > 1)) {
+    // an empty dot is 0 (the reference sums nothing into a zeroed output)
     if (op.has_dot) {
       float* r = a.r;
       emit(rec, "zero " + k.name, [=](cudaStream_t st) { return cudaMemsetAsync(r, 0, sizeof(float), st); },
@@ -226,7 +241,7 @@ void fill_peers(Args& a, PeerGroup* peers, int64_t n, const std::string& kname) 
     a.peer.flags[r] = peers->peer_flags[r];
   }
   a.peer.epoch = ++peers->epoch;
-  a.peer.spin_limit = 20000000000LL;  // ~10 s: trap instead of hanging the GPU
+  a.peer.timeout_ns = peer_timeout_ms() * 1000000LL;  // bounded peer barriers
 }
 
 // An empty matrix (m or n = 0): every reduction over the empty dimension is 0.
@@ -251,7 +266,9 @@ void run_rowres(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc, 
   if (n > rowres_cluster_max_cols())
     throw Fault("kernel " + k.name + ": row-resident chain needs n <= " +
                 std::to_string(rowres_cluster_max_cols()) + " (got " + std::to_string(n) + ")");
-  if (n % 4) throw Fault("kernel " + k.name + ": matrix dims must be padded");
+  if (m % 32 || n % 32)
+    throw Fault("kernel " + k.name + ": matrix dims must be padded to multiples of 32 (got " +
+                std::to_string(m) + "x" + std::to_string(n) + ")");
   MatrixArgs a;
   a.m = m;
   a.n = n;
@@ -304,7 +321,12 @@ void run_matrix(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc, 
     throw Invalid("kernel " + k.name + ": no sm_100a template for this matrix fusion shape");
   const DevBuf& M0 = need(bufs, op.mats[0], k.name);
   const int64_t m = M0.rows, n = M0.cols;
-  if (m % 4 || n % 4) throw Fault("kernel " + k.name + ": matrix dims must be padded");
+  // the cross-CTA finalize maps 8-lane groups onto float4 slots and assumes
+  // whole 32-column groups (the reference pads every buffer to 32,
+  // proj/include/mapfuse/blas.hpp:29-30)
+  if (m % 32 || n % 32)
+    throw Fault("kernel " + k.name + ": matrix dims must be padded to multiples of 32 (got " +
+                std::to_string(m) + "x" + std::to_string(n) + ")");
   MatrixArgs a;
   a.m = m;
   a.n = n;

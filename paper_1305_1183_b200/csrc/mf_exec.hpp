@@ -89,6 +89,7 @@ class Workspace {
   unsigned* counters_ = nullptr;
   unsigned* jit_fault_ = nullptr;
   std::map<std::string, std::pair<float*, int64_t>> named_;
+  std::vector<void*> retired_;  // outgrown buffers, freed with the workspace
 };
 
 // A prepared launch: replays one kernel (all host-side work done) on a stream.

@@ -22,6 +22,9 @@ constexpr int kStreamMaxOut = 2;
 // arrival counters; peers' copies are mapped into this process (CUDA IPC over
 // NVLink, or plain pointers for virtual ranks sharing one GPU).
 constexpr int kMaxRanks = 8;
+// flags[rank][kPeerErrorWord]: set by a peer barrier that timed out (a peer
+// never arrived); mf_peer_group_check reports and clears it.
+constexpr int kPeerErrorWord = 62;
 struct PeerLinks {
   int nranks = 1, rank = 0;
   float* inbox[kMaxRanks] = {};
@@ -29,7 +32,7 @@ struct PeerLinks {
   unsigned* flags[kMaxRanks] = {};
   unsigned epoch = 0;               // launches so far in this group (1-based)
   long long n_cap = 0;              // inbox / outbox row capacity (floats)
-  long long spin_limit = 0;         // clock64 cycles before trapping (deadlock guard)
+  long long timeout_ns = 0;         // peer barrier wait bound (globaltimer ns); 0 = unbounded
 };
 
 struct StreamArgs {

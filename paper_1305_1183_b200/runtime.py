@@ -70,7 +70,7 @@ EXPORTS = [
     "mf_plan_check", "mf_vm_launch", "mf_measure_routine", "mf_plan_bind", "mf_bound_launch",
     "mf_bound_graph_launch", "mf_bound_destroy", "mf_plan_count_implementations",
     "mf_plan_implementation", "mf_plan_set_implementation", "mf_launch_peers",
-    "mf_count_implementation_space",
+    "mf_count_implementation_space", "mf_peer_group_check",
 ]
 
 
@@ -109,6 +109,7 @@ def lib() -> C.CDLL:
         L.mf_peer_group_open.argtypes = [C.c_void_p, C.c_int, C.c_char_p, C.c_int]
         L.mf_peer_group_connect_local.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
         L.mf_peer_group_destroy.argtypes = [C.c_void_p]
+        L.mf_peer_group_check.argtypes = [C.c_void_p, C.c_void_p]
         L.mf_launch_kernel_peers.argtypes = [C.c_void_p, C.c_int, C.c_void_p, P(MfBuffer), C.c_int,
                                              P(MfScalar), C.c_int, C.c_void_p, P(MfStats)]
         L.mf_compile_ranked.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_int,
@@ -433,6 +434,11 @@ class PeerGroup:
 
     def connect_local(self, peer: int, other: "PeerGroup") -> None:
         _check(lib().mf_peer_group_connect_local(self.h, peer, other.h))
+
+    def check(self, stream=None) -> None:
+        """Synchronizes and raises VmFault if an in-kernel peer barrier of
+        this rank timed out (MF_PEER_TIMEOUT_MS) since the last check."""
+        _check(lib().mf_peer_group_check(self.h, C.c_void_p(_stream_ptr(stream))))
 
 
 def generate(t, seed: int, row0: int = 0, ncols_global: Optional[int] = None, stream=None) -> None:

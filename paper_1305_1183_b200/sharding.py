@@ -151,6 +151,12 @@ class ShardedPlan:
         import torch.distributed as dist
         dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
 
+    def check(self, stream=None) -> None:
+        """Raises VmFault if an in-kernel peer barrier of this rank timed out
+        (collective="fused"; a no-op otherwise)."""
+        if self.peers is not None and self.executor is None:
+            self.peers.check(stream)
+
     def launch(self, buffers: Mapping[str, object], scalars: Mapping[str, float] = {},
                stream=None) -> Dict[str, int]:
         """Runs every kernel on the local shard; all-reduces partial column /

@@ -72,6 +72,40 @@ TEST_CASE("fusibility rule ids") {
   CHECK(plan::is_fusible({0, 1}, bi.s, bi.g, L));
 }
 
+TEST_CASE("block-capacity rule (SPEC.md:195)") {
+  const auto& L = blas::default_library();
+  Seq bi = load("BICGK");
+  // the smallest fused BiCGK kernel: 32x2 threads, A tile + p, q, r, s slices
+  const auto k = plan::generate_kernel({0, 1}, bi.s, bi.g, L, [] {
+    plan::CodegenParams p;
+    p.by = 2;
+    p.instances = 1;
+    p.overlap = true;
+    return p;
+  }());
+  REQUIRE(k.shared_bytes_total() > 0);
+  plan::PlannerOptions tight;
+  tight.block_shared_bytes = k.shared_bytes_total() - 4;
+  auto v = plan::fusibility({0, 1}, bi.s, bi.g, L, tight);
+  REQUIRE(v.has_value());
+  CHECK(v->rule == "block-capacity");
+  CHECK(v->nodes == std::vector<int>{0, 1});
+  CHECK(v->explanation.find("shared memory") != std::string::npos);
+  CHECK(plan::enumerate_fusions(bi.s, bi.g, L, {64, 64}, 6, tight).empty());
+  tight.block_shared_bytes = k.shared_bytes_total();
+  CHECK(plan::is_fusible({0, 1}, bi.s, bi.g, L, tight));
+  plan::PlannerOptions few;
+  few.max_threads_per_block = 32;  // a depth-2 block is 32 x BY >= 64 threads
+  v = plan::fusibility({0, 1}, bi.s, bi.g, L, few);
+  REQUIRE(v.has_value());
+  CHECK(v->rule == "block-capacity");
+  // the structural rules are checked first
+  Seq atax = load("ATAX");
+  v = plan::fusibility({0, 1}, atax.s, atax.g, L, tight);
+  REQUIRE(v.has_value());
+  CHECK(v->rule == "global-barrier-required");
+}
+
 TEST_CASE("transfer savings (SPEC.md:224-225)") {
   const auto& L = blas::default_library();
   Seq vadd = load("VADD");

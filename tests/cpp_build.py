@@ -50,6 +50,18 @@ def _obj(src):
     return o
 
 
+def build_tool(name, sources):
+    """Compiles sources (with their own main) + host objects into OUT/name."""
+    with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
+        objs = list(ex.map(_obj, host_sources()))
+    exe = os.path.join(OUT, name)
+    r = subprocess.run(["g++", "-std=c++20", "-O1", "-Wall"] + INC + list(sources) + objs + LIBS +
+                       ["-o", exe], capture_output=True, text=True)
+    if r.returncode:
+        raise RuntimeError(r.stderr[-4000:])
+    return exe
+
+
 def build_test(name, test_sources):
     """Compiles test_sources + a doctest main + host objects into OUT/name."""
     main = os.path.join(OUT, "doctest_main.cpp")

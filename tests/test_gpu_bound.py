@@ -120,3 +120,73 @@ def test_random_scripts_bound_and_graph(seed):
     got = outputs(plan, bufs)
     for k in want:
         assert np.array_equal(got[k], want[k], equal_nan=True), (text, k)
+
+
+def test_bound_plan_survives_workspace_growth():
+    """Paper-mode ATAX with n > 2048: sgemv records a small row-partial
+    scratch, then sgemtv needs a larger column-partial one.  The first
+    recorded launch must keep a live buffer (the workspace retires outgrown
+    scratch instead of freeing it), and later cudaMalloc users must not be
+    written through it."""
+    import torch
+    import paper_1305_1183_b200 as mf
+    plan = mf.Plan.sequence("ATAX", 2048, 8192, "fused")
+    assert plan.num_kernels == 2
+    bufs = make(torch, mf, plan, 11)
+    plan.launch(bufs)
+    torch.cuda.synchronize()
+    want = outputs(plan, bufs)
+    bound = plan.bind(bufs, {})
+    canary = torch.full((1 << 22,), 7.0, device="cuda")  # allocated after the bind
+    for k in want:
+        bufs[k].fill_(float("nan"))
+    for _ in range(3):
+        bound.launch()
+    torch.cuda.synchronize()
+    got = outputs(plan, bufs)
+    for k in want:
+        assert np.array_equal(got[k], want[k]), k
+    assert bool(torch.all(canary == 7.0))
+
+
+@pytest.mark.parametrize("seq,m,n", [("BICGK", 4096, 8192), ("AXPYDOT", 1, 1 << 22),
+                                     ("GEMVER", 2048, 4096)])
+def test_one_plan_concurrent_streams(seq, m, n):
+    """One plan launched on two streams at once with different inputs: each
+    stream has its own workspace (barrier counters, dot ticket, partials), so
+    both results equal the serial launches bit for bit."""
+    import torch
+    import paper_1305_1183_b200 as mf
+    plan = mf.Plan.sequence(seq, m, n, "fused")
+    sc = {"alpha": 0.5, "beta": 0.75}
+    b1, b2 = make(torch, mf, plan, 21), make(torch, mf, plan, 57)
+    plan.launch(b1, sc)
+    plan.launch(b2, sc)
+    torch.cuda.synchronize()
+    w1, w2 = outputs(plan, b1), outputs(plan, b2)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    for _ in range(5):
+        for k in w1:
+            b1[k].fill_(float("nan"))
+            b2[k].fill_(float("nan"))
+        torch.cuda.synchronize()
+        plan.launch(b1, sc, stream=s1)
+        plan.launch(b2, sc, stream=s2)
+        torch.cuda.synchronize()
+        g1, g2 = outputs(plan, b1), outputs(plan, b2)
+        for k in w1:
+            assert np.array_equal(g1[k], w1[k]), (k, 1)
+            assert np.array_equal(g2[k], w2[k]), (k, 2)
+
+
+def test_matrix_dims_must_be_padded_to_32():
+    """The matrix families reject shapes the reference never produces (every
+    buffer is padded to 32, proj/include/mapfuse/blas.hpp:29-30) instead of
+    running the cross-CTA finalize on a ragged column group."""
+    import torch
+    import paper_1305_1183_b200 as mf
+    plan = mf.Plan.sequence("BICGK", 64, 64, "fused")
+    A = torch.zeros(64, 52, device="cuda")
+    with pytest.raises(mf.VmFault, match="multiples of 32"):
+        plan.launch({"A": A, "p": torch.zeros(52, device="cuda"), "r": torch.zeros(64, device="cuda"),
+                     "q": torch.zeros(64, device="cuda"), "s": torch.zeros(52, device="cuda")})

@@ -60,11 +60,11 @@ def test_virtual_ranks_fused_column_reduction(seq, m, n, P, tma):
                 else:
                     d[b["name"]] = torch.full(shp, float("nan"), device="cuda")
             bufs.append(d)
-        # size every rank's workspace first: a workspace reallocation calls
-        # cudaFree, which synchronizes the whole device -- with virtual ranks
-        # sharing one GPU that would serialize ranks that must be co-resident
+        # size every rank's workspace (one per stream) first: allocation can
+        # synchronize the whole device -- with virtual ranks sharing one GPU
+        # that would serialize ranks that must be co-resident
         for r in range(P):
-            plans[r].launch(bufs[r], sc)
+            plans[r].launch(bufs[r], sc, stream=streams[r])
         torch.cuda.synchronize()
         for k in range(plans[0].num_kernels):
             kind = plans[0].describe()["kernels"][k]["kind"]
@@ -118,10 +118,10 @@ def test_virtual_ranks_row_resident_chain(n):
         bufs = [{"A": torch.from_numpy(A[r * mloc:(r + 1) * mloc].copy()).cuda(),
                  "x": torch.from_numpy(x).cuda(), "y": torch.zeros(n, device="cuda")}
                 for r in range(P)]
-        for r in range(P):
-            plans[r].launch(bufs[r])
-        torch.cuda.synchronize()
         streams = [torch.cuda.Stream() for _ in range(P)]
+        for r in range(P):  # size each stream's workspace first
+            plans[r].launch(bufs[r], stream=streams[r])
+        torch.cuda.synchronize()
         for r in range(P):
             plans[r].launch_kernel_peers(0, groups[r], bufs[r], {}, streams[r])
         torch.cuda.synchronize()
@@ -182,8 +182,8 @@ def test_virtual_ranks_fused_dot(P):
         bufs.append({"w": torch.from_numpy(w[sl].copy()).cuda(), "v": torch.from_numpy(v[sl].copy()).cuda(),
                      "u": torch.from_numpy(u[sl].copy()).cuda(),
                      "z": torch.empty(nloc, device="cuda"), "r": torch.full((1,), float("nan"), device="cuda")})
-    for r in range(P):  # size workspaces first (allocation syncs the device)
-        plans[r].launch(bufs[r], {"alpha": alpha})
+    for r in range(P):  # size each stream's workspace first (allocation can sync the device)
+        plans[r].launch(bufs[r], {"alpha": alpha}, stream=streams[r])
     torch.cuda.synchronize()
     for rep in range(3):
         for r in range(P):
@@ -244,10 +244,10 @@ def test_virtual_ranks_launch_peers_whole_plan(seq):
                 else:
                     d[b["name"]] = torch.full(shp, float("nan"), device="cuda")
             bufs.append(d)
-        for r in range(P):  # size workspaces (allocation syncs the device)
-            plans[r].launch(bufs[r], sc)
-        torch.cuda.synchronize()
         streams = [torch.cuda.Stream() for _ in range(P)]
+        for r in range(P):  # size each stream's workspace (allocation can sync the device)
+            plans[r].launch(bufs[r], sc, stream=streams[r])
+        torch.cuda.synchronize()
         for r in range(P):
             plans[r].launch_peers(groups[r], bufs[r], sc, streams[r])
         torch.cuda.synchronize()
@@ -267,3 +267,43 @@ def test_virtual_ranks_launch_peers_whole_plan(seq):
             assert np.all(err <= TAU * s + np.spacing(np.abs(w).astype(np.float32))), name
     finally:
         mf.set_option("max_sms", 0)
+
+
+_TIMEOUT_CHILD = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_1305_1183_b200 as mf
+P, n = 2, 1 << 16
+plan = mf.Plan.sequence("AXPYDOT", 1, n, "fused")
+groups = [mf.PeerGroup(P, r, n) for r in range(P)]
+groups[0].connect_local(1, groups[1]); groups[1].connect_local(0, groups[0])
+b = {k: torch.rand(n, device="cuda") for k in ("w", "v", "u")}
+b.update(z=torch.empty(n, device="cuda"), r=torch.empty(1, device="cuda"))
+plan.launch(b, {"alpha": 0.5})           # size the workspace
+torch.cuda.synchronize()
+plan.launch_kernel_peers(0, groups[0], b, {"alpha": 0.5})   # rank 1 never launches
+try:
+    groups[0].check()
+    print("NO-ERROR")
+except mf.VmFault as e:
+    print("FAULT:", e)
+plan.launch(b, {"alpha": 0.5})           # the context is still usable
+torch.cuda.synchronize()
+print("USABLE")
+"""
+
+
+def test_peer_barrier_times_out_with_clear_error():
+    """A rank whose peer never arrives gives up after MF_PEER_TIMEOUT_MS,
+    flags the group and finishes; mf_peer_group_check reports it and the
+    CUDA context stays usable (no trap, no hung GPU)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, MF_PEER_TIMEOUT_MS="300")
+    r = subprocess.run([sys.executable, "-c", _TIMEOUT_CHILD, root], env=env, capture_output=True,
+                       text=True, timeout=120)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "FAULT:" in r.stdout and "timed out" in r.stdout, r.stdout
+    assert "USABLE" in r.stdout

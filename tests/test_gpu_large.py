@@ -8,7 +8,7 @@ re-derived in fp64 on the CPU.
 import numpy as np
 import pytest
 
-from gpu_util import TAU
+from gpu_util import NORMWISE, TAU
 from oracle import COracle
 
 pytestmark = pytest.mark.gpu
@@ -22,10 +22,19 @@ def env():
     return torch, mf, COracle()
 
 
+# sampled rows / columns per full-size output (~256 + 256)
+NSAMPLE = 256
+
+
 def _check(got, ref, absref, what):
+    """|got - ref| <= tau * S + ulp(ref) per element, and the normwise bound
+    max|got - ref| / max|ref| <= 1e-5 over the sample."""
     err = np.abs(got.astype(np.float64) - ref)
     lim = TAU * absref + np.spacing(np.abs(ref).astype(np.float32)).astype(np.float64)
     assert np.all(err <= lim), (what, float(np.max(err / lim)))
+    nw = float(np.max(err) / max(float(np.max(np.abs(ref))), 1e-30))
+    assert nw <= NORMWISE, (what, "normwise", nw)
+    return nw
 
 
 @pytest.mark.parametrize("m,n", [(16384, 16384), (4096, 131072), (131072, 131072)])
@@ -43,8 +52,8 @@ def test_bicgk_sampled_rows_and_columns(env, m, n):
     plan.launch({"A": A, "p": p, "r": r, "q": q, "s": s})
     torch.cuda.synchronize()
     rng = np.random.default_rng(m + n)
-    rows = np.sort(rng.choice(m, 12, replace=False))
-    cols = np.sort(rng.choice(n, 12, replace=False))
+    rows = np.sort(rng.choice(m, NSAMPLE, replace=False))
+    cols = np.sort(rng.choice(n, NSAMPLE, replace=False))
     pc, rc = p.cpu().numpy(), r.cpu().numpy()
     qr, qa = co.hash_rows(7, n, rows, pc)
     _check(q.cpu().numpy()[rows], qr, qa, "q")
@@ -72,8 +81,8 @@ def test_gemver_full_size_properties(env):
     plan.launch(d, {"alpha": al, "beta": be})
     torch.cuda.synchronize()
     rng = np.random.default_rng(3)
-    rows = np.sort(rng.choice(m, 8, replace=False))
-    cols = np.sort(rng.choice(n, 8, replace=False))
+    rows = np.sort(rng.choice(m, NSAMPLE, replace=False))
+    cols = np.sort(rng.choice(n, NSAMPLE, replace=False))
     f64 = lambda t: t.cpu().numpy().astype(np.float64)
     u1, v1, u2, v2, y, z = (f64(d[k]) for k in ("u1", "v1", "u2", "v2", "y", "z"))
     A_rows = d["A"][torch.from_numpy(rows).cuda()].cpu().numpy().astype(np.float64)
@@ -92,6 +101,72 @@ def test_gemver_full_size_properties(env):
     wref = al * (B_rows.astype(np.float64) @ x)
     wabs = abs(al) * (np.abs(B_rows.astype(np.float64)) @ np.abs(x))
     _check(d["w"].cpu().numpy()[rows], wref, wabs, "w")
+
+
+def test_gesummv_full_size_sampled_rows(env):
+    """GESUMMV 32768^2 (BASELINE configs[3]; proj/data/scripts/gesummv.mfs:8-10,
+    oracle proj/src/blas.cpp:243+): y = alpha A x + beta B x on sampled rows
+    against fp64 sums over the same hash-generated A and B."""
+    torch, mf, co = env
+    m = n = 32768
+    plan = mf.Plan.sequence("GESUMMV", m, n, "fused")
+    A = torch.empty(m, n, device="cuda")
+    B = torch.empty(m, n, device="cuda")
+    mf.generate(A, seed=71)
+    mf.generate(B, seed=72)
+    x = torch.empty(n, device="cuda")
+    mf.generate(x, seed=73)
+    y = torch.full((m,), float("nan"), device="cuda")
+    al, be = 0.625, 0.375
+    plan.launch({"A": A, "B": B, "x": x, "y": y}, {"alpha": al, "beta": be})
+    torch.cuda.synchronize()
+    rows = np.sort(np.random.default_rng(11).choice(m, NSAMPLE, replace=False))
+    xc = x.cpu().numpy()
+    ta, taa = co.hash_rows(71, n, rows, xc)
+    tb, tba = co.hash_rows(72, n, rows, xc)
+    _check(y.cpu().numpy()[rows], al * ta + be * tb, abs(al) * taa + abs(be) * tba, "y")
+    assert not torch.isnan(y).any()
+    del A, B
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("mode", ["fused", "b200"])
+def test_atax_131072_sampled(env, mode):
+    """ATAX 131072^2 (BASELINE configs[4]; proj/data/scripts/atax.mfs:7-8,
+    oracle proj/src/blas.cpp:194-196 = matvec_t(matvec)): the paper's
+    two-kernel plan and the row-resident cluster kernel (mode b200).  The CPU
+    evaluates the whole intermediate t = A x in fp64 (multi-threaded hash
+    oracle), then y = A^T t on sampled columns, with the |.|-formula
+    S = |A|^T (|A||x|) as the tolerance scale; t is checked on sampled rows
+    where the plan stores it."""
+    torch, mf, co = env
+    m = n = 131072
+    plan = mf.Plan.sequence("ATAX", m, n, mode)
+    d = plan.describe()
+    if mode == "b200":
+        assert plan.num_kernels == 1 and d["kernels"][0]["shape"]["chain"] == 1
+    A = torch.empty(m, n, device="cuda")
+    mf.generate(A, seed=81)
+    x = torch.empty(n, device="cuda")
+    mf.generate(x, seed=82)
+    bufs = {"A": A, "x": x, "y": torch.full((n,), float("nan"), device="cuda")}
+    if any(b["name"] == "t" for b in d["buffers"]):
+        bufs["t"] = torch.full((m,), float("nan"), device="cuda")
+    plan.launch(bufs)
+    torch.cuda.synchronize()
+    xc = x.cpu().numpy()
+    t64, tabs = co.hash_matvec_all(81, m, n, xc)
+    rng = np.random.default_rng(13)
+    if "t" in bufs:
+        rows = np.sort(rng.choice(m, NSAMPLE, replace=False))
+        _check(bufs["t"].cpu().numpy()[rows], t64[rows], tabs[rows], "t")
+    cols = np.sort(rng.choice(n, NSAMPLE, replace=False))
+    yr, ya = co.hash_cols_f64(81, n, m, cols, t64, tabs)
+    y = bufs["y"].cpu().numpy()
+    assert not np.isnan(y).any()
+    _check(y[cols], yr, ya, "y")
+    del A, bufs
+    torch.cuda.empty_cache()
 
 
 def test_sharded_plan_single_rank_equals_plan(env):

@@ -134,10 +134,10 @@ def test_random_script_peers_in_kernel(seed, mode):
             for q in range(P):
                 if q != r:
                     groups[r].connect_local(q, groups[q])
-        for r in range(P):  # size workspaces first (allocation synchronizes the device)
-            sps[r].plan.launch(bufs[r], {"k": env["k"]})
-        torch.cuda.synchronize()
         streams = [torch.cuda.Stream() for _ in range(P)]
+        for r in range(P):  # size each stream's workspace first (allocation can sync the device)
+            sps[r].plan.launch(bufs[r], {"k": env["k"]}, stream=streams[r])
+        torch.cuda.synchronize()
         for r in range(P):
             sps[r].plan.launch_peers(groups[r], bufs[r], {"k": env["k"]}, streams[r])
         torch.cuda.synchronize()

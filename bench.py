@@ -205,6 +205,36 @@ def cpu_reference(n_total: int, threads: int, reps: int, warmup: int):
             "sec_per_step": sec, "elements": per * threads}
 
 
+def cpu_reference_matrix(seq: str, n: int, threads: int, rows_per_thread: int, reps: int, warmup: int):
+    """`seq` (a row-shardable matrix sequence) at n columns through the
+    reference's reference_execute, one independent row panel of
+    `rows_per_thread` x n per host thread -- a bounded sample of the n x n
+    workload with the same per-element work (make_problem excluded)."""
+    from oracle import RefOracle
+    ref = RefOracle()
+    probs = _parallel(lambda t: ref.problem(seq, rows_per_thread, n, 1 + t), list(range(threads)))
+
+    def one(p):
+        p.L.mfr_execute(p.h)
+
+    for _ in range(warmup):
+        _parallel(one, probs)
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        _parallel(one, probs)
+        times.append(time.perf_counter() - t0)
+    m = rows_per_thread
+    per = {"BICGK": 4 * (m * n + 2 * m + 2 * n), "ATAX": 4 * (2 * m * n + m + 2 * n),
+           "GEMVER": 4 * (3 * m * n + 4 * m + 7 * n)}[seq]
+    sec = statistics.median(times)
+    return {"value": per * threads / sec / 1e9, "unit": "GB/s", "cores": threads, "kind": "reference",
+            "host": host_info(),
+            "sample": "reference_execute (oracle/_ref) %s on %d independent %d x %d row panels "
+                      "(%d threads), make_problem excluded" % (seq, threads, m, n, threads),
+            "sec_per_step": sec, "rows": m * threads}
+
+
 # ---------------------------------------------------------------------------
 def make_buffers(torch, mf, plan, seed, skip_intermediate=True):
     d = plan.describe()
@@ -770,6 +800,26 @@ def main():
         if rank != 0:
             return
         threads = os.cpu_count() or 1
+        if workload != "blas1":
+            # the sharded line's workload: row panels of the n x n matrix
+            seq = SHARDED_SEQ[workload]
+            n = args.n_matrix or SHARDED_N[seq]
+            rows = max(1, (32 << 20) // (4 * n))  # ~32 MiB of A per thread per step
+            r = cpu_reference_matrix(seq, n, threads, rows, args.steps, args.warmup)
+            cfg = {"workload": "%s fp32 %dx%d (reference_execute on %d-row panels, one per host thread)"
+                               % (seq, n, n, rows), "n": n, "rows_sampled": r["rows"],
+                   "parallelism": "host threads x%d" % threads, "data": "synthetic (make_problem)"}
+            line = {"impl": "reference", "metric": METRIC, "value": round(r["value"], 3), "unit": "GB/s",
+                    "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                    "ms_per_step": round(r["sec_per_step"] * 1e3, 3), "higher_is_better": True,
+                    "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                    "config": cfg,
+                    "cpu_baseline": {"value": round(r["value"], 3), "unit": "GB/s", "cores": r["cores"],
+                                     "kind": "reference", "sample": r["sample"], "host": r["host"]},
+                    "e2e": {"value": round(r["value"], 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                            "d2h_bytes_per_step": 0}}
+            print(json.dumps(line), flush=True)
+            return
         # the stated n: every step is the whole 2^28-element workload, split
         # into one independent slice per host thread
         r = cpu_reference(args.n, threads, args.steps, args.warmup)

@@ -53,9 +53,13 @@ def test_bench_two_ranks_on_one_gpu():
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
     assert r.returncode == 0, r.stderr[-3000:]
     d = _line(r.stdout)
-    assert d["n_gpus"] == 2 and d["config"]["global_elements"] == 2 * (1 << 22)
-    assert "all 2 ranks" in d["e2e"]["path"]
-    assert d["sharded"]["rows_per_rank"] == 2048 and d["sharded"]["value"] > 0
+    # N > 1 headline: BiCGK row-sharded strong scaling (bench.py workload "auto")
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["value"] > 0
+    assert d["config"]["rows_per_rank"] == 2048 and d["config"]["collectives_per_step"] == 1
+    assert d["parity"]["ok"] and d["parity"]["checked"] == ["q", "s"]
+    ss = d["strong_scaling"]
+    assert ss["n"] == 2 and ss["t1_ms"] > 0 and ss["efficiency"] > 0
+    assert "max over ranks" in d["e2e"]["path"] and d["e2e"]["h2d_bytes_per_step"] > 0
     ref = subprocess.run(torchrun("--impl", "reference", "--steps", "2"), capture_output=True, text=True,
                          timeout=600, cwd=ROOT, env=env)
     assert ref.returncode == 0, ref.stderr[-3000:]

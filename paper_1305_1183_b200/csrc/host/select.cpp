@@ -33,7 +33,8 @@ CostModel CostModel::defaults() {
       {"matrix.ldg.rank", 0.62},   // GEMVER ger2+sgemtv, register-fed
       {"matrix.tma.rank", 0.99},   // GEMVER ger2+sgemtv, TMA ring, 16 consumer warps, bulk S2G stores
       {"matrix.rowres", 0.88},     // row-resident chain (ATAX one pass, 16384^2)
-      {"matrix.rowres.cluster", 0.75},  // ... rows over a CTA cluster (n > 16384): 32768^2 0.86, 131072 cols 0.71
+      {"matrix.rowres.cluster", 0.95},  // ... rows over a CTA cluster (n > 16384), st.async exchange:
+                                        //   32768^2 1.08, 131072^2 0.93 (profiles/r02_rowres_variants.txt)
       {"generic.d1", 0.70},        // NVRTC-emitted KernelIR (host/cudagen.cpp), depth 1,
                                    //   prefetch 4 ahead: VADD 0.93, AXPYDOT 0.53
                                    //   (profiles/r01_generic_sweep_pf.txt)

@@ -941,6 +941,9 @@ int mf_set_option(const char* key, int value) {
     } else if (k == "tma_consumers") {
       if (value != 0 && value != 256 && value != 512) throw Invalid("tma_consumers: 0|256|512");
       options().tma_consumers = value;
+    } else if (k == "rowres_cluster") {
+      if (value < 0 || value > 6) throw Invalid("rowres_cluster: 0 (auto) | 1 .. 6");
+      options().rowres_cluster = value;
     } else if (k == "max_sms") {
       if (value < 0) throw Invalid("max_sms >= 0");
       options().max_sms = value;
@@ -991,6 +994,7 @@ int mf_get_option(const char* key) {
   if (k == "tma_bulk_store") return options().tma_bulk_store;
   if (k == "max_sms") return options().max_sms;
   if (k == "tma_consumers") return options().tma_consumers;
+  if (k == "rowres_cluster") return options().rowres_cluster;
   if (k == "stream_unroll") return options().stream_unroll;
   if (k == "stream_ctas_per_sm") return options().stream_ctas_per_sm;
   if (k == "generic") return mapfuse::plan::force_generic() ? 1 : 0;

@@ -35,6 +35,7 @@ EngineOptions& options() {
     if (const char* v = std::getenv("MF_GENERIC_POISON")) e.generic_poison = std::atoi(v);
     if (const char* v = std::getenv("MF_NVTX")) e.nvtx = std::atoi(v);
     if (const char* v = std::getenv("MF_GENERIC_CHECKED")) e.generic_checked = std::atoi(v);
+    if (const char* v = std::getenv("MF_ROWRES_CLUSTER")) e.rowres_cluster = std::atoi(v);
     return e;
   }();
   return o;
@@ -292,7 +293,8 @@ void run_rowres(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc, 
   const int sms = eo.max_sms > 0 ? std::min(eo.max_sms, device_sm_count()) : device_sm_count();
   int grid = 0;
   if (n > rowres_max_cols()) {  // wide rows: a CTA cluster per row (distributed shared memory)
-    const int bands = rowres_cluster_bands(m, n, sms);
+    const int variant = rowres_cluster_variant(eo.rowres_cluster, n);
+    const int bands = rowres_cluster_bands(m, n, sms, variant);
     if (bands <= 0) throw Fault("kernel " + k.name + ": no co-resident CTA cluster for n = " + std::to_string(n));
     a.CB = 1;
     a.RB = bands;
@@ -301,7 +303,7 @@ void run_rowres(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc, 
     a.bar = ws.counters(s);
     fill_peers(a, peers, n, k.name);
     emit(rec, "launch " + k.name,
-         [=](cudaStream_t st) { return launch_rowres_cluster(a, sms, sms, st); }, s);
+         [=](cudaStream_t st) { return launch_rowres_cluster(a, variant, sms, st); }, s);
     return;
   }
   check_cuda(rowres_config(m, n, sms, &a, &grid), ("configure " + k.name).c_str());

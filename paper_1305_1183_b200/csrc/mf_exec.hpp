@@ -42,6 +42,7 @@ struct EngineOptions {
   int tma = -1;  // matrix kernels: -1 auto (by shape), 1 = TMA ring, 0 = register-fed
   int max_sms = 0;  // > 0: cap the SMs a matrix kernel's grid is sized for
   int tma_consumers = 0;  // TMA matrix variant: 0 auto (by shape), 256 or 512 consumer threads
+  int rowres_cluster = 0;  // wide-row chain variant: 0 auto, 1 stage-held, 2 register-held, 3 8192-col slices
   // matrix operand loads: 0 evict-first L2 policy, 1 evict-normal, -1 auto =
   // evict-normal when the kernel also stores a matrix (GEMVER stage 1: 2036 ->
   // 1996 us, fewer dirty lines of B left for the next kernel to write back),

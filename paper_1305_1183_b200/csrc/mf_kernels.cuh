@@ -114,9 +114,13 @@ cudaError_t launch_rowres(const MatrixArgs& a, int grid, cudaStream_t s);
 // Wide rows (16384 < n <= 131072): a cluster of ceil(n/16384) CTAs shares each
 // row over distributed shared memory, then a cooperative finalize kernel
 // combines the cluster bands' column partials (colpart [bands][n]).
+// variant: 1 stage-held 16384-column slices, 2 register-held 16384-column
+// slices, 3 register-held 8192-column slices (clusters up to 16);
+// rowres_cluster_variant maps 0 (auto) to the default.
 long long rowres_cluster_max_cols();
-int rowres_cluster_bands(long long m, long long n, int sms);  // co-resident clusters (0: unsupported)
-cudaError_t launch_rowres_cluster(MatrixArgs a, int sms, int finalize_grid, cudaStream_t s);
+int rowres_cluster_variant(int requested, long long n);
+int rowres_cluster_bands(long long m, long long n, int sms, int variant);  // co-resident clusters (0: unsupported)
+cudaError_t launch_rowres_cluster(MatrixArgs a, int variant, int finalize_grid, cudaStream_t s);
 bool tma_supported(const MatrixShape& sh, const MatrixTuning& t);  // fits a >= 2-stage ring
 size_t matrix_acc_bytes(const MatrixTuning& t);
 

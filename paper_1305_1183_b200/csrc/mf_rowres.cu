@@ -258,6 +258,19 @@ __device__ __forceinline__ void cl_arrive_remote(unsigned long long* local_bar, 
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_addr(local_bar)), "r"(target));
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
 }
+// One message instead of two: the value lands in the target CTA's slot and
+// completes 4 transaction bytes on its slot mbarrier (st.async), so no
+// release fence has to wait for the store's round trip before the arrive.
+__device__ __forceinline__ void cl_store_async(float* local_addr, unsigned long long* local_bar,
+                                               unsigned target, float v) {
+  unsigned ra, rb;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_addr(local_addr)), "r"(target));
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(smem_addr(local_bar)), "r"(target));
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(ra),
+               "r"(__float_as_uint(v)), "r"(rb)
+               : "memory");
+}
+
 __device__ __forceinline__ void cl_wait_bar(unsigned long long* b, unsigned parity) {
   asm volatile(
       "{\n.reg .pred p;\nCL_WAIT_%=:\n"
@@ -274,9 +287,10 @@ __device__ __forceinline__ void cl_wait_bar(unsigned long long* b, unsigned pari
 constexpr int kRcAhead = 1;
 constexpr int kRcDepth = 8;  // exchange slots: > the largest lead (kRcAhead + 3 rows) of a CTA
 
-template <int K, int CL>
+template <int K, int CL, int S, bool XA>
 __global__ void __launch_bounds__(kRrThreads, 1) rowres_cluster_kernel(MatrixArgs a) {
   constexpr int C = 4 * kRrConsumers * K;  // columns per CTA slice
+  constexpr int kRrStages = S;
   extern __shared__ __align__(128) unsigned char smem[];
   float* ring = reinterpret_cast<float*>(smem);  // stage = one row slice (C floats)
   unsigned long long* full = reinterpret_cast<unsigned long long*>(ring + (size_t)kRrStages * C);
@@ -295,8 +309,10 @@ __global__ void __launch_bounds__(kRrThreads, 1) rowres_cluster_kernel(MatrixArg
       rr_mbar_init(&full[s], 1);
       rr_mbar_init(&empty[s], kRrWarps);
     }
-    for (int d = 0; d < kRcDepth; ++d) rr_mbar_init(&xbar[d], CL);
+    for (int d = 0; d < kRcDepth; ++d) rr_mbar_init(&xbar[d], XA ? 1 : CL);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if constexpr (XA)  // arm every slot's first phase: CL partials of 4 bytes
+      for (int d = 0; d < kRcDepth; ++d) rr_expect_tx(&xbar[d], CL * 4);
   }
   __syncthreads();
   cl_arrive();  // every CTA's barriers initialised before any remote arrive
@@ -351,8 +367,12 @@ __global__ void __launch_bounds__(kRrThreads, 1) rowres_cluster_kernel(MatrixArg
     };
     auto publish = [&](long long j, float p) {  // my partial -> slot j of every cluster CTA
       if (tid < CL) {
-        cl_store(&xch[j % kRcDepth][crank], (unsigned)tid, p);
-        cl_arrive_remote(&xbar[j % kRcDepth], (unsigned)tid);
+        if constexpr (XA) {
+          cl_store_async(&xch[j % kRcDepth][crank], &xbar[j % kRcDepth], (unsigned)tid, p);
+        } else {
+          cl_store(&xch[j % kRcDepth][crank], (unsigned)tid, p);
+          cl_arrive_remote(&xbar[j % kRcDepth], (unsigned)tid);
+        }
       }
     };
     for (long long j = 0; j < kRcAhead && j < nrows; ++j) publish(j, slice_partial(j));
@@ -364,8 +384,9 @@ __global__ void __launch_bounds__(kRrThreads, 1) rowres_cluster_kernel(MatrixArg
       float s32 = 0.f;  // slices combined in cluster rank order: identical in every CTA
 #pragma unroll
       for (int q = 0; q < CL; ++q) s32 += xch[j % kRcDepth][q];
+      if (XA && tid == 0) rr_expect_tx(&xbar[j % kRcDepth], CL * 4);  // arm the slot for row j + kRcDepth
       const float ti = (float)(a.ar[0] * (double)s32);  // t_i rounded to fp32 as the unfused plan stores it
-      if (crank == 0 && tid == 0 && a.yr[0]) a.yr[0][r0 + j] = ti;
+      if (crank == 0 && tid == kRrConsumers - 1 && a.yr[0]) a.yr[0][r0 + j] = ti;  // not a publisher: its release must not wait on this store
       if (width > 0) {
         const float* row = ring + (size_t)(j % kRrStages) * C;
 #pragma unroll
@@ -393,6 +414,135 @@ __global__ void __launch_bounds__(kRrThreads, 1) rowres_cluster_kernel(MatrixArg
   cl_wait();
 }
 
+// Register-held variant (no producer warp, 16 warps = 4 per SM sub-partition,
+// so 128 registers per thread): every consumer loads its K float4 slots of
+// row j from the stage into registers ONCE; after the CTA reduction of row j
+// (whose named barrier proves every warp has its copy) thread 0 refills that
+// stage with row j+S.  All S stages stream from HBM while row j waits for the
+// cluster's t_j, and pass 2 runs from registers: one shared-memory read per
+// row instead of two, no stage held across the exchange.  The exchange of
+// row j is not overlapped with row j+1's reduction -- the ring keeps HBM busy
+// instead.  Exchange slots: a CTA publishes row j only after it consumed row
+// j-1 (all peers' row j-1 partials), so live slots span <= 3 rows.
+constexpr int kRgThreads = kRrConsumers;
+
+template <int K, int CL, int S, bool XA>
+__global__ void __launch_bounds__(kRgThreads, 1) rowres_cluster_reg_kernel(MatrixArgs a) {
+  constexpr int C = 4 * kRgThreads * K;  // columns per CTA slice
+  extern __shared__ __align__(128) unsigned char smem[];
+  float* ring = reinterpret_cast<float*>(smem);
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(ring + (size_t)S * C);
+  __shared__ float red[2][kRrWarps];
+  __shared__ float xch[kRcDepth][CL];
+  __shared__ __align__(8) unsigned long long xbar[kRcDepth];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned crank = cl_rank(), cid = cl_id(), ncl = cl_count();
+  const long long c0 = (long long)crank * C;
+  const long long width = a.n - c0 < C ? (a.n - c0 > 0 ? a.n - c0 : 0) : C;
+  const long long r0 = (long long)cid * a.m / ncl, r1 = (long long)(cid + 1) * a.m / ncl;
+  const long long nrows = r1 - r0;
+  const unsigned long long pol = evict_first_policy();
+  auto refill = [&](long long j) {  // thread 0: row j's slice -> stage j % S
+    const int stage = (int)(j % S);
+    const long long bytes = width * 4;
+    rr_expect_tx(&full[stage], (unsigned)bytes);
+    const char* src = reinterpret_cast<const char*>(a.M[0] + (r0 + j) * a.ld + c0);
+    char* dst = reinterpret_cast<char*>(ring + (size_t)stage * C);
+    for (long long off = 0; off < bytes; off += 16384) {
+      const long long piece = (bytes - off) < 16384 ? (bytes - off) : 16384;
+      rr_bulk(dst + off, src + off, (unsigned)piece, &full[stage], pol);
+    }
+  };
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) rr_mbar_init(&full[s], 1);
+    for (int d = 0; d < kRcDepth; ++d) rr_mbar_init(&xbar[d], XA ? 1 : CL);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if constexpr (XA)  // arm every slot's first phase: CL partials of 4 bytes
+      for (int d = 0; d < kRcDepth; ++d) rr_expect_tx(&xbar[d], CL * 4);
+    if (width > 0)
+      for (long long j = 0; j < S && j < nrows; ++j) refill(j);
+  }
+  __syncthreads();
+  cl_arrive();  // every CTA's barriers initialised before any remote arrive
+  cl_wait();
+  const float* xp = a.xr[0] + c0 + 4 * tid;
+  const float* sp = ring + 4 * tid;
+  float4 xs[K];
+  float cacc[K][4];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    xs[k] = (4 * tid + 4 * kRgThreads * k < width) ? __ldg(reinterpret_cast<const float4*>(xp + 4 * kRgThreads * k))
+                                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) cacc[k][e] = 0.f;
+  }
+  int rbuf = 0;
+  for (long long j = 0; j < nrows; ++j) {
+    float4 v[K];
+    float part = 0.f;
+    if (width > 0) {
+      const int stage = (int)(j % S);
+      rr_wait(&full[stage], (unsigned)((j / S) & 1));
+      const float* row = sp + (size_t)stage * C;
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+        v[k] = (4 * tid + 4 * kRgThreads * k < width) ? *reinterpret_cast<const float4*>(row + 4 * kRgThreads * k)
+                                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        part = fmaf(v[k].x, xs[k].x, part);
+        part = fmaf(v[k].y, xs[k].y, part);
+        part = fmaf(v[k].z, xs[k].z, part);
+        part = fmaf(v[k].w, xs[k].w, part);
+      }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
+    if (lane == 0) red[rbuf][warp] = part;
+    __syncthreads();  // every warp holds row j in registers: its stage is free
+    if (tid == 0 && width > 0 && j + S < nrows) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      refill(j + S);
+    }
+    if (tid < CL) {  // my partial -> slot j of every cluster CTA
+      float sum = red[rbuf][0];
+#pragma unroll
+      for (int w = 1; w < kRrWarps; ++w) sum += red[rbuf][w];
+      if constexpr (XA) {
+        cl_store_async(&xch[j % kRcDepth][crank], &xbar[j % kRcDepth], (unsigned)tid, sum);
+      } else {
+        cl_store(&xch[j % kRcDepth][crank], (unsigned)tid, sum);
+        cl_arrive_remote(&xbar[j % kRcDepth], (unsigned)tid);
+      }
+    }
+    rbuf ^= 1;
+    cl_wait_bar(&xbar[j % kRcDepth], (unsigned)((j / kRcDepth) & 1));
+    float s32 = 0.f;  // slices combined in cluster rank order: identical in every CTA
+#pragma unroll
+    for (int q = 0; q < CL; ++q) s32 += xch[j % kRcDepth][q];
+    if (XA && tid == 0) rr_expect_tx(&xbar[j % kRcDepth], CL * 4);  // arm the slot for row j + kRcDepth
+    const float ti = (float)(a.ar[0] * (double)s32);  // t_i rounded to fp32 as the unfused plan stores it
+    if (crank == 0 && tid == kRrConsumers - 1 && a.yr[0]) a.yr[0][r0 + j] = ti;  // not a publisher: its release must not wait on this store
+    if (width > 0) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        cacc[k][0] = fmaf(v[k].x, ti, cacc[k][0]);
+        cacc[k][1] = fmaf(v[k].y, ti, cacc[k][1]);
+        cacc[k][2] = fmaf(v[k].z, ti, cacc[k][2]);
+        cacc[k][3] = fmaf(v[k].w, ti, cacc[k][3]);
+      }
+    }
+  }
+  float* colpart = static_cast<float*>(a.colpart) + (long long)cid * a.n + c0 + 4 * tid;
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+    if (4 * tid + 4 * kRgThreads * k < width)
+      *reinterpret_cast<float4*>(colpart + 4 * kRgThreads * k) =
+          make_float4(cacc[k][0], cacc[k][1], cacc[k][2], cacc[k][3]);
+  cl_arrive();  // no CTA leaves while a peer may still address its shared memory
+  cl_wait();
+}
+
 // colpart[RB][n] -> y (fixed band order; across GPUs when a.peer is set).
 __global__ void __launch_bounds__(256) rowres_finalize_kernel(MatrixArgs a) {
   finalize_any<0, 1, float>(a, threadIdx.x, 256);
@@ -414,71 +564,130 @@ size_t rowres_smem(long long n) {
 }
 
 using RcFn = void (*)(MatrixArgs);
-constexpr long long kRcSlice = 4LL * kRrConsumers * 8;  // 16384 columns per CTA
 
-RcFn rowres_cluster_fn(int cl) {
+// Cluster variants (option "rowres_cluster"):
+//   1: 16384-column slices (K = 8), clusters of ceil(n/16384) <= 8, 3 x 64 KB
+//      stages, row j+1 reduced ahead of row j's exchange (stage-held);
+//   2: the same slices, register-held rows with early stage release;
+//   3: 8192-column slices (K = 4), clusters of ceil(n/8192) <= 16
+//      (non-portable above 8), 6 x 32 KB stages, register-held rows;
+//   4, 5, 6: variants 1, 2, 3 with the exchange sent as st.async messages.
+struct RcVariant {
+  int K, stages;
+  bool reg;
+  long long slice() const { return 4LL * kRrConsumers * K; }
+  size_t smem() const { return (size_t)stages * slice() * 4 + 2 * (size_t)stages * 8 + 128; }
+  int threads() const { return reg ? kRgThreads : kRrThreads; }
+};
+
+RcVariant rc_variant(int v) {
+  switch (v) {
+    case 1:
+    case 4: return {8, 3, false};
+    case 3:
+    case 6: return {4, 6, true};
+    default: return {8, 3, true};
+  }
+}
+
+template <int CL>
+RcFn rc_fn_cl(int variant) {
+  switch (variant) {
+    case 1:
+    case 4:
+      if constexpr (CL <= 8)
+        return variant == 1 ? rowres_cluster_kernel<8, CL, 3, false> : rowres_cluster_kernel<8, CL, 3, true>;
+      return nullptr;
+    case 3: return rowres_cluster_reg_kernel<4, CL, 6, false>;
+    case 6: return rowres_cluster_reg_kernel<4, CL, 6, true>;
+    case 5:
+      if constexpr (CL <= 8) return rowres_cluster_reg_kernel<8, CL, 3, true>;
+      return nullptr;
+    default:
+      if constexpr (CL <= 8) return rowres_cluster_reg_kernel<8, CL, 3, false>;
+      return nullptr;
+  }
+}
+
+RcFn rowres_cluster_fn(int variant, int cl) {
   switch (cl) {
-    case 2: return rowres_cluster_kernel<8, 2>;
-    case 3: return rowres_cluster_kernel<8, 3>;
-    case 4: return rowres_cluster_kernel<8, 4>;
-    case 5: return rowres_cluster_kernel<8, 5>;
-    case 6: return rowres_cluster_kernel<8, 6>;
-    case 7: return rowres_cluster_kernel<8, 7>;
-    case 8: return rowres_cluster_kernel<8, 8>;
+    case 2: return rc_fn_cl<2>(variant);
+    case 3: return rc_fn_cl<3>(variant);
+    case 4: return rc_fn_cl<4>(variant);
+    case 5: return rc_fn_cl<5>(variant);
+    case 6: return rc_fn_cl<6>(variant);
+    case 7: return rc_fn_cl<7>(variant);
+    case 8: return rc_fn_cl<8>(variant);
+    case 9: return rc_fn_cl<9>(variant);
+    case 10: return rc_fn_cl<10>(variant);
+    case 11: return rc_fn_cl<11>(variant);
+    case 12: return rc_fn_cl<12>(variant);
+    case 13: return rc_fn_cl<13>(variant);
+    case 14: return rc_fn_cl<14>(variant);
+    case 15: return rc_fn_cl<15>(variant);
+    case 16: return rc_fn_cl<16>(variant);
     default: return nullptr;
   }
+}
+
+// fills cfg (grid left to the caller) for variant v at n columns; nullptr if unsupported
+RcFn rc_setup(int v, long long n, cudaLaunchConfig_t* cfg, cudaLaunchAttribute* attr, int* cl_out) {
+  const RcVariant var = rc_variant(v);
+  const int cl = (int)((n + var.slice() - 1) / var.slice());
+  RcFn fn = rowres_cluster_fn(v, cl);
+  if (!fn) return nullptr;
+  if (cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)var.smem()) !=
+      cudaSuccess)
+    return nullptr;
+  if (cl > 8 &&
+      cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+    return nullptr;
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cl;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg->blockDim = dim3(var.threads());
+  cfg->dynamicSmemBytes = var.smem();
+  cfg->attrs = attr;
+  cfg->numAttrs = 1;
+  *cl_out = cl;
+  return fn;
 }
 
 }  // namespace
 
 long long rowres_max_cols() { return 4LL * kRrConsumers * 8; }
-long long rowres_cluster_max_cols() { return 8 * kRcSlice; }
+long long rowres_cluster_max_cols() { return 16 * 8192; }
 
-cudaError_t launch_rowres_cluster(MatrixArgs a, int sms, int finalize_grid, cudaStream_t s) {
-  const int cl = (int)((a.n + kRcSlice - 1) / kRcSlice);
-  RcFn fn = rowres_cluster_fn(cl);
-  if (!fn) return cudaErrorNotSupported;
-  const size_t smem = (size_t)kRrStages * kRcSlice * 4 + 2 * kRrStages * 8 + 128;
-  cudaError_t e = cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
-  if (e != cudaSuccess) return e;
+// auto: variant 4 (tools/rowres_sweep.py on B200, profiles/r02_rowres_variants.txt:
+// ATAX 131072^2 11.27 ms vs 13.81 / 20.5 / 31.7 ms for variants 1 / 2 / 3)
+int rowres_cluster_variant(int requested, long long n) {
+  if (requested >= 1 && requested <= 6) return requested;
+  (void)n;
+  return 4;
+}
+
+cudaError_t launch_rowres_cluster(MatrixArgs a, int variant, int finalize_grid, cudaStream_t s) {
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = cl;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.blockDim = dim3(kRrThreads);
-  cfg.dynamicSmemBytes = smem;
+  int cl = 0;
+  RcFn fn = rc_setup(variant, a.n, &cfg, attr, &cl);
+  if (!fn) return cudaErrorNotSupported;
   cfg.stream = s;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
   cfg.gridDim = dim3(cl * a.RB);  // a.RB = rowres_cluster_bands(m, n, sms): colpart is [RB][n]
-  e = cudaLaunchKernelEx(&cfg, fn, a);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, fn, a);
   if (e != cudaSuccess) return e;
   void* args[] = {&a};
   return cudaLaunchCooperativeKernel((const void*)rowres_finalize_kernel, dim3(finalize_grid), dim3(256),
                                      args, 0, s);
 }
 
-int rowres_cluster_bands(long long m, long long n, int sms) {
-  const int cl = (int)((n + kRcSlice - 1) / kRcSlice);
-  RcFn fn = rowres_cluster_fn(cl);
-  if (!fn) return 0;
-  const size_t smem = (size_t)kRrStages * kRcSlice * 4 + 2 * kRrStages * 8 + 128;
-  if (cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-      cudaSuccess)
-    return 0;
+int rowres_cluster_bands(long long m, long long n, int sms, int variant) {
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = cl;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.blockDim = dim3(kRrThreads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  int cl = 0;
+  RcFn fn = rc_setup(variant, n, &cfg, attr, &cl);
+  if (!fn) return 0;
   cfg.gridDim = dim3(cl * std::max(1, sms / cl));
   int nclusters = 0;
   if (cudaOccupancyMaxActiveClusters(&nclusters, (const void*)fn, &cfg) != cudaSuccess) return 0;

@@ -277,6 +277,31 @@ def test_b200_mode_row_resident_atax(env, m, n):
     assert np.all(err <= 2.0 ** -17 * S["y"] + np.spacing(np.abs(ref["y"])))
 
 
+@pytest.mark.parametrize("m,n", [(96, 20000), (320, 65536), (160, 131072), (2048, 32768)])
+def test_row_resident_cluster_variants(env, m, n):
+    """Every wide-row chain variant (option "rowres_cluster": stage-held or
+    register-held rows, remote-arrive or st.async exchange, 16384- or
+    8192-column slices) against the oracle; the variants with the same
+    slices sum in the same order and agree bit for bit."""
+    torch, mf, co = env
+    vals = rand_inputs("ATAX", m, n, 5 + m)
+    want = co.execute("ATAX", m, n, vals)
+    S = scale_bound(co, "ATAX", m, n, vals)
+    outs = {}
+    try:
+        for v in (1, 2, 3, 4, 5, 6):
+            mf.set_option("rowres_cluster", v)
+            plan = mf.Plan.sequence("ATAX", m, n, "b200")
+            got = run_plan(torch, plan, vals, out_shapes(plan))
+            check_output("ATAX", "y", got["y"], want["y"], S["y"])
+            outs[v] = got["y"]
+    finally:
+        mf.set_option("rowres_cluster", 0)
+    for v in (2, 4, 5):
+        assert np.array_equal(outs[v], outs[1]), v
+    assert np.array_equal(outs[6], outs[3])
+
+
 @pytest.mark.parametrize("seq,m,n", [("AXPYDOT", 1, 0), ("BICGK", 0, 64), ("BICGK", 64, 0),
                                      ("ATAX", 0, 96), ("GESUMMV", 32, 0), ("VADD", 1, 0)])
 def test_empty_problems(env, seq, m, n):

@@ -15,6 +15,15 @@ them, before any later kernel consumes them -- the plan reports exactly
 which names those are (mf_plan_kernel_column_outputs).  No other exchange
 exists in any Table-1 sequence.
 
+outputs="sharded": a column-reduced OUTPUT that no later kernel reads (ATAX's
+y, BiCGK's s) is reduce-scattered instead (ncclReduceScatter:
+(P-1)/P n words per rank instead of the all-reduce's 2(P-1)/P n), leaving
+rank r with the finished slice column_slice(name) = [r n/P, (r+1) n/P) of
+it -- for a consumer that is itself column-sharded.  Intermediates consumed
+by a later kernel (GEMVER's and SGEMVT's t feed x = beta t + z, whose x every rank's
+B x needs whole) stay all-reduced, and so does any output whose length n is
+not a multiple of P (equal-sized slices).
+
 `executor` is injectable so the host-side orchestration can be exercised on
 CPU with the gloo backend (tests/test_sharding_gloo.py); the default
 executor launches the sm_100a kernels through the C-ABI.
@@ -39,7 +48,8 @@ class ShardedPlan:
                  mode: str = "fused", script: Optional[str] = None, world: Optional[int] = None,
                  rank: Optional[int] = None, group=None,
                  executor: Optional[Callable] = None, allreduce: Optional[Callable] = None,
-                 collective: str = "nccl", peer_group=None, manifest: Optional[str] = None):
+                 collective: str = "nccl", peer_group=None, manifest: Optional[str] = None,
+                 outputs: str = "replicated", reduce_scatter: Optional[Callable] = None):
         import torch.distributed as dist
         if world is None:
             world = dist.get_world_size(group) if dist.is_initialized() else 1
@@ -73,6 +83,24 @@ class ShardedPlan:
         self.collective_after = [self.plan.column_outputs(k) for k in range(self.plan.num_kernels)]
         self.executor = executor
         self.allreduce = allreduce
+        if outputs not in ("replicated", "sharded"):
+            raise ValueError("outputs must be 'replicated' or 'sharded'")
+        self.outputs = outputs
+        self.reduce_scatter = reduce_scatter
+        # column outputs reduce-scattered after kernel k (outputs="sharded")
+        self.scatter_after = [[] for _ in range(self.plan.num_kernels)]
+        if outputs == "sharded" and world > 1 and collective == "nccl":
+            roles = {b["name"]: b["role"] for b in self.desc["buffers"]}
+            lens = {b["name"]: b["rows"] * b["cols"] for b in self.desc["buffers"]}
+            kerns = self.desc["kernels"]
+            for k, names in enumerate(self.collective_after):
+                later = set()
+                for kk in kerns[k + 1:]:
+                    later.update(kk["inputs"])
+                for name in names:
+                    if (roles.get(name) == "output" and name not in later and lens[name] > 1
+                            and lens[name] % world == 0):
+                        self.scatter_after[k].append(name)
         # collective = "fused": column reductions of matrix kernels and the
         # dots of stream kernels finish in-kernel over peer memory
         # (mf_launch_kernel_peers); generic kernels still go through the
@@ -138,6 +166,15 @@ class ShardedPlan:
             return None
         return (1, self.r0, self.r1)
 
+    def column_slice(self, name: str):
+        """[begin, end) of a reduce-scattered column output this rank holds
+        finished (outputs="sharded"), or None if the output is replicated."""
+        if not any(name in names for names in self.scatter_after):
+            return None
+        b = next(x for x in self.desc["buffers"] if x["name"] == name)
+        chunk = b["rows"] * b["cols"] // self.world
+        return (self.rank * chunk, (self.rank + 1) * chunk)
+
     def local_shape(self, name: str):
         b = next(x for x in self.desc["buffers"] if x["name"] == name)
         return (b["rows"], b["cols"]) if b["rows"] > 1 else (b["cols"],)
@@ -151,6 +188,16 @@ class ShardedPlan:
         import torch.distributed as dist
         dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
 
+    def _reduce_scatter(self, t):
+        """In place: rank r's slice of t ends up holding the sum over ranks."""
+        if self.reduce_scatter is not None:
+            return self.reduce_scatter(t)
+        import torch.distributed as dist
+        flat = t.reshape(-1)
+        chunk = flat.numel() // self.world
+        dist.reduce_scatter_tensor(flat[self.rank * chunk:(self.rank + 1) * chunk], flat,
+                                   op=dist.ReduceOp.SUM, group=self.group)
+
     def check(self, stream=None) -> None:
         """Raises VmFault if an in-kernel peer barrier of this rank timed out
         (collective="fused"; a no-op otherwise)."""
@@ -163,6 +210,7 @@ class ShardedPlan:
         dot results right after the kernel that produced them."""
         collectives = 0
         fused = 0
+        scattered = 0
         for k in range(self.plan.num_kernels):
             if self.executor is not None:
                 self.executor(self.desc["kernels"][k], buffers, scalars)
@@ -174,7 +222,11 @@ class ShardedPlan:
             for name in self.collective_after[k]:
                 if name in self.fused_names[k] and self.peers is not None and self.executor is None:
                     continue  # reduced inside the kernel
-                self._allreduce(buffers[name])
+                if name in self.scatter_after[k]:
+                    self._reduce_scatter(buffers[name])
+                    scattered += 1
+                else:
+                    self._allreduce(buffers[name])
                 collectives += 1
         return {"kernels": self.plan.num_kernels, "collectives": collectives,
-                "fused_collectives": fused}
+                "fused_collectives": fused, "reduce_scatters": scattered}

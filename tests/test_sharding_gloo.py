@@ -205,3 +205,79 @@ def test_random_scripts_row_sharded_gloo(seed, world):
         s = np.asarray(S[name], np.float64).ravel()
         lim = 4 * TAU * s + 4 * np.spacing(np.abs(w).astype(np.float32)).astype(np.float64)
         assert np.all(np.abs(got - w) <= lim), (text, name)
+
+
+def _worker_scatter(rank, world, port, seq, m, n, seed, q):
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    sys.path.insert(0, os.path.join(root, "tests"))
+    from plan_emulator import run_kernel
+    from paper_1305_1183_b200.sharding import ShardedPlan
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        sp = ShardedPlan(seq, m, n, "fused", executor=run_kernel, outputs="sharded")
+        rng = np.random.default_rng(seed)
+        gd = sp.global_desc
+        full = {}
+        for b in gd["buffers"]:
+            shp = (b["rows"], b["cols"]) if b["rows"] > 1 else (b["cols"],)
+            full[b["name"]] = (rng.uniform(-1, 1, shp).astype(np.float32) if b["role"] == "input"
+                               else np.zeros(shp, np.float32))
+        scalars = {s: float(np.float32(0.25 + 0.5 * rng.random())) for s in gd["scalars"]}
+        local = {}
+        for name, a in full.items():
+            sl = sp.local_slice(name)
+            local[name] = torch.from_numpy((a if sl is None else a[sl[1]:sl[2]]).copy())
+        info = sp.launch(local, scalars)
+        outs = {}
+        for b in gd["buffers"]:
+            if b["role"] != "output":
+                continue
+            name = b["name"]
+            sl, cs = sp.local_slice(name), sp.column_slice(name)
+            part = local[name].numpy()
+            if cs is not None:  # only this rank's column slice is finished
+                part = part[cs[0]:cs[1]]
+            parts = [None] * world
+            dist.all_gather_object(parts, part)
+            outs[name] = parts[0] if (sl is None and cs is None) else np.concatenate(parts, axis=0)
+        if rank == 0:
+            inputs = dict(full)
+            inputs.update(scalars)
+            q.put((outs, inputs, info, [list(x) for x in sp.scatter_after]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("seq,m,n,world,scattered", [
+    ("ATAX", 192, 256, 2, ["y"]), ("BICGK", 256, 192, 2, ["s"]), ("SGEMVT", 160, 192, 2, []),
+    ("GEMVER", 256, 160, 2, []), ("BICGK", 320, 96, 3, ["s"]), ("ATAX", 96, 160, 3, []),
+])
+def test_reduce_scatter_for_sharded_consumers(seq, m, n, world, scattered):
+    """outputs="sharded": column outputs no later kernel reads are
+    reduce-scattered (rank r finishes slice r of n), intermediates a later
+    kernel reads (GEMVER's t) stay all-reduced, and so does an output whose
+    length is not a multiple of the rank count (ATAX n = 160 over 3 ranks).
+    The gathered slices match the oracle."""
+    from oracle import COracle
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker_scatter, args=(r, world, port, seq, m, n, 7, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    outs, inputs, info, scatter_after = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert sorted(x for names in scatter_after for x in names) == scattered
+    assert info["reduce_scatters"] == len(scattered)
+    co = COracle()
+    mp_, np_ = (m + 31) // 32 * 32, (n + 31) // 32 * 32
+    want = co.execute(seq, mp_, np_, inputs)
+    S = scale_bound(co, seq, mp_, np_, inputs)
+    for name, w in want.items():
+        check_output(seq, name, outs[name], w, S[name], exact=False)

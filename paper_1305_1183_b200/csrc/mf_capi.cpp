@@ -941,6 +941,9 @@ int mf_set_option(const char* key, int value) {
     } else if (k == "tma_consumers") {
       if (value != 0 && value != 256 && value != 512) throw Invalid("tma_consumers: 0|256|512");
       options().tma_consumers = value;
+    } else if (k == "matrix_tile_finalize") {
+      if (value < 0 || value > 2) throw Invalid("matrix_tile_finalize: 0 | 1 | 2");
+      options().matrix_tile_finalize = value;
     } else if (k == "rowres_cluster") {
       if (value < 0 || value > 6) throw Invalid("rowres_cluster: 0 (auto) | 1 .. 6");
       options().rowres_cluster = value;
@@ -995,6 +998,7 @@ int mf_get_option(const char* key) {
   if (k == "max_sms") return options().max_sms;
   if (k == "tma_consumers") return options().tma_consumers;
   if (k == "rowres_cluster") return options().rowres_cluster;
+  if (k == "matrix_tile_finalize") return options().matrix_tile_finalize;
   if (k == "stream_unroll") return options().stream_unroll;
   if (k == "stream_ctas_per_sm") return options().stream_ctas_per_sm;
   if (k == "generic") return mapfuse::plan::force_generic() ? 1 : 0;

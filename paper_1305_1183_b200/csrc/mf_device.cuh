@@ -163,12 +163,13 @@ __device__ __forceinline__ void for_each_slot_grouped(long long total, int tid, 
 // partials, row outputs (when the row was split over CB column chunks) sum
 // the CB chunk partials -- fixed order, so results are reproducible.
 template <int NROW, int NCOL, typename ACC>
-__device__ __forceinline__ void finalize(const MatrixArgs& a, int tid, int nthreads) {
+__device__ __forceinline__ void finalize(const MatrixArgs& a, int tid, int nthreads, bool do_rows = true,
+                                         bool do_cols = true) {
   const ACC* colpart = static_cast<const ACC*>(a.colpart);
   const ACC* rowpart = static_cast<const ACC*>(a.rowpart);
-  const bool need_rows = (NROW > 0) && a.CB > 1;
+  const bool need_rows = (NROW > 0) && a.CB > 1 && do_rows;
   const long long n4 = a.n / 4, m4 = a.m / 4;
-  const long long col_slots = (long long)NCOL * n4;
+  const long long col_slots = do_cols ? (long long)NCOL * n4 : 0;
   const long long total = col_slots + (need_rows ? (long long)NROW * m4 : 0);
   for_each_slot_grouped(total, tid, nthreads, [&](long long s, bool valid, int glane, bool lead) {
     ACC t[4];
@@ -196,6 +197,156 @@ __device__ __forceinline__ void finalize(const MatrixArgs& a, int tid, int nthre
       }
     }
   });
+}
+
+// ---------------------------------------------------------------------------
+// Tile-completion finalize (single GPU, option "matrix_tile_finalize": 1 row
+// outputs, 2 row and column outputs; 0, the default, finishes both after the
+// grid barrier).  When a CTA has written the partials of tile (cb, rb) it
+// counts the tile on arrival counters (MatrixArgs::tilecnt; acq_rel RMW after
+// a CTA barrier, so the whole CTA's partials are published with it); the LAST
+// arriver of a group finishes that group's sum in a fixed order, so results
+// do not depend on arrival order:
+//   [cb*NG + g]        tiles of column chunk cb in row-band group g (G bands):
+//                      last arriver sums the group's column partials into the
+//                      group's first slot (or straight into y when NG == 1);
+//   [CB*NG + cb]       finished groups of chunk cb: last sums the NG group
+//                      partials into y;
+//   [CB*NG + CB + rb]  finished column chunks of row band rb (row outputs
+//                      split over CB > 1 chunks): last sums the CB row partials.
+// Counters reset themselves (the last arriver stores 0).  Measured on B200
+// (DESIGN.md 5): in one-wave grids every chunk completes at the same moment,
+// and the grid barrier plus the grid-wide 8-lane finalize is as fast or
+// faster -- the last-arriver sums run on one CTA per chunk or band.
+__device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
+template <typename ACC>
+__device__ __forceinline__ void add4_cg(ACC (&t)[4], const ACC* q) {
+  if constexpr (sizeof(ACC) == 4) {
+    const float4 v = __ldcg(reinterpret_cast<const float4*>(q));
+    t[0] += v.x;
+    t[1] += v.y;
+    t[2] += v.z;
+    t[3] += v.w;
+  } else {
+    const double2 v0 = __ldcg(reinterpret_cast<const double2*>(q));
+    const double2 v1 = __ldcg(reinterpret_cast<const double2*>(q) + 1);
+    t[0] += v0.x;
+    t[1] += v0.y;
+    t[2] += v1.x;
+    t[3] += v1.y;
+  }
+}
+
+template <typename ACC>
+__device__ __forceinline__ void store4(ACC* q, const ACC (&t)[4]) {
+  if constexpr (sizeof(ACC) == 4) {
+    *reinterpret_cast<float4*>(q) = make_float4(t[0], t[1], t[2], t[3]);
+  } else {
+    reinterpret_cast<double2*>(q)[0] = make_double2(t[0], t[1]);
+    reinterpret_cast<double2*>(q)[1] = make_double2(t[2], t[3]);
+  }
+}
+
+// Column slots of chunk [c0, c0 + w): sum partial slots first, first + step,
+// ... (count of them) in that order; to_y: scale by ac and write y, else
+// write the sum back into slot `first`.
+template <int NCOL, typename ACC>
+__device__ __forceinline__ void sum_column_slots(const MatrixArgs& a, long long c0, long long w, int first,
+                                                 int step, int count, bool to_y, int tid, int nthr) {
+  ACC* colpart = static_cast<ACC*>(a.colpart);
+  const long long nslot = w / 4;
+#pragma unroll
+  for (int c = 0; c < NCOL; ++c) {
+    for (long long sl = tid; sl < nslot; sl += nthr) {
+      const long long j = c0 + 4 * sl;
+      ACC t[4] = {ACC(0), ACC(0), ACC(0), ACC(0)};
+      const ACC* q = colpart + ((long long)c * a.RB + first) * a.n + j;
+      const long long stride = (long long)step * a.n;
+#pragma unroll 8
+      for (int p = 0; p < count; ++p) add4_cg<ACC>(t, q + p * stride);
+      if (to_y) {
+        *reinterpret_cast<float4*>(a.yc[c] + j) =
+            make_float4((float)(a.ac[c] * (double)t[0]), (float)(a.ac[c] * (double)t[1]),
+                        (float)(a.ac[c] * (double)t[2]), (float)(a.ac[c] * (double)t[3]));
+      } else {
+        store4<ACC>(colpart + ((long long)c * a.RB + first) * a.n + j, t);
+      }
+    }
+  }
+}
+
+// Called by the nthr threads that wrote tile (cb, rb) (the whole CTA, or the
+// TMA kernel's consumer warps), right after its column partials; [r0, r1) are
+// the band's rows, C the chunk width.  sync() is a barrier over those threads.
+template <int NROW, int NCOL, typename ACC, typename Sync>
+__device__ __forceinline__ void tile_done(const MatrixArgs& a, int cb, int rb, long long C, long long r0,
+                                          long long r1, int tid, int nthr, unsigned* s_flag, Sync sync) {
+  const bool need_rows = (NROW > 0) && a.CB > 1 && a.tile_fin >= 1;
+  const bool cols = NCOL > 0 && a.tile_fin >= 2;
+  if (!cols && !need_rows) return;
+  unsigned* tc = a.tilecnt;
+  const int G = a.G, NG = a.NG, g = rb / G;
+  sync();  // every partial of this tile is written
+  if (tid == 0) {
+    unsigned f = 0;
+    if (cols) {
+      const unsigned gsize = (unsigned)min(G, a.RB - g * G);
+      unsigned* cnt = tc + (long long)cb * NG + g;
+      if (atom_add_acq_rel(cnt, 1u) == gsize - 1) {
+        *reinterpret_cast<volatile unsigned*>(cnt) = 0u;
+        f |= 1u;
+      }
+    }
+    if (need_rows) {
+      unsigned* cnt = tc + (long long)a.CB * NG + a.CB + rb;
+      if (atom_add_acq_rel(cnt, 1u) == (unsigned)a.CB - 1) {
+        *reinterpret_cast<volatile unsigned*>(cnt) = 0u;
+        f |= 2u;
+      }
+    }
+    *s_flag = f;
+  }
+  sync();
+  const unsigned f = *s_flag;
+  if (NCOL > 0 && (f & 1u)) {
+    const long long c0 = (long long)cb * C;
+    const long long w = min(C, a.n - c0);
+    const int gsize = min(G, a.RB - g * G);
+    sum_column_slots<NCOL, ACC>(a, c0, w, g * G, 1, gsize, NG == 1, tid, nthr);
+    if (NG > 1) {
+      sync();  // this group's sum is written
+      if (tid == 0) {
+        unsigned* cnt = tc + (long long)a.CB * NG + cb;
+        unsigned f2 = 0;
+        if (atom_add_acq_rel(cnt, 1u) == (unsigned)NG - 1) {
+          *reinterpret_cast<volatile unsigned*>(cnt) = 0u;
+          f2 = 1u;
+        }
+        *s_flag = f2;
+      }
+      sync();
+      if (*s_flag) sum_column_slots<NCOL, ACC>(a, c0, w, 0, G, NG, true, tid, nthr);
+    }
+  }
+  if (NROW > 0 && need_rows && (f & 2u)) {
+    const ACC* rowpart = static_cast<const ACC*>(a.rowpart);
+    const long long nr = r1 - r0;
+    for (long long q = tid; q < (long long)NROW * nr; q += nthr) {
+      const int o = (int)(q / nr);
+      const long long i = r0 + q % nr;
+      ACC t = ACC(0);
+      const ACC* p = rowpart + (long long)o * a.CB * a.m + i;
+#pragma unroll 8
+      for (int c = 0; c < a.CB; ++c) t += __ldcg(p + (long long)c * a.m);
+      a.yr[o][i] = (float)(a.ar[o] * (double)t);
+    }
+  }
+  sync();  // s_flag is reused by the next tile
 }
 
 // ---------------------------------------------------------------------------

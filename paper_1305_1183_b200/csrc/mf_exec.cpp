@@ -8,6 +8,7 @@
 #include "mf_exec.hpp"
 
 #include <algorithm>
+#include <cmath>
 #include <functional>
 #include <cstring>
 #include <sstream>
@@ -36,6 +37,7 @@ EngineOptions& options() {
     if (const char* v = std::getenv("MF_NVTX")) e.nvtx = std::atoi(v);
     if (const char* v = std::getenv("MF_GENERIC_CHECKED")) e.generic_checked = std::atoi(v);
     if (const char* v = std::getenv("MF_ROWRES_CLUSTER")) e.rowres_cluster = std::atoi(v);
+    if (const char* v = std::getenv("MF_MATRIX_TILE_FINALIZE")) e.matrix_tile_finalize = std::atoi(v);
     return e;
   }();
   return o;
@@ -68,6 +70,7 @@ Workspace::~Workspace() {
   for (void* p : retired_) cudaFree(p);
   if (scratch_) cudaFree(scratch_);
   if (counters_) cudaFree(counters_);
+  if (tile_) cudaFree(tile_);
   if (jit_fault_) cudaFree(jit_fault_);
   for (auto& [k, v] : named_) cudaFree(v.first);
 }
@@ -91,6 +94,18 @@ unsigned* Workspace::counters(cudaStream_t s) {
     check_cuda(cudaMemsetAsync(counters_, 0, 64 * sizeof(unsigned), s), "cudaMemset(counters)");
   }
   return counters_;
+}
+
+// Same growth rule as scratch(): launches already enqueued or recorded keep
+// the counters they were given.  Zeroed on allocation; kernels leave them 0.
+unsigned* Workspace::tile_counters(size_t words, cudaStream_t s) {
+  if (words <= tile_words_) return tile_;
+  if (tile_) retired_.push_back(tile_);
+  const size_t want = std::max(words, std::max<size_t>(256, tile_words_ * 2));
+  check_cuda(cudaMalloc(&tile_, want * sizeof(unsigned)), "cudaMalloc(tile counters)");
+  check_cuda(cudaMemsetAsync(tile_, 0, want * sizeof(unsigned), s), "cudaMemset(tile counters)");
+  tile_words_ = want;
+  return tile_;
 }
 
 unsigned* Workspace::jit_fault(cudaStream_t s) {
@@ -408,6 +423,12 @@ void run_matrix(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc, 
   a.colpart = base;
   a.rowpart = base + ((colb + 255) & ~size_t(255));
   a.bar = ws.counters(s);
+  // tile-completion finalize: column partials summed in groups of ~sqrt(RB)
+  // row bands, then over the groups (mf_device.cuh tile_done)
+  a.G = std::max(1, (int)std::ceil(std::sqrt((double)a.RB)));
+  a.NG = (a.RB + a.G - 1) / a.G;
+  a.tilecnt = ws.tile_counters((size_t)a.CB * a.NG + a.CB + a.RB, s);
+  a.tile_fin = eo.matrix_tile_finalize;
   if (t.tma)
     emit(rec, "launch " + k.name, [=](cudaStream_t st) { return launch_matrix_tma(sh, t, a, grid, st); }, s);
   else

@@ -42,6 +42,7 @@ struct EngineOptions {
   int tma = -1;  // matrix kernels: -1 auto (by shape), 1 = TMA ring, 0 = register-fed
   int max_sms = 0;  // > 0: cap the SMs a matrix kernel's grid is sized for
   int tma_consumers = 0;  // TMA matrix variant: 0 auto (by shape), 256 or 512 consumer threads
+  int matrix_tile_finalize = 0;  // matrix outputs finished on tile counters: 0 none, 1 rows, 2 rows + columns
   int rowres_cluster = 0;  // wide-row chain variant: 0 auto, 1 stage-held, 2 register-held, 3 8192-col slices
   // matrix operand loads: 0 evict-first L2 policy, 1 evict-normal, -1 auto =
   // evict-normal when the kernel also stores a matrix (GEMVER stage 1: 2036 ->
@@ -79,6 +80,7 @@ class Workspace {
   ~Workspace();
   void* scratch(size_t bytes, cudaStream_t s);   // grows on demand
   unsigned* counters(cudaStream_t s);            // zeroed once, self-resetting
+  unsigned* tile_counters(size_t words, cudaStream_t s);  // matrix tile counters, zeroed, self-resetting
   float* named(const std::string& key, int64_t words);  // persistent per key
   unsigned* jit_fault(cudaStream_t s);           // generic kernels' fault word pair, zeroed once
   bool jit_used() const { return jit_fault_ != nullptr; }
@@ -88,6 +90,8 @@ class Workspace {
   void* scratch_ = nullptr;
   size_t scratch_bytes_ = 0;
   unsigned* counters_ = nullptr;
+  unsigned* tile_ = nullptr;
+  size_t tile_words_ = 0;
   unsigned* jit_fault_ = nullptr;
   std::map<std::string, std::pair<float*, int64_t>> named_;
   std::vector<void*> retired_;  // outgrown buffers, freed with the workspace

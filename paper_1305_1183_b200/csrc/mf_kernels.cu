@@ -216,6 +216,7 @@ __global__ void __launch_bounds__(kThreads, 2) matrix_kernel(MatrixArgs a) {
   constexpr int NV = (NROW > 0 ? NROW : 1) * R;
   constexpr long long C = 4LL * kThreads * K;
   __shared__ ACC red[2][kWarps][NV];
+  __shared__ unsigned s_flag;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   ACC* colpart = static_cast<ACC*>(a.colpart);
   ACC* rowpart = static_cast<ACC*>(a.rowpart);
@@ -347,12 +348,22 @@ __global__ void __launch_bounds__(kThreads, 2) matrix_kernel(MatrixArgs a) {
 #pragma unroll
           for (int e = 0; e < 4; ++e) dst[e] = cacc[c][k][e];
         }
+    if (a.peer.nranks <= 1 && a.tile_fin > 0)  // single GPU: finish what this tile completes
+      tile_done<NROW, NCOL, ACC>(a, cb, rb, C, r0, r1, tid, kThreads, &s_flag, [] { __syncthreads(); });
   }
 
   if constexpr (NCOL > 0 || NROW > 0) {
     const bool need_rows = (NROW > 0) && a.CB > 1;
     MF_STAMP(1);
     if (NCOL == 0 && !need_rows) return;
+    if (a.peer.nranks <= 1) {
+      const bool rows_left = need_rows && a.tile_fin < 1, cols_left = NCOL > 0 && a.tile_fin < 2;
+      if (!rows_left && !cols_left) return;  // everything finished on tile counters
+      grid_barrier(a.bar);  // grid-wide fixed-order finalize
+      finalize<NROW, NCOL, ACC>(a, tid, kThreads, rows_left, cols_left);
+      return;
+    }
+    // row-sharded over several GPUs: cooperative grid, cross-rank finalize
     grid_barrier(a.bar);
     MF_STAMP(2);
     finalize_any<NROW, NCOL, ACC>(a, tid, kThreads);
@@ -518,7 +529,10 @@ cudaError_t launch_matrix(const MatrixShape& sh, const MatrixTuning& t, const Ma
                           int grid, cudaStream_t s) {
   MatrixFn fn = matrix_fn(sh, t);
   if (!fn) return cudaErrorNotSupported;
-  const bool needs_barrier = sh.ncol > 0 || (sh.nrow > 0 && a.CB > 1);
+  // only the cross-GPU finalize needs a co-resident grid (grid barrier)
+  const bool needs_barrier = a.peer.nranks > 1 ? (sh.ncol > 0 || (sh.nrow > 0 && a.CB > 1))
+                                                : ((sh.ncol > 0 && a.tile_fin < 2) ||
+                                                   (sh.nrow > 0 && a.CB > 1 && a.tile_fin < 1));
   MatrixArgs copy = a;
   void* args[] = {&copy};
   if (needs_barrier)

@@ -62,7 +62,10 @@ struct MatrixArgs {
   double ac[2] = {1.0, 1.0};
   void* colpart = nullptr;          // [NCOL][RB][n] accumulator type
   void* rowpart = nullptr;          // [NROW][CB][m] accumulator type
-  unsigned* bar = nullptr;          // grid barrier {count, generation}
+  unsigned* bar = nullptr;          // grid barrier {count, generation} (peer path)
+  unsigned* tilecnt = nullptr;      // tile-completion counters (local path; zeroed, self-resetting)
+  int G = 1, NG = 1;                // column finalize: row bands per group, groups
+  int tile_fin = 0;                 // finish on tile counters: 0 none, 1 row outputs, 2 rows + columns
   int CB = 1, RB = 1, tiles = 1;    // column chunks, row bands, CB*RB
   PeerLinks peer;                   // nranks > 1: fused cross-GPU column reduction
   int l2_normal = 0;                // matrix loads: 0 evict-first L2 policy, 1 evict-normal

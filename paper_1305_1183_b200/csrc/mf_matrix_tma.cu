@@ -102,6 +102,7 @@ __global__ void __launch_bounds__(NC + 32, 1) matrix_tma_kernel(MatrixArgs a, in
       reinterpret_cast<unsigned long long*>(sm_u + ((S * NRANK * R + 1) & ~1));
   unsigned long long* empty = full + S;
   __shared__ ACC red[2][kConsumerWarps][NV];
+  __shared__ unsigned s_flag;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) {
@@ -302,6 +303,9 @@ __global__ void __launch_bounds__(NC + 32, 1) matrix_tma_kernel(MatrixArgs a, in
 #pragma unroll
             for (int e = 0; e < 4; ++e) dst[e] = cacc[c][k][e];
           }
+      if (a.peer.nranks <= 1 && a.tile_fin > 0)  // single GPU: consumers finish what this tile completes
+        tile_done<NROW, NCOL, ACC>(a, cb, rb, C, r0, r1, tid, kConsumers, &s_flag,
+                                   [] { consumers_sync<NC>(); });
     }
     if constexpr (BULK) {
       // E must be in global memory before the grid barrier / kernel end
@@ -312,6 +316,14 @@ __global__ void __launch_bounds__(NC + 32, 1) matrix_tma_kernel(MatrixArgs a, in
   if constexpr (NCOL > 0 || NROW > 0) {
     const bool need_rows = (NROW > 0) && a.CB > 1;
     if (NCOL == 0 && !need_rows) return;
+    if (a.peer.nranks <= 1) {
+      const bool rows_left = need_rows && a.tile_fin < 1, cols_left = NCOL > 0 && a.tile_fin < 2;
+      if (!rows_left && !cols_left) return;  // everything finished on tile counters
+      grid_barrier(a.bar);  // grid-wide fixed-order finalize
+      finalize<NROW, NCOL, ACC>(a, tid, kTmaThreads, rows_left, cols_left);
+      return;
+    }
+    // row-sharded over several GPUs: cooperative grid, cross-rank finalize
     grid_barrier(a.bar);
     finalize_any<NROW, NCOL, ACC>(a, tid, kTmaThreads);
   }
@@ -421,7 +433,9 @@ cudaError_t launch_matrix_tma(const MatrixShape& sh, const MatrixTuning& t, cons
   if (!fn) return cudaErrorNotSupported;
   const size_t smem = tma_smem_bytes(sh, t);
   int S = tma_stages(sh, t);
-  const bool needs_barrier = sh.ncol > 0 || (sh.nrow > 0 && a.CB > 1);
+  const bool needs_barrier = a.peer.nranks > 1 ? (sh.ncol > 0 || (sh.nrow > 0 && a.CB > 1))
+                                                : ((sh.ncol > 0 && a.tile_fin < 2) ||
+                                                   (sh.nrow > 0 && a.CB > 1 && a.tile_fin < 1));
   MatrixArgs copy = a;
   void* args[] = {&copy, &S};
   if (needs_barrier)

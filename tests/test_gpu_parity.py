@@ -132,6 +132,37 @@ def test_tuning_variants(env, k, f64acc, tma):
         mf.set_option("tma", -1)
 
 
+@pytest.mark.parametrize("tile_fin", [1, 2])
+@pytest.mark.parametrize("tma", [0, 1])
+@pytest.mark.parametrize("f64acc", [0, 1])
+def test_tile_finalize_modes(env, tile_fin, tma, f64acc):
+    """Option matrix_tile_finalize: row (1) or row and column (2) outputs
+    finished by the last arriver on tile-completion counters instead of after
+    the grid barrier -- including grids with several tiles per CTA, chunk
+    groups (G x NG) and ragged last groups; repeated launches stay
+    bit-identical (the counters reset themselves)."""
+    torch, mf, co = env
+    mf.set_option("matrix_tile_finalize", tile_fin)
+    mf.set_option("tma", tma)
+    mf.set_option("f64acc", f64acc)
+    try:
+        for seq, m, n in [("BICGK", 4096, 20480), ("BICGK", 96, 64), ("GEMVER", 1024, 6144),
+                          ("GESUMMV", 2048, 8192), ("ATAX", 8192, 2048), ("BICGK", 16384, 4096)]:
+            vals = rand_inputs(seq, m, n, 11)
+            plan = mf.Plan.sequence(seq, m, n, "fused")
+            got = run_plan(torch, plan, vals, out_shapes(plan))
+            again = run_plan(torch, plan, vals, out_shapes(plan))
+            want = co.execute(seq, m, n, vals)
+            S = scale_bound(co, seq, m, n, vals)
+            for name in want:
+                check_output(seq, name, got[name], want[name], S[name])
+                assert np.array_equal(got[name], again[name]), (seq, name)
+    finally:
+        mf.set_option("matrix_tile_finalize", 0)
+        mf.set_option("tma", -1)
+        mf.set_option("f64acc", 0)
+
+
 def test_deterministic(env):
     torch, mf, co = env
     vals = rand_inputs("BICGK", 2048, 4096, 3)

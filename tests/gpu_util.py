@@ -48,5 +48,8 @@ def check_output(seq, name, got, want, S, exact=None):
     assert bad.size == 0, "%s.%s: %d elements exceed tau*S (worst ratio %.3g)" % (
         seq, name, bad.size, float(np.max(err / np.maximum(lim, 1e-300))))
     nw = float(np.max(err) / max(np.max(np.abs(want)), 1e-30))
-    assert nw <= NORMWISE, "%s.%s normwise %.3g" % (seq, name, nw)
+    # normwise bound on vectors only: for a 1x1 output (a dot) it is the
+    # relative error of one sum, which cancellation leaves unbounded in fp32
+    # arithmetic of any order -- the elementwise tau*S bound above covers it
+    assert got.size == 1 or nw <= NORMWISE, "%s.%s normwise %.3g" % (seq, name, nw)
     return {"max_scaled": float(np.max(err / np.maximum(S, 1e-30))), "normwise": nw}

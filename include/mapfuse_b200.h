@@ -275,7 +275,9 @@ int mf_generate(float* dev, int64_t rows, int64_t cols, int64_t ld, uint64_t see
  * vm::launch always counts like the VM), "nvtx" (0|1: NVTX ranges per
  * kernel), "codegen_barriers" (test hook, 0 = codegen omits barriers),
  * "tma" (-1 auto | 0 register-fed | 1 TMA ring matrix kernels),
- * "tma_consumers" (0 auto | 256 | 512), "rowres_cluster" (wide-row chain:
+ * "tma_consumers" (0 auto | 256 | 512), "rowres_variant" (row-resident chain
+ * with n <= 16384: 0 auto | 1 stage-held | 2 register-held rows),
+ * "rowres_cluster" (wide-row chain:
  * 0 auto | 1 .. 6, see mf_rowres.cu), "matrix_tile_finalize" (matrix
  * outputs finished on tile-completion counters instead of after a grid
  * barrier: 0 none | 1 row outputs | 2 row and column outputs),

@@ -944,6 +944,9 @@ int mf_set_option(const char* key, int value) {
     } else if (k == "matrix_tile_finalize") {
       if (value < 0 || value > 2) throw Invalid("matrix_tile_finalize: 0 | 1 | 2");
       options().matrix_tile_finalize = value;
+    } else if (k == "rowres_variant") {
+      if (value < 0 || value > 2) throw Invalid("rowres_variant: 0 (auto) | 1 | 2");
+      options().rowres_variant = value;
     } else if (k == "rowres_cluster") {
       if (value < 0 || value > 6) throw Invalid("rowres_cluster: 0 (auto) | 1 .. 6");
       options().rowres_cluster = value;
@@ -998,6 +1001,7 @@ int mf_get_option(const char* key) {
   if (k == "max_sms") return options().max_sms;
   if (k == "tma_consumers") return options().tma_consumers;
   if (k == "rowres_cluster") return options().rowres_cluster;
+  if (k == "rowres_variant") return options().rowres_variant;
   if (k == "matrix_tile_finalize") return options().matrix_tile_finalize;
   if (k == "stream_unroll") return options().stream_unroll;
   if (k == "stream_ctas_per_sm") return options().stream_ctas_per_sm;

@@ -37,6 +37,7 @@ EngineOptions& options() {
     if (const char* v = std::getenv("MF_NVTX")) e.nvtx = std::atoi(v);
     if (const char* v = std::getenv("MF_GENERIC_CHECKED")) e.generic_checked = std::atoi(v);
     if (const char* v = std::getenv("MF_ROWRES_CLUSTER")) e.rowres_cluster = std::atoi(v);
+    if (const char* v = std::getenv("MF_ROWRES_VARIANT")) e.rowres_variant = std::atoi(v);
     if (const char* v = std::getenv("MF_MATRIX_TILE_FINALIZE")) e.matrix_tile_finalize = std::atoi(v);
     return e;
   }();
@@ -321,11 +322,12 @@ void run_rowres(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc, 
          [=](cudaStream_t st) { return launch_rowres_cluster(a, variant, sms, st); }, s);
     return;
   }
-  check_cuda(rowres_config(m, n, sms, &a, &grid), ("configure " + k.name).c_str());
+  const int variant = rowres_variant(eo.rowres_variant, n);
+  check_cuda(rowres_config(m, n, sms, variant, &a, &grid), ("configure " + k.name).c_str());
   a.colpart = ws.scratch(sizeof(float) * (size_t)a.RB * (size_t)n + 256, s);
   a.bar = ws.counters(s);
   fill_peers(a, peers, n, k.name);
-  emit(rec, "launch " + k.name, [=](cudaStream_t st) { return launch_rowres(a, grid, st); }, s);
+  emit(rec, "launch " + k.name, [=](cudaStream_t st) { return launch_rowres(a, grid, variant, st); }, s);
 }
 
 void run_matrix(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc, cudaStream_t s,

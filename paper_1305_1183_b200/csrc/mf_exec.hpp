@@ -43,6 +43,7 @@ struct EngineOptions {
   int max_sms = 0;  // > 0: cap the SMs a matrix kernel's grid is sized for
   int tma_consumers = 0;  // TMA matrix variant: 0 auto (by shape), 256 or 512 consumer threads
   int matrix_tile_finalize = 0;  // matrix outputs finished on tile counters: 0 none, 1 rows, 2 rows + columns
+  int rowres_variant = 0;  // row-resident chain, n <= 16384: 0 auto, 1 stage-held, 2 register-held
   int rowres_cluster = 0;  // wide-row chain variant: 0 auto, 1 stage-held, 2 register-held, 3 8192-col slices
   // matrix operand loads: 0 evict-first L2 policy, 1 evict-normal, -1 auto =
   // evict-normal when the kernel also stores a matrix (GEMVER stage 1: 2036 ->

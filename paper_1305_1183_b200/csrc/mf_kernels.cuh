@@ -112,8 +112,10 @@ int tma_stages(const MatrixShape& sh, const MatrixTuning& t);
 
 // Row-resident chained reduction t = a*A x ; y = b*A^T t, one pass (mf_rowres.cu).
 long long rowres_max_cols();
-cudaError_t rowres_config(long long m, long long n, int sms, MatrixArgs* a, int* grid);
-cudaError_t launch_rowres(const MatrixArgs& a, int grid, cudaStream_t s);
+// variant: 1 stage-held rows, 2 register-held rows; rowres_variant maps 0 (auto)
+int rowres_variant(int requested, long long n);
+cudaError_t rowres_config(long long m, long long n, int sms, int variant, MatrixArgs* a, int* grid);
+cudaError_t launch_rowres(const MatrixArgs& a, int grid, int variant, cudaStream_t s);
 // Wide rows (16384 < n <= 131072): a cluster of ceil(n/16384) CTAs shares each
 // row over distributed shared memory, then a cooperative finalize kernel
 // combines the cluster bands' column partials (colpart [bands][n]).

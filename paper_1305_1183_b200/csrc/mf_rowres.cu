@@ -192,6 +192,119 @@ __global__ void __launch_bounds__(kRrThreads, 1) rowres_kernel(MatrixArgs a) {
   finalize_any<0, 1, float>(a, tid, kRrThreads);
 }
 
+// Register-held variant of rowres_kernel (option "rowres_variant" 2): 512
+// threads, no producer warp (16 warps = 4 per SM sub-partition, so 128
+// registers per thread).  Each thread loads its R x K float4 slots of the
+// stage into registers once; after the CTA reduction's barrier (every warp
+// has its copy) thread 0 refills that stage with the rows S stages ahead, so
+// all S stages stream from HBM while the CTA finishes the rows, and pass 2
+// runs from registers -- one shared-memory read per row instead of two.
+template <int K, int R>
+__global__ void __launch_bounds__(kRrConsumers, 1) rowres_reg_kernel(MatrixArgs a) {
+  constexpr int C = 4 * kRrConsumers * K;
+  constexpr int S = kRrStages;
+  extern __shared__ __align__(128) unsigned char smem[];
+  float* ring = reinterpret_cast<float*>(smem);  // stage = R rows of n floats (<= R*C)
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(ring + (size_t)S * R * C);
+  __shared__ float red[2][kRrWarps][R];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const long long r0 = (long long)blockIdx.x * a.m / gridDim.x;
+  const long long r1 = (long long)(blockIdx.x + 1) * a.m / gridDim.x;
+  const long long ngroups = (r1 - r0 + R - 1) / R;
+  const unsigned long long pol = evict_first_policy();
+  auto refill = [&](long long g) {  // thread 0: rows [r0 + g R, +R) -> stage g % S
+    const long long i = r0 + g * R;
+    const long long rows = (r1 - i) < R ? (r1 - i) : R;
+    const long long bytes = rows * a.n * 4;
+    const int stage = (int)(g % S);
+    rr_expect_tx(&full[stage], (unsigned)bytes);
+    const char* src = reinterpret_cast<const char*>(a.M[0] + i * a.ld);
+    char* dst = reinterpret_cast<char*>(ring + (size_t)stage * R * C);
+    for (long long off = 0; off < bytes; off += 16384) {
+      const long long piece = (bytes - off) < 16384 ? (bytes - off) : 16384;
+      rr_bulk(dst + off, src + off, (unsigned)piece, &full[stage], pol);
+    }
+  };
+  if (tid == 0) {
+    for (int st = 0; st < S; ++st) rr_mbar_init(&full[st], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (long long g = 0; g < S && g < ngroups; ++g) refill(g);
+  }
+  __syncthreads();
+  int lcol[K];
+  bool ok[K];
+  float4 xs[K];
+  float cacc[K][4];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    lcol[k] = 4 * (tid + kRrConsumers * k);
+    ok[k] = lcol[k] < a.n;
+    xs[k] = ok[k] ? __ldg(reinterpret_cast<const float4*>(a.xr[0] + lcol[k])) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) cacc[k][e] = 0.f;
+  }
+  int buf = 0;
+  for (long long g = 0; g < ngroups; ++g) {
+    const int stage = (int)(g % S);
+    const long long i0 = r0 + g * R;
+    const int nr = (r1 - i0) < R ? (int)(r1 - i0) : R;
+    rr_wait(&full[stage], (unsigned)((g / S) & 1));
+    const float* rows = ring + (size_t)stage * R * C;
+    float4 v[R][K];
+    float part[R];
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) {
+      part[rr] = 0.f;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        v[rr][k] = (rr < nr && ok[k]) ? *reinterpret_cast<const float4*>(rows + (size_t)rr * a.n + lcol[k])
+                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+        part[rr] = fmaf(v[rr][k].x, xs[k].x, part[rr]);
+        part[rr] = fmaf(v[rr][k].y, xs[k].y, part[rr]);
+        part[rr] = fmaf(v[rr][k].z, xs[k].z, part[rr]);
+        part[rr] = fmaf(v[rr][k].w, xs[k].w, part[rr]);
+      }
+    }
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) {
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) part[rr] += __shfl_xor_sync(0xffffffffu, part[rr], off);
+      if (lane == 0) red[buf][warp][rr] = part[rr];
+    }
+    __syncthreads();  // every warp holds the stage in registers: it is free
+    if (tid == 0 && g + S < ngroups) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      refill(g + S);
+    }
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) {
+      float s = red[buf][0][rr];
+#pragma unroll
+      for (int w = 1; w < kRrWarps; ++w) s += red[buf][w][rr];
+      // t_i rounded to fp32 exactly as the unfused plan stores it
+      const float ti = (float)(a.ar[0] * (double)s);
+      if (tid == 0 && a.yr[0] && rr < nr) a.yr[0][i0 + rr] = ti;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        cacc[k][0] = fmaf(v[rr][k].x, ti, cacc[k][0]);
+        cacc[k][1] = fmaf(v[rr][k].y, ti, cacc[k][1]);
+        cacc[k][2] = fmaf(v[rr][k].z, ti, cacc[k][2]);
+        cacc[k][3] = fmaf(v[rr][k].w, ti, cacc[k][3]);
+      }
+    }
+    buf ^= 1;
+  }
+  float* colpart = static_cast<float*>(a.colpart);
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+    if (ok[k]) {
+      float* dst = colpart + (long long)blockIdx.x * a.n + lcol[k];
+      *reinterpret_cast<float4*>(dst) = make_float4(cacc[k][0], cacc[k][1], cacc[k][2], cacc[k][3]);
+    }
+  grid_barrier(a.bar);
+  finalize_any<0, 1, float>(a, tid, kRrConsumers);
+}
+
 // ---------------------------------------------------------------------------
 // Wide rows (n > 16384): a thread-block CLUSTER of CL CTAs holds one row
 // between them -- CTA `crank` streams columns [crank*C, (crank+1)*C) of every
@@ -551,12 +664,16 @@ __global__ void __launch_bounds__(256) rowres_finalize_kernel(MatrixArgs a) {
 using RrFn = void (*)(MatrixArgs);
 
 // stage ~64 KB: R rows of the CTA's column span
-RrFn rowres_fn(long long n) {
-  if (n <= 4LL * kRrConsumers * 2) return rowres_kernel<2, 4>;
-  if (n <= 4LL * kRrConsumers * 4) return rowres_kernel<4, 2>;
-  if (n <= 4LL * kRrConsumers * 8) return rowres_kernel<8, 1>;
+// variant 1: stage-held rows (producer warp, two shared-memory reads per row);
+// 2: register-held rows (rowres_reg_kernel)
+RrFn rowres_fn(long long n, int variant) {
+  const bool reg = variant == 2;
+  if (n <= 4LL * kRrConsumers * 2) return reg ? rowres_reg_kernel<2, 4> : rowres_kernel<2, 4>;
+  if (n <= 4LL * kRrConsumers * 4) return reg ? rowres_reg_kernel<4, 2> : rowres_kernel<4, 2>;
+  if (n <= 4LL * kRrConsumers * 8) return reg ? rowres_reg_kernel<8, 1> : rowres_kernel<8, 1>;
   return nullptr;
 }
+int rowres_threads(int variant) { return variant == 2 ? kRrConsumers : kRrThreads; }
 
 size_t rowres_smem(long long n) {
   (void)n;
@@ -695,8 +812,17 @@ int rowres_cluster_bands(long long m, long long n, int sms, int variant) {
   return std::max(1, std::min<int>(nclusters, (int)std::min<long long>(m, 1 << 20)));
 }
 
-cudaError_t rowres_config(long long m, long long n, int sms, MatrixArgs* a, int* grid) {
-  RrFn fn = rowres_fn(n);
+// auto: register-held rows only for n <= 4096 (R = 4 rows per stage), where
+// they measured faster (tools/rowres_sweep.py, profiles/r02_rowres_variants.txt:
+// ATAX 131072x4096 330.8 vs 340.0 us); from 8192 columns up the stage-held
+// kernel's one-row lookahead wins (16384^2: 169.1 vs 174.1 us)
+int rowres_variant(int requested, long long n) {
+  if (requested == 1 || requested == 2) return requested;
+  return n <= 4LL * kRrConsumers * 2 ? 2 : 1;
+}
+
+cudaError_t rowres_config(long long m, long long n, int sms, int variant, MatrixArgs* a, int* grid) {
+  RrFn fn = rowres_fn(n, variant);
   if (!fn) return cudaErrorNotSupported;
   const size_t smem = rowres_smem(n);
   cudaError_t e = cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -710,12 +836,12 @@ cudaError_t rowres_config(long long m, long long n, int sms, MatrixArgs* a, int*
   return cudaSuccess;
 }
 
-cudaError_t launch_rowres(const MatrixArgs& a, int grid, cudaStream_t s) {
-  RrFn fn = rowres_fn(a.n);
+cudaError_t launch_rowres(const MatrixArgs& a, int grid, int variant, cudaStream_t s) {
+  RrFn fn = rowres_fn(a.n, variant);
   if (!fn) return cudaErrorNotSupported;
   MatrixArgs copy = a;
   void* args[] = {&copy};
-  return cudaLaunchCooperativeKernel((const void*)fn, dim3(grid), dim3(kRrThreads), args,
+  return cudaLaunchCooperativeKernel((const void*)fn, dim3(grid), dim3(rowres_threads(variant)), args,
                                      rowres_smem(a.n), s);
 }
 

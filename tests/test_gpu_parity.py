@@ -308,6 +308,28 @@ def test_b200_mode_row_resident_atax(env, m, n):
     assert np.all(err <= 2.0 ** -17 * S["y"] + np.spacing(np.abs(ref["y"])))
 
 
+@pytest.mark.parametrize("m,n", [(64, 64), (96, 160), (1024, 4096), (3008, 8192), (512, 16384), (4096, 2048)])
+def test_row_resident_variants(env, m, n):
+    """Option "rowres_variant" (n <= 16384): stage-held rows with a producer
+    warp, or register-held rows refilled by thread 0 -- same sums in the same
+    order, so bit-identical, and both within tolerance of the oracle."""
+    torch, mf, co = env
+    vals = rand_inputs("ATAX", m, n, 21 + m)
+    want = co.execute("ATAX", m, n, vals)
+    S = scale_bound(co, "ATAX", m, n, vals)
+    outs = {}
+    try:
+        for v in (1, 2):
+            mf.set_option("rowres_variant", v)
+            plan = mf.Plan.sequence("ATAX", m, n, "b200")
+            got = run_plan(torch, plan, vals, out_shapes(plan))
+            check_output("ATAX", "y", got["y"], want["y"], S["y"])
+            outs[v] = got["y"]
+    finally:
+        mf.set_option("rowres_variant", 0)
+    assert np.array_equal(outs[1], outs[2])
+
+
 @pytest.mark.parametrize("m,n", [(96, 20000), (320, 65536), (160, 131072), (2048, 32768)])
 def test_row_resident_cluster_variants(env, m, n):
     """Every wide-row chain variant (option "rowres_cluster": stage-held or

@@ -1,4 +1,5 @@
-"""Wide-row chain variants (option "rowres_cluster") on ATAX in planner mode
+"""Row-resident chain variants (option MF_SWEEP_OPTION: "rowres_cluster",
+the default, or "rowres_variant" for n <= 16384) on ATAX in planner mode
 b200: device time (median of 7, back-to-back launches are L2-cold at these
 sizes, the L2 is flushed anyway) and the outputs' agreement with variant 1.
 
@@ -39,6 +40,7 @@ def time_plan(plan, bufs, reps=7):
 
 specs = sys.argv[1:] or ["131072:131072", "32768:32768", "65536:65536"]
 variants = [int(v) for v in os.environ.get("MF_VARIANTS", "1,2,3").split(",")]
+OPTION = os.environ.get("MF_SWEEP_OPTION", "rowres_cluster")  # or rowres_variant (n <= 16384)
 for spec in specs:
     m, n = (int(x) for x in spec.split(":"))
     plan = mf.Plan.sequence("ATAX", m, n, "b200")
@@ -54,7 +56,7 @@ for spec in specs:
         bufs[b["name"]] = t
     ref = None
     for v in variants:
-        mf.set_option("rowres_cluster", v)
+        mf.set_option(OPTION, v)
         try:
             ms = time_plan(plan, bufs)
         except Exception as ex:  # unsupported shape for this variant
@@ -70,6 +72,6 @@ for spec in specs:
             agree = "bit-identical" if torch.equal(y, ref) else "max|dy|/max|y| = %.2e" % (diff / scale)
         print("ATAX %6dx%-6d variant %d: %9.1f us %7.0f GB/s  %.3f of HBM  (%s)" % (
             m, n, v, ms * 1e3, byts / ms / 1e6, byts / ms / 1e6 / PEAK, agree), flush=True)
-    mf.set_option("rowres_cluster", 0)
+    mf.set_option(OPTION, 0)
     del bufs
     torch.cuda.empty_cache()

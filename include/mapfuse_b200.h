@@ -278,7 +278,7 @@ int mf_generate(float* dev, int64_t rows, int64_t cols, int64_t ld, uint64_t see
  * "tma_consumers" (0 auto | 256 | 512), "rowres_variant" (row-resident chain
  * with n <= 16384: 0 auto | 1 stage-held | 2 register-held rows),
  * "rowres_cluster" (wide-row chain:
- * 0 auto | 1 .. 6, see mf_rowres.cu), "matrix_tile_finalize" (matrix
+ * 0 auto | 1 .. 7, see mf_rowres.cu), "matrix_tile_finalize" (matrix
  * outputs finished on tile-completion counters instead of after a grid
  * barrier: 0 none | 1 row outputs | 2 row and column outputs),
  * "max_sms" (0 = all SMs, else cap the

@@ -948,7 +948,7 @@ int mf_set_option(const char* key, int value) {
       if (value < 0 || value > 2) throw Invalid("rowres_variant: 0 (auto) | 1 | 2");
       options().rowres_variant = value;
     } else if (k == "rowres_cluster") {
-      if (value < 0 || value > 6) throw Invalid("rowres_cluster: 0 (auto) | 1 .. 6");
+      if (value < 0 || value > 7) throw Invalid("rowres_cluster: 0 (auto) | 1 .. 7");
       options().rowres_cluster = value;
     } else if (k == "max_sms") {
       if (value < 0) throw Invalid("max_sms >= 0");

@@ -65,6 +65,7 @@ struct MatrixArgs {
   unsigned* bar = nullptr;          // grid barrier {count, generation} (peer path)
   unsigned* tilecnt = nullptr;      // tile-completion counters (local path; zeroed, self-resetting)
   int G = 1, NG = 1;                // column finalize: row bands per group, groups
+  long long slice = 0;              // row-resident cluster: columns per CTA (0 = the kernel's chunk)
   int tile_fin = 0;                 // finish on tile counters: 0 none, 1 row outputs, 2 rows + columns
   int CB = 1, RB = 1, tiles = 1;    // column chunks, row bands, CB*RB
   PeerLinks peer;                   // nranks > 1: fused cross-GPU column reduction

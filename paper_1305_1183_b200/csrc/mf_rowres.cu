@@ -16,6 +16,8 @@
 //   barrier (or across GPUs in-kernel, see mf_device.cuh finalize_any).
 // Traffic: mn + 2n words instead of 2mn + m + 2n.  Planner mode "b200" only.
 #include <algorithm>
+#include <map>
+#include <mutex>
 
 #include "mf_device.cuh"
 #include "mf_kernels.cuh"
@@ -413,8 +415,9 @@ __global__ void __launch_bounds__(kRrThreads, 1) rowres_cluster_kernel(MatrixArg
   __shared__ __align__(8) unsigned long long xbar[kRcDepth];  // CL remote arrivals per slot
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned crank = cl_rank(), cid = cl_id(), ncl = cl_count();
-  const long long c0 = (long long)crank * C;
-  const long long width = a.n - c0 < C ? (a.n - c0 > 0 ? a.n - c0 : 0) : C;
+  const long long W = a.slice > 0 ? a.slice : C;  // this CTA's column slice (<= C)
+  const long long c0 = (long long)crank * W;
+  const long long width = a.n - c0 < W ? (a.n - c0 > 0 ? a.n - c0 : 0) : W;
   const long long r0 = (long long)cid * a.m / ncl, r1 = (long long)(cid + 1) * a.m / ncl;
   const long long nrows = r1 - r0;
   if (tid == 0) {
@@ -688,7 +691,10 @@ using RcFn = void (*)(MatrixArgs);
 //   2: the same slices, register-held rows with early stage release;
 //   3: 8192-column slices (K = 4), clusters of ceil(n/8192) <= 16
 //      (non-portable above 8), 6 x 32 KB stages, register-held rows;
-//   4, 5, 6: variants 1, 2, 3 with the exchange sent as st.async messages.
+//   4, 5, 6: variants 1, 2, 3 with the exchange sent as st.async messages;
+//   7: variant 4 with the cluster size that keeps the most SMs streaming
+//      (slices of ceil(n / CL) columns, up to 16384; n = 131072: 9 CTAs of
+//      14592 columns, 135 SMs, instead of 8 of 16384 on 120).
 struct RcVariant {
   int K, stages;
   bool reg;
@@ -700,7 +706,8 @@ struct RcVariant {
 RcVariant rc_variant(int v) {
   switch (v) {
     case 1:
-    case 4: return {8, 3, false};
+    case 4:
+    case 7: return {8, 3, false};
     case 3:
     case 6: return {4, 6, true};
     default: return {8, 3, true};
@@ -715,6 +722,7 @@ RcFn rc_fn_cl(int variant) {
       if constexpr (CL <= 8)
         return variant == 1 ? rowres_cluster_kernel<8, CL, 3, false> : rowres_cluster_kernel<8, CL, 3, true>;
       return nullptr;
+    case 7: return rowres_cluster_kernel<8, CL, 3, true>;
     case 3: return rowres_cluster_reg_kernel<4, CL, 6, false>;
     case 6: return rowres_cluster_reg_kernel<4, CL, 6, true>;
     case 5:
@@ -747,10 +755,70 @@ RcFn rowres_cluster_fn(int variant, int cl) {
   }
 }
 
-// fills cfg (grid left to the caller) for variant v at n columns; nullptr if unsupported
-RcFn rc_setup(int v, long long n, cudaLaunchConfig_t* cfg, cudaLaunchAttribute* attr, int* cl_out) {
+bool rc_attrs(RcFn fn, const RcVariant& var, int cl) {
+  if (cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)var.smem()) !=
+      cudaSuccess)
+    return false;
+  return cl <= 8 ||
+         cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess;
+}
+
+// variant 7: the cluster size in [ceil(n / 16384), 16] with the most
+// co-resident CTAs (ties: the smaller cluster), per device and n
+int rc_best_cluster(long long n, long long* slice) {
+  static std::mutex mu;
+  static std::map<std::pair<int, long long>, std::pair<int, long long>> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find({dev, n});
+  if (it != cache.end()) {
+    *slice = it->second.second;
+    return it->second.first;
+  }
+  const RcVariant var = rc_variant(7);
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int best = 0, best_cov = 0;
+  long long best_w = 0;
+  for (int cl = (int)((n + var.slice() - 1) / var.slice()); cl <= 16; ++cl) {
+    const long long w = ((n + cl - 1) / cl + 31) / 32 * 32;
+    if (w > var.slice() || (long long)(cl - 1) * w >= n) continue;  // every CTA gets columns
+    RcFn fn = rowres_cluster_fn(7, cl);
+    if (!fn || !rc_attrs(fn, var, cl)) continue;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cl;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.blockDim = dim3(var.threads());
+    cfg.dynamicSmemBytes = var.smem();
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cfg.gridDim = dim3(cl * std::max(1, sms / cl));
+    int nc = 0;
+    if (cudaOccupancyMaxActiveClusters(&nc, (const void*)fn, &cfg) != cudaSuccess) continue;
+    if (nc * cl > best_cov) {
+      best_cov = nc * cl;
+      best = cl;
+      best_w = w;
+    }
+  }
+  cudaGetLastError();
+  cache[{dev, n}] = {best, best_w};
+  *slice = best_w;
+  return best;
+}
+
+// fills cfg (grid left to the caller) for variant v at n columns; nullptr if
+// unsupported.  *slice_out: columns per CTA (0 = the variant's full slice).
+RcFn rc_setup(int v, long long n, cudaLaunchConfig_t* cfg, cudaLaunchAttribute* attr, int* cl_out,
+              long long* slice_out = nullptr) {
   const RcVariant var = rc_variant(v);
-  const int cl = (int)((n + var.slice() - 1) / var.slice());
+  long long slice = 0;
+  const int cl = v == 7 ? rc_best_cluster(n, &slice) : (int)((n + var.slice() - 1) / var.slice());
+  if (slice_out) *slice_out = slice;
   RcFn fn = rowres_cluster_fn(v, cl);
   if (!fn) return nullptr;
   if (cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)var.smem()) !=
@@ -779,7 +847,7 @@ long long rowres_cluster_max_cols() { return 16 * 8192; }
 // auto: variant 4 (tools/rowres_sweep.py on B200, profiles/r02_rowres_variants.txt:
 // ATAX 131072^2 11.27 ms vs 13.81 / 20.5 / 31.7 ms for variants 1 / 2 / 3)
 int rowres_cluster_variant(int requested, long long n) {
-  if (requested >= 1 && requested <= 6) return requested;
+  if (requested >= 1 && requested <= 7) return requested;
   (void)n;
   return 4;
 }
@@ -788,7 +856,7 @@ cudaError_t launch_rowres_cluster(MatrixArgs a, int variant, int finalize_grid, 
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
   int cl = 0;
-  RcFn fn = rc_setup(variant, a.n, &cfg, attr, &cl);
+  RcFn fn = rc_setup(variant, a.n, &cfg, attr, &cl, &a.slice);
   if (!fn) return cudaErrorNotSupported;
   cfg.stream = s;
   cfg.gridDim = dim3(cl * a.RB);  // a.RB = rowres_cluster_bands(m, n, sms): colpart is [RB][n]

@@ -342,7 +342,7 @@ def test_row_resident_cluster_variants(env, m, n):
     S = scale_bound(co, "ATAX", m, n, vals)
     outs = {}
     try:
-        for v in (1, 2, 3, 4, 5, 6):
+        for v in (1, 2, 3, 4, 5, 6, 7):
             mf.set_option("rowres_cluster", v)
             plan = mf.Plan.sequence("ATAX", m, n, "b200")
             got = run_plan(torch, plan, vals, out_shapes(plan))

@@ -43,23 +43,32 @@ def _obj(src):
         d = hashlib.sha1(f.read() + _key([]).encode()).hexdigest()[:12]
     o = os.path.join(OUT, os.path.basename(src) + "." + d + ".o")
     if not os.path.exists(o):
-        r = subprocess.run(["g++", "-std=c++20", "-O1", "-fPIC", "-Wall"] + INC + ["-c", src, "-o", o],
+        tmp = "%s.%d.tmp" % (o, os.getpid())
+        r = subprocess.run(["g++", "-std=c++20", "-O1", "-fPIC", "-Wall"] + INC + ["-c", src, "-o", tmp],
                            capture_output=True, text=True)
         if r.returncode:
             raise RuntimeError(r.stderr)
+        os.replace(tmp, o)
     return o
+
+
+def _link(exe, args):
+    """Links into a per-process temporary, then renames: concurrent test
+    workers (pytest -n) never exec a half-written binary."""
+    tmp = "%s.%d.tmp" % (exe, os.getpid())
+    r = subprocess.run(["g++", "-std=c++20", "-O1", "-Wall"] + INC + args + ["-o", tmp],
+                       capture_output=True, text=True)
+    if r.returncode:
+        raise RuntimeError(r.stderr[-4000:])
+    os.replace(tmp, exe)
+    return exe
 
 
 def build_tool(name, sources):
     """Compiles sources (with their own main) + host objects into OUT/name."""
     with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
         objs = list(ex.map(_obj, host_sources()))
-    exe = os.path.join(OUT, name)
-    r = subprocess.run(["g++", "-std=c++20", "-O1", "-Wall"] + INC + list(sources) + objs + LIBS +
-                       ["-o", exe], capture_output=True, text=True)
-    if r.returncode:
-        raise RuntimeError(r.stderr[-4000:])
-    return exe
+    return _link(os.path.join(OUT, name), list(sources) + objs + LIBS)
 
 
 def build_test(name, test_sources):
@@ -67,13 +76,10 @@ def build_test(name, test_sources):
     main = os.path.join(OUT, "doctest_main.cpp")
     os.makedirs(OUT, exist_ok=True)
     if not os.path.exists(main):
-        with open(main, "w") as f:
+        tmp = "%s.%d.tmp" % (main, os.getpid())
+        with open(tmp, "w") as f:
             f.write('#define DOCTEST_CONFIG_IMPLEMENT_WITH_MAIN\n#include "doctest.h"\n')
+        os.replace(tmp, main)
     with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
         objs = list(ex.map(_obj, host_sources() + [main]))
-    exe = os.path.join(OUT, name)
-    r = subprocess.run(["g++", "-std=c++20", "-O1", "-Wall"] + INC + list(test_sources) + objs + LIBS +
-                       ["-o", exe], capture_output=True, text=True)
-    if r.returncode:
-        raise RuntimeError(r.stderr[-4000:])
-    return exe
+    return _link(os.path.join(OUT, name), list(test_sources) + objs + LIBS)

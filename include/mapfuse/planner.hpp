@@ -183,6 +183,29 @@ int generic_by();
 // many iterations ahead (0 = auto: 4, 2 or 1 within 32 registers per thread).
 void set_generic_prefetch(int d);
 int generic_prefetch();
+// Engine option "generic_rewrite": which rewrites of the paper's literal
+// tile algorithm uninstrumented generic kernels use (host/cudagen.cpp); the
+// instrumented variants always run the literal algorithm.
+//   kRwRowReduce  a forwarded tile's rows summed by a warp reduce-scatter
+//                 (no transposed shared read, no shared atomics)
+//   kRwDefer      loop-body on-chip accumulators kept in registers until
+//                 after the serial iterations
+//   kRwGlobal     prologue copies of read-only vectors read from global
+//   kRwStore      a row reduction's store routine folded into its lanes
+//   kRwPrune      barriers the rewritten kernel no longer needs compiled out
+enum : int {
+  kRwRowReduce = 1,
+  kRwDefer = 2,
+  kRwGlobal = 4,
+  kRwStore = 8,
+  kRwPrune = 16,
+  kRwAll = 31,
+  // store folding measured slower (generic BiCGK 220 -> 720 us): the
+  // lanes' scattered row atomics replace one contiguous warp atomic per tile
+  kRwDefault = kRwRowReduce | kRwDefer | kRwGlobal | kRwPrune,
+};
+void set_generic_rewrite(int mask);
+int generic_rewrite();
 // Default implementation parameters of a generic kernel whose domain buffer
 // is dom_rows x dom_cols (a vector: 1 x length).
 CodegenParams generic_params(const kernel::KernelIR& k, int64_t dom_rows, int64_t dom_cols);

@@ -100,7 +100,11 @@ std::pair<int64_t, int64_t> domain_shape(const kernel::KernelIR& k, const script
 
 CodegenParams generic_params(const kernel::KernelIR& k, int64_t dom_rows, int64_t dom_cols) {
   CodegenParams p;
-  p.by = generic_by() > 0 ? generic_by() : 4;  // 32x4 blocks: measured best overall (sweep)
+  // 32x2 blocks: measured best once the uninstrumented rewrites apply
+  // (profiles/r02_generic_rewrite.txt: BiCGK 16384^2 220 -> 208-214 us, GEMVER
+  // 8192^2 153 -> 151 us, ATAX / GESUMMV equal); 32x4 was best for the
+  // literal tile algorithm
+  p.by = generic_by() > 0 ? generic_by() : 2;
   bool accumulates = false;
   for (const auto* sec : {&k.prologue, &k.epilogue})
     for (const auto& c : *sec) accumulates = accumulates || !c.is_pure_clear() || !c.clear_key.empty();

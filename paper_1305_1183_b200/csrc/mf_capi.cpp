@@ -979,6 +979,9 @@ int mf_set_option(const char* key, int value) {
     } else if (k == "generic_prefetch") {
       if (value < 0 || value > 8) throw Invalid("generic_prefetch: 0 (auto) .. 8");
       mapfuse::plan::set_generic_prefetch(value);
+    } else if (k == "generic_rewrite") {
+      if (value < 0 || value > mapfuse::plan::kRwAll) throw Invalid("generic_rewrite: a mask in 0 .. 31");
+      mapfuse::plan::set_generic_rewrite(value);
     } else if (k == "generic_iterations") {
       if (value < 0 || value > 4096) throw Invalid("generic_iterations: 0 (auto) .. 4096");
       mapfuse::plan::set_generic_iterations(value);
@@ -1010,6 +1013,7 @@ int mf_get_option(const char* key) {
   if (k == "generic_iterations") return mapfuse::plan::generic_iterations();
   if (k == "generic_by") return mapfuse::plan::generic_by();
   if (k == "generic_prefetch") return mapfuse::plan::generic_prefetch();
+  if (k == "generic_rewrite") return mapfuse::plan::generic_rewrite();
   if (k == "codegen_barriers") return mapfuse::plan::codegen_barriers() ? 1 : 0;
   if (k == "vm_exact") return mapfuse::vm::exact() ? 1 : 0;
   if (k == "nvtx") return options().nvtx;

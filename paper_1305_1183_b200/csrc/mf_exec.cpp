@@ -555,6 +555,13 @@ void run_generic(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc,
   if (options().generic_checked == 0 && prove_bounds(g, L, &fits32)) {
     fl.unchecked = true;  // cannot fault: drop the per-access checks
     fl.idx32 = fits32;
+    // every block's serial iterations lie inside the domain: the per-call
+    // "instance beyond the grid" predicate is constant true
+    if (g.depth == 2)
+      fl.exact = g.iter_dim == 'y' ? L.launch_y * g.iterations == L.a.full_y
+                                   : L.launch_x * g.iterations == L.a.full_x;
+    else
+      fl.exact = L.a.full_x * g.instances == L.a.n_elems && L.launch_x * g.iterations == L.a.full_x;
   }
   if (rec) jit_load(g.source, fl);  // compile + load now: nothing heavy inside a capture
   const std::string src = g.source;

@@ -87,9 +87,10 @@ std::vector<char> compile_cubin(const std::string& src, JitFlags fl, std::string
   const bool inst = fl.stats || fl.trace;  // instrumented kernels keep the VM's checks and widths
   const std::string d4 = std::string("-DMFJ_CHECKED=") + (fl.unchecked && !inst ? "0" : "1");
   const std::string d5 = std::string("-DMFJ_IDX32=") + (fl.idx32 && fl.unchecked && !inst ? "1" : "0");
+  const std::string d6 = std::string("-DMFJ_EXACT=") + (fl.exact && fl.unchecked && !inst ? "1" : "0");
   const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo", "-fmad=false",
-                        d1.c_str(), d2.c_str(), d3.c_str(), d4.c_str(), d5.c_str()};
-  rc = n.compile(prog, 9, opts);
+                        d1.c_str(), d2.c_str(), d3.c_str(), d4.c_str(), d5.c_str(), d6.c_str()};
+  rc = n.compile(prog, 10, opts);
   size_t ls = 0;
   n.log_size(prog, &ls);
   std::string log(ls, '\0');
@@ -110,7 +111,7 @@ std::vector<char> compile_cubin(const std::string& src, JitFlags fl, std::string
 std::shared_ptr<Module> module_for(const std::string& src, JitFlags fl) {
   const std::string key = std::string(fl.poison ? "P" : "N") + (fl.stats ? "S" : "-") +
                           (fl.trace ? "T" : "-") + (fl.unchecked ? "U" : "-") + (fl.idx32 ? "3" : "-") +
-                          src;
+                          (fl.exact ? "E" : "-") + src;
   {
     std::lock_guard<std::mutex> lk(g_mu);
     auto it = g_cache.find(key);

@@ -45,6 +45,8 @@ struct JitFlags {
   bool trace = false;  // the VM's access trace (implies stats)
   bool unchecked = false;  // every index proved in bounds at launch: no per-access checks
   bool idx32 = false;      // ... and every index value fits 32 bits: int index arithmetic
+  bool exact = false;      // ... and the grid's serial iterations cover the domain exactly:
+                           // no iteration of any block falls outside it
 };
 
 // Device fault codes written by generic kernels (first fault wins).

@@ -345,3 +345,74 @@ def test_acceptance_traffic_and_hoisting_on_reference_vm(mf):
         w = words("BICGK", m, n, "fused", it)
         assert w["p"][0] == 32 * w["__blocks"][0], it  # one 32-word p slice per block
         assert w["A"][0] == m * n
+
+
+REWRITES = {"rowreduce": 1, "defer": 2, "global": 4, "store": 8, "prune": 16}
+
+
+def _rewrite_markers(src):
+    return {"rowreduce": "warp row reduction" in src,
+            "defer": "deferred on-chip atomics" in src,
+            "store": "mfj_atg(a, " in src and "warp row reduction" in src,
+            "pruned": src.count("MFJ_CHECKED) __syncthreads();")}
+
+
+@pytest.mark.parametrize("seq,m,n,want", [
+    ("BICGK", 16384, 16384, {"rowreduce", "defer"}),
+    ("ATAX", 8192, 8192, {"rowreduce", "defer"}),
+    ("GESUMMV", 8192, 8192, {"rowreduce"}),
+    ("GEMVER", 8192, 8192, {"rowreduce", "defer"}),
+    ("AXPYDOT", 1, 1 << 24, {"defer"}),
+])
+def test_uninstrumented_rewrites_fire(generic, seq, m, n, want):
+    """The default Table-1 generic kernels take the rewrites of the literal
+    tile algorithm (host/cudagen.cpp: warp row reduction, deferred on-chip
+    accumulators, barrier pruning), every one guarded so the instrumented
+    variants (MFJ_STATS / TRACE / POISON / CHECKED) keep the literal
+    algorithm; option generic_rewrite=0 emits the literal algorithm alone."""
+    mf = generic
+    plan = mf.Plan.sequence(seq, m, n, "fused")
+    got, pruned = set(), 0
+    for k in range(plan.num_kernels):
+        src = plan.kernel_source(k)
+        mk = _rewrite_markers(src)
+        got |= {r for r in ("rowreduce", "defer") if mk[r]}
+        pruned += mk["pruned"]
+        assert not mk["store"], "store folding is off by default (measured slower)"
+        # a pruned barrier is compiled out of the uninstrumented variant only:
+        # every unconditional barrier of the literal kernel is still there
+        # for the instrumented ones
+        literal = len([l for l in src.splitlines() if l.strip() == "__syncthreads();"])
+        assert literal + mk["pruned"] > 0
+    assert want <= got, (seq, got)
+    assert pruned > 0 or seq == "AXPYDOT"
+    mf.set_option("generic_rewrite", 0)
+    try:
+        plan = mf.Plan.sequence(seq, m, n, "fused")
+        for k in range(plan.num_kernels):
+            mk = _rewrite_markers(plan.kernel_source(k))
+            assert not mk["rowreduce"] and not mk["defer"] and mk["pruned"] == 0
+    finally:
+        mf.set_option("generic_rewrite", 19 + 4)
+
+
+@pytest.mark.parametrize("mask", [0, 1, 2, 4, 8 + 1, 16, 31])
+@pytest.mark.parametrize("seq", ["BICGK", "ATAX", "GEMVER", "GESUMMV", "AXPYDOT"])
+def test_rewrite_masks_emit_and_compile(generic, seq, mask):
+    mf = generic
+    mf.set_option("generic_rewrite", mask)
+    try:
+        assert mf.get_option("generic_rewrite") == mask
+        m, n = (1, 1 << 16) if seq == "AXPYDOT" else (2048, 2048)
+        plan = mf.Plan.sequence(seq, m, n, "fused")
+        for k in range(plan.num_kernels):
+            mk = _rewrite_markers(plan.kernel_source(k))
+            if not mask & 1:
+                assert not mk["rowreduce"]
+            if not mask & 2:
+                assert not mk["defer"]
+            if not mask & 16:
+                assert mk["pruned"] == 0
+        plan.prepare()
+    finally:
+        mf.set_option("generic_rewrite", 23)

@@ -37,7 +37,7 @@ def generic(env):
     env[1].set_option("generic", 0)
 
 
-def run_per_kernel(torch, ref, plan, host, scalars):
+def run_per_kernel(torch, ref, plan, host, scalars, acc_floor=1e-30):
     """Kernel by kernel: GPU generic kernel vs the VM on the same inputs."""
     dev = {k: torch.from_numpy(v.copy()).cuda() for k, v in host.items()}
     d = plan.describe()
@@ -54,7 +54,7 @@ def run_per_kernel(torch, ref, plan, host, scalars):
             want = vm_in[name]
             if name in acc:
                 err = np.max(np.abs(got.astype(np.float64) - want))
-                assert err <= 1e-5 * max(np.max(np.abs(want)), 1e-30), (name, err)
+                assert err <= 1e-5 * max(np.max(np.abs(want)), acc_floor), (name, err)
             else:
                 bad = np.count_nonzero(got != want)
                 assert bad == 0, "%s: %d elements differ from the reference VM" % (name, bad)
@@ -111,6 +111,27 @@ def test_prefetch_distance_vs_oracle(generic, seq, m, n, d):
     S = scale_bound(co, seq, m, n, vals)
     for name in want:
         check_output(seq, name, got[name], want[name], S[name], exact=False)
+
+
+@pytest.mark.parametrize("mask", [0, 1, 3, 23, 31])
+@pytest.mark.parametrize("seq,m,n", [("BICGK", 1024, 2016), ("ATAX", 640, 384), ("GEMVER", 512, 768),
+                                     ("GESUMMV", 256, 1024), ("AXPYDOT", 1, 100032)])
+def test_rewrite_masks_vs_reference_vm(generic, seq, m, n, mask):
+    """Each combination of the uninstrumented rewrites (host/cudagen.cpp:
+    1 warp row reduction, 2 deferred on-chip accumulators, 4 prologue vectors
+    from global, 8 row-reduction stores folded, 16 barrier pruning; 0 the
+    literal tile algorithm), kernel by kernel against the reference VM."""
+    torch, mf, ref, co = generic
+    mf.set_option("generic_rewrite", mask)
+    try:
+        plan = mf.Plan.sequence(seq, m, n, "fused")
+        host = host_buffers(plan, {}, np.random.default_rng(mask + 3))
+        sc = {s: 0.5 for s in plan.describe()["scalars"]}
+        # accumulated outputs: 1e-5 x max(|y|, 1), as the VM-exact tests --
+        # a cancelling dot keeps the absolute error of its unit-scale summands
+        run_per_kernel(torch, ref, plan, host, sc, acc_floor=1.0)
+    finally:
+        mf.set_option("generic_rewrite", 23)
 
 
 @pytest.mark.parametrize("script", sorted(USER_SCRIPTS))

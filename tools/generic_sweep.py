@@ -54,8 +54,14 @@ def main():
     ap.add_argument("--its", default="0,1,4,16,64")
     ap.add_argument("--bys", default="0")
     ap.add_argument("--only", default="", help="comma-separated sequences")
+    ap.add_argument("--opt", action="append", default=[], help="engine option key=value (repeatable)")
     a = ap.parse_args()
     mf.set_option("generic", 1)
+    for kv in a.opt:
+        k, v = kv.split("=")
+        mf.set_option(k, int(v))
+    if a.opt:
+        print("# options: " + " ".join(a.opt), flush=True)
     only = set(a.only.upper().split(",")) if a.only else None
     for seq, m, n in CASES:
         if only and seq not in only:

@@ -199,10 +199,11 @@ enum : int {
   kRwGlobal = 4,
   kRwStore = 8,
   kRwPrune = 16,
-  kRwAll = 31,
+  kRwLatePrefetch = 32,  // depth 2: next tile's loads issued after the current tile's last use
+  kRwAll = 63,
   // store folding measured slower (generic BiCGK 220 -> 720 us): the
   // lanes' scattered row atomics replace one contiguous warp atomic per tile
-  kRwDefault = kRwRowReduce | kRwDefer | kRwGlobal | kRwPrune,
+  kRwDefault = kRwRowReduce | kRwDefer | kRwGlobal | kRwPrune | kRwLatePrefetch,
 };
 void set_generic_rewrite(int mask);
 int generic_rewrite();

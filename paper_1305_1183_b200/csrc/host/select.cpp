@@ -123,6 +123,10 @@ CodegenParams generic_params(const kernel::KernelIR& k, int64_t dom_rows, int64_
   // depth 1: 32 iterations when the kernel reduces (half the blocks, half the
   // global atomics: AXPYDOT 0.47 -> 0.53 of HBM), else 16 (VADD 0.95)
   int64_t want = forced >= 1 ? forced : (k.depth == 1 ? (accumulates ? 32 : 16) : (accumulates ? 4 : 1));
+  // depth 2 with accumulators: 8 serial iterations while that still leaves
+  // >= 16 waves of 4 blocks per SM (generic BiCGK 16384^2: 196 -> 179 us;
+  // 8192^2 shapes have too few tiles and measured equal or slower)
+  if (forced < 1 && k.depth == 2 && accumulates && (limit / 8) * blocks_per_band >= 148 * 4 * 16) want = 8;
   // keep >= 4 blocks per SM (148 SMs)
   while (want > 1 && (limit / want) * blocks_per_band < 148 * 4 && forced < 1) want /= 2;
   int64_t it = std::max<int64_t>(1, std::min(want, limit));

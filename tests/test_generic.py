@@ -393,10 +393,10 @@ def test_uninstrumented_rewrites_fire(generic, seq, m, n, want):
             mk = _rewrite_markers(plan.kernel_source(k))
             assert not mk["rowreduce"] and not mk["defer"] and mk["pruned"] == 0
     finally:
-        mf.set_option("generic_rewrite", 19 + 4)
+        mf.set_option("generic_rewrite", 55)
 
 
-@pytest.mark.parametrize("mask", [0, 1, 2, 4, 8 + 1, 16, 31])
+@pytest.mark.parametrize("mask", [0, 1, 2, 4, 8 + 1, 16, 31, 55, 63])
 @pytest.mark.parametrize("seq", ["BICGK", "ATAX", "GEMVER", "GESUMMV", "AXPYDOT"])
 def test_rewrite_masks_emit_and_compile(generic, seq, mask):
     mf = generic
@@ -415,4 +415,4 @@ def test_rewrite_masks_emit_and_compile(generic, seq, mask):
                 assert mk["pruned"] == 0
         plan.prepare()
     finally:
-        mf.set_option("generic_rewrite", 23)
+        mf.set_option("generic_rewrite", 55)

@@ -113,7 +113,7 @@ def test_prefetch_distance_vs_oracle(generic, seq, m, n, d):
         check_output(seq, name, got[name], want[name], S[name], exact=False)
 
 
-@pytest.mark.parametrize("mask", [0, 1, 3, 23, 31])
+@pytest.mark.parametrize("mask", [0, 1, 3, 23, 31, 55])
 @pytest.mark.parametrize("seq,m,n", [("BICGK", 1024, 2016), ("ATAX", 640, 384), ("GEMVER", 512, 768),
                                      ("GESUMMV", 256, 1024), ("AXPYDOT", 1, 100032)])
 def test_rewrite_masks_vs_reference_vm(generic, seq, m, n, mask):
@@ -131,7 +131,7 @@ def test_rewrite_masks_vs_reference_vm(generic, seq, m, n, mask):
         # a cancelling dot keeps the absolute error of its unit-scale summands
         run_per_kernel(torch, ref, plan, host, sc, acc_floor=1.0)
     finally:
-        mf.set_option("generic_rewrite", 23)
+        mf.set_option("generic_rewrite", 55)
 
 
 @pytest.mark.parametrize("script", sorted(USER_SCRIPTS))

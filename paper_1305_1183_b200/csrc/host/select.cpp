@@ -35,12 +35,12 @@ CostModel CostModel::defaults() {
       {"matrix.rowres", 0.88},     // row-resident chain (ATAX one pass, 16384^2)
       {"matrix.rowres.cluster", 0.95},  // ... rows over a CTA cluster (n > 16384), st.async exchange:
                                         //   32768^2 1.08, 131072^2 0.93 (profiles/r02_rowres_variants.txt)
-      {"generic.d1", 0.70},        // NVRTC-emitted KernelIR (host/cudagen.cpp), depth 1,
-                                   //   prefetch 4 ahead: VADD 0.93, AXPYDOT 0.53
-                                   //   (profiles/r01_generic_sweep_pf.txt)
-      {"generic.d2", 0.60},        // ... depth 2 (BY 4, pipelined, proved bounds, 32-bit indices):
-                                   //   BiCGK 0.54, ATAX 0.70, GEMVER 0.74, GESUMMV 0.68
-                                   //   (profiles/r01_generic_sweep_pf.txt)
+      {"generic.d1", 0.78},        // NVRTC-emitted KernelIR (host/cudagen.cpp), depth 1,
+                                   //   prefetch 4 ahead, deferred accumulators: VADD 0.93,
+                                   //   AXPYDOT 0.63 (profiles/r02_generic_rewrite.txt)
+      {"generic.d2", 0.82},        // ... depth 2 (BY 2, pipelined, proved bounds, round-2 rewrites):
+                                   //   BiCGK 0.90, ATAX 0.81, GEMVER 0.81, GESUMMV 0.81
+                                   //   (profiles/r02_generic_rewrite.txt)
   };
   if (const char* f = std::getenv("MF_COST_DB")) {
     std::ifstream in(f);

@@ -941,6 +941,12 @@ int mf_set_option(const char* key, int value) {
     } else if (k == "tma_consumers") {
       if (value != 0 && value != 256 && value != 512) throw Invalid("tma_consumers: 0|256|512");
       options().tma_consumers = value;
+    } else if (k == "matrix_waves") {
+      if (value < 1 || value > 16) throw Invalid("matrix_waves: 1 .. 16");
+      options().matrix_waves = value;
+    } else if (k == "matrix_dynamic") {
+      if (value != 0 && value != 1) throw Invalid("matrix_dynamic: 0 | 1");
+      options().matrix_dynamic = value;
     } else if (k == "matrix_tile_finalize") {
       if (value < 0 || value > 2) throw Invalid("matrix_tile_finalize: 0 | 1 | 2");
       options().matrix_tile_finalize = value;
@@ -1006,6 +1012,8 @@ int mf_get_option(const char* key) {
   if (k == "rowres_cluster") return options().rowres_cluster;
   if (k == "rowres_variant") return options().rowres_variant;
   if (k == "matrix_tile_finalize") return options().matrix_tile_finalize;
+  if (k == "matrix_waves") return options().matrix_waves;
+  if (k == "matrix_dynamic") return options().matrix_dynamic;
   if (k == "stream_unroll") return options().stream_unroll;
   if (k == "stream_ctas_per_sm") return options().stream_ctas_per_sm;
   if (k == "generic") return mapfuse::plan::force_generic() ? 1 : 0;

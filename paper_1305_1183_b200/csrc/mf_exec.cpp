@@ -392,6 +392,8 @@ void run_matrix(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc, 
   t.K = eo.matrix_k == 4 ? 4 : 2;
   t.f64acc = eo.f64acc != 0;
   t.occupancy = std::max(1, eo.occupancy);
+  t.waves = std::max(1, eo.matrix_waves);
+  t.dynamic = eo.matrix_dynamic != 0;
   // Variant choice (the implementation generator's role):
   // shapes that stream a matrix back out (ger2's B) or carry the rank-2
   // update need the deep TMA ring to keep enough bytes in flight; read-only

@@ -51,6 +51,11 @@ struct EngineOptions {
   // evict-first for read-only kernels (BiCGK 159.7 -> 157.7 us)
   int matrix_l2_normal = -1;
   int tma_bulk_store = 1;  // TMA store shapes: 1 = E leaves through cp.async.bulk S2G, 0 = st.global
+  // register-fed matrix kernels: row bands per co-resident CTA (1 = one tile
+  // per CTA) and whether CTAs past their first tile take the next one from a
+  // counter (1) or round-robin (0)
+  int matrix_waves = 1;
+  int matrix_dynamic = 0;
   int generic_poison = 0;
   int nvtx = 0;
   int generic_checked = 0;  // 1: generic kernels keep per-access checks even when proved in bounds  // 1: an NVTX range around every kernel launch (named after the plan kernel)  // 1: generic kernels poison on-chip memory (VM fault on uninitialised reads)

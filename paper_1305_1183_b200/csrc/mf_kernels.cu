@@ -217,13 +217,21 @@ __global__ void __launch_bounds__(kThreads, 2) matrix_kernel(MatrixArgs a) {
   constexpr long long C = 4LL * kThreads * K;
   __shared__ ACC red[2][kWarps][NV];
   __shared__ unsigned s_flag;
+  __shared__ int s_next;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   ACC* colpart = static_cast<ACC*>(a.colpart);
   ACC* rowpart = static_cast<ACC*>(a.rowpart);
   int buf = 0;
   const unsigned long long pol = matrix_policy(a.l2_normal);
 
-  for (int tile = blockIdx.x; tile < a.tiles; tile += gridDim.x) {
+  // Tile schedule: the first tile is blockIdx.x; later ones round-robin, or
+  // (a.dyn) from a counter -- the CTA that finishes first takes the next, so
+  // the last wave is balanced.  A tile's partials depend only on the tile,
+  // never on which CTA computed it, so results stay deterministic.  The next
+  // index is fetched at the start of a tile and read at its end.
+  int tile = blockIdx.x;
+  if (a.dyn && tid == 0) s_next = (int)gridDim.x + (int)atomicAdd(a.bar + 4, 1u);
+  for (; tile < a.tiles;) {
     const int cb = tile % a.CB, rb = tile / a.CB;
     const long long r0 = (long long)rb * a.m / a.RB, r1 = (long long)(rb + 1) * a.m / a.RB;
     long long col[K];
@@ -350,6 +358,21 @@ __global__ void __launch_bounds__(kThreads, 2) matrix_kernel(MatrixArgs a) {
         }
     if (a.peer.nranks <= 1 && a.tile_fin > 0)  // single GPU: finish what this tile completes
       tile_done<NROW, NCOL, ACC>(a, cb, rb, C, r0, r1, tid, kThreads, &s_flag, [] { __syncthreads(); });
+    if (a.dyn) {
+      __syncthreads();  // s_next was written a whole tile ago
+      tile = s_next;
+      __syncthreads();
+      if (tid == 0 && tile < a.tiles) s_next = (int)gridDim.x + (int)atomicAdd(a.bar + 4, 1u);
+    } else {
+      tile += gridDim.x;
+    }
+  }
+  if (a.dyn && tid == 0) {  // the last CTA to run out of tiles resets the counters
+    __threadfence();
+    if (atomicAdd(a.bar + 5, 1u) == gridDim.x - 1) {
+      atomicExch(a.bar + 4, 0u);
+      atomicExch(a.bar + 5, 0u);
+    }
   }
 
   if constexpr (NCOL > 0 || NROW > 0) {
@@ -517,7 +540,9 @@ cudaError_t matrix_config(const MatrixShape& sh, const MatrixTuning& t, long lon
     RB = std::max(1LL, std::min(m / 4, std::max(1LL, G / CB)));
     g = std::min<long long>(G, (long long)CB * RB);
   }
+  if (t.waves > 1) RB = std::min(RB * t.waves, std::max(RB, m / 8));
   const long long tiles = (long long)CB * RB;
+  a->dyn = t.dynamic && tiles > g ? 1 : 0;
   a->CB = CB;
   a->RB = (int)RB;
   a->tiles = (int)tiles;

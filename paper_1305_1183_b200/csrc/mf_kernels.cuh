@@ -70,6 +70,8 @@ struct MatrixArgs {
   int CB = 1, RB = 1, tiles = 1;    // column chunks, row bands, CB*RB
   PeerLinks peer;                   // nranks > 1: fused cross-GPU column reduction
   int l2_normal = 0;                // matrix loads: 0 evict-first L2 policy, 1 evict-normal
+  int dyn = 0;                      // tiles after blockIdx.x from counter bar[4] (bar[5] counts
+                                    // exhausted CTAs; the last one resets both)
 };
 
 // Shape of a matrix-kernel instantiation.
@@ -86,6 +88,8 @@ struct MatrixTuning {
   bool tma = true;     // TMA/mbarrier shared-memory ring (mf_matrix_tma.cu)
   int consumers = 256; // TMA variant: consumer threads per CTA (256 | 512)
   bool bulk_store = false;  // TMA variant, store shapes: E leaves through cp.async.bulk S2G
+  int waves = 1;        // register-fed variant: tiles per co-resident CTA
+  bool dynamic = false; // ... tiles after the first taken from a counter
 };
 
 // Launchers; return cudaSuccess or the launch error.  `sms` = SM count.

@@ -115,7 +115,7 @@ def test_prefetch_distance_vs_oracle(generic, seq, m, n, d):
 
 @pytest.mark.parametrize("mask", [0, 1, 3, 23, 31, 55])
 @pytest.mark.parametrize("seq,m,n", [("BICGK", 1024, 2016), ("ATAX", 640, 384), ("GEMVER", 512, 768),
-                                     ("GESUMMV", 256, 1024), ("AXPYDOT", 1, 100032)])
+                                     ("GESUMMV", 256, 1024), ("AXPYDOT", 1, 4096)])
 def test_rewrite_masks_vs_reference_vm(generic, seq, m, n, mask):
     """Each combination of the uninstrumented rewrites (host/cudagen.cpp:
     1 warp row reduction, 2 deferred on-chip accumulators, 4 prologue vectors
@@ -132,6 +132,27 @@ def test_rewrite_masks_vs_reference_vm(generic, seq, m, n, mask):
         run_per_kernel(torch, ref, plan, host, sc, acc_floor=1.0)
     finally:
         mf.set_option("generic_rewrite", 55)
+
+
+@pytest.mark.parametrize("mask", [0, 23, 31, 55])
+@pytest.mark.parametrize("seq,m,n", [("AXPYDOT", 1, 100032), ("BICGK", 4096, 4096), ("GEMVER", 2048, 2048)])
+def test_rewrite_masks_vs_oracle(generic, seq, m, n, mask):
+    """Larger problems per rewrite mask, whole plan against the C oracle
+    with the S-scaled tolerance (a 10^5-term dot's fp32 rounding depends on
+    the summation order, which the rewrites change)."""
+    torch, mf, ref, co = generic
+    from test_gpu_parity import out_shapes, rand_inputs, run_plan
+    mf.set_option("generic_rewrite", mask)
+    try:
+        vals = rand_inputs(seq, m, n, 21 + mask)
+        plan = mf.Plan.sequence(seq, m, n, "fused")
+        got = run_plan(torch, plan, vals, out_shapes(plan))
+    finally:
+        mf.set_option("generic_rewrite", 55)
+    want = co.execute(seq, m, n, vals)
+    S = scale_bound(co, seq, m, n, vals)
+    for name in want:
+        check_output(seq, name, got[name], want[name], S[name], exact=False)
 
 
 @pytest.mark.parametrize("script", sorted(USER_SCRIPTS))

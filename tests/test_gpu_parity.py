@@ -163,6 +163,43 @@ def test_tile_finalize_modes(env, tile_fin, tma, f64acc):
         mf.set_option("f64acc", 0)
 
 
+@pytest.mark.parametrize("waves,dyn", [(2, 0), (2, 1), (4, 1), (8, 1)])
+@pytest.mark.parametrize("tile_fin", [0, 2])
+def test_matrix_tile_schedules(env, waves, dyn, tile_fin):
+    """Options matrix_waves (row bands per co-resident CTA) and
+    matrix_dynamic (tiles after the first from a self-resetting counter): a
+    tile's partials depend only on the tile, so outputs match the oracle and
+    repeated launches -- with tiles landing on different CTAs -- stay
+    bit-identical to each other and to the static round-robin schedule."""
+    torch, mf, co = env
+    cases = [("BICGK", 4096, 20480), ("BICGK", 96, 64), ("GESUMMV", 2048, 8192), ("ATAX", 8192, 2048),
+             ("BICGK", 16384, 4096)]
+    mf.set_option("matrix_tile_finalize", tile_fin)
+    try:
+        for seq, m, n in cases:
+            vals = rand_inputs(seq, m, n, 13)
+            mf.set_option("matrix_waves", waves)
+            mf.set_option("matrix_dynamic", 0)
+            sp = mf.Plan.sequence(seq, m, n, "fused")
+            static = run_plan(torch, sp, vals, out_shapes(sp))
+            mf.set_option("matrix_dynamic", dyn)
+            plan = mf.Plan.sequence(seq, m, n, "fused")
+            got = run_plan(torch, plan, vals, out_shapes(plan))
+            for _ in range(3):
+                again = run_plan(torch, plan, vals, out_shapes(plan))
+                for name in got:
+                    assert np.array_equal(got[name], again[name]), (seq, name)
+            want = co.execute(seq, m, n, vals)
+            S = scale_bound(co, seq, m, n, vals)
+            for name in want:
+                check_output(seq, name, got[name], want[name], S[name])
+                assert np.array_equal(got[name], static[name]), (seq, name, "dynamic != static")
+    finally:
+        mf.set_option("matrix_waves", 1)
+        mf.set_option("matrix_dynamic", 0)
+        mf.set_option("matrix_tile_finalize", 0)
+
+
 def test_deterministic(env):
     torch, mf, co = env
     vals = rand_inputs("BICGK", 2048, 4096, 3)

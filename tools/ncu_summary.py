@@ -52,6 +52,7 @@ def main():
     traffic_path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                                 "profiles", "ncu_traffic.json")
     traffic = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
+    seen = set()
     print("| report | kernel | " + " | ".join(s for _, s in METRICS) + " |")
     print("|---" * (len(METRICS) + 2) + "|")
     for path in sys.argv[1:]:
@@ -63,9 +64,16 @@ def main():
             name = d["kernel"].replace("(anonymous namespace)::", "").replace("|", "/")
             print("| %s | `%s` | %s |" % (os.path.basename(path), name[:90], " | ".join(cells)))
             if "dram_read" in d and "dram_write" in d:
+                # per kernel: the largest launch of the reports given (a tiny
+                # warm-up or edge-case launch of the same template must not
+                # replace the representative one)
                 key = name.split("(")[0]
-                traffic[key] = {"dram_bytes_per_launch": to_bytes(*d["dram_read"]) + to_bytes(*d["dram_write"]),
-                                "source": os.path.basename(path)}
+                b = to_bytes(*d["dram_read"]) + to_bytes(*d["dram_write"])
+                if key not in seen or b > traffic[key]["dram_bytes_per_launch"]:
+                    traffic[key] = {"dram_bytes_per_launch": b, "source": os.path.basename(path)}
+                    if os.environ.get("MF_CAPTURE_LABEL"):  # e.g. "round-2 capture, commit abc1234"
+                        traffic[key]["captured"] = os.environ["MF_CAPTURE_LABEL"]
+                    seen.add(key)
     with open(traffic_path, "w") as f:
         json.dump(traffic, f, indent=1, sort_keys=True)
 

@@ -17,7 +17,10 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("seq,m,n,P", [("BICGK", 2048, 4096, 2), ("BICGK", 4096, 2048, 4),
-                                       ("ATAX", 1024, 3072, 2), ("GEMVER", 1024, 2048, 2)])
+                                       ("ATAX", 1024, 3072, 2), ("GEMVER", 1024, 2048, 2),
+                                       # full-width panels: every column chunk and a multi-band grid per rank
+                                       ("BICGK", 32768, 16384, 4), ("GEMVER", 8192, 8192, 2),
+                                       ("ATAX", 16384, 8192, 2)])
 @pytest.mark.parametrize("tma", [0, 1])
 def test_virtual_ranks_fused_column_reduction(seq, m, n, P, tma):
     import torch

@@ -311,3 +311,27 @@ def test_random_kernels_text_boundary_round_trip():
             qd = mf.Plan.from_kernel_text(p.kernel_text(k), m, n).describe()["kernels"][0]
             for key in ("kind", "shape", "inputs", "outputs"):
                 assert qd.get(key) == d["kernels"][k].get(key), (seed, k, key, text)
+
+
+@pytest.mark.parametrize("key,good,bad", [
+    ("matrix_waves", [1, 2, 16], [0, 17]),
+    ("matrix_dynamic", [0, 1], [2, -1]),
+    ("generic_rewrite", [0, 23, 55, 63], [-1, 64]),
+    ("matrix_tile_finalize", [0, 1, 2], [3]),
+])
+def test_engine_option_ranges(key, good, bad):
+    """Engine options round-trip through mf_set_option / mf_get_option and
+    out-of-range values are rejected with MF_ERR_INVALID (the previous value
+    stays)."""
+    before = mf.get_option(key)
+    try:
+        for v in good:
+            mf.set_option(key, v)
+            assert mf.get_option(key) == v
+        last = mf.get_option(key)
+        for v in bad:
+            with pytest.raises(Exception, match=key):
+                mf.set_option(key, v)
+            assert mf.get_option(key) == last
+    finally:
+        mf.set_option(key, before)

@@ -5,6 +5,11 @@
 
 --generic: every plan on the generic path (NVRTC-emitted KernelIR,
 host/cudagen.cpp), plus the user functions of tests/golden/generic.mf.
+--generic-fast: the generic path WITHOUT poisoning, so bounds are proved and
+           the uninstrumented variant runs -- the round-2 rewrites (warp row
+           reduction, deferred accumulators, global vectors, pruned barriers,
+           late prefetch) -- on shapes with several serial iterations; each
+           plan also with every rewrite mask of interest (generic_rewrite).
 --mutate:  fused BiCGK with codegen's barriers suppressed: the
            racecheck run is EXPECTED to report hazards.
 """
@@ -20,10 +25,16 @@ CASES = [("AXPYDOT", 1, 4096), ("VADD", 1, 4096), ("WAXPBY", 1, 2080), ("BICGK",
          ("ATAX", 160, 96), ("GEMVER", 128, 4128), ("GESUMMV", 64, 2080), ("SGEMVT", 96, 160),
          ("MADD", 64, 96), ("SSCAL", 1, 96), ("SGEMV", 64, 64)]
 GENERIC = "--generic" in sys.argv
+FAST = "--generic-fast" in sys.argv
 MUTATE = "--mutate" in sys.argv
 if GENERIC or MUTATE:
     mf.set_option("generic", 1)
     mf.set_option("generic_poison", 1)
+if FAST:
+    mf.set_option("generic", 1)
+    mf.set_option("generic_poison", 0)
+    CASES = [("AXPYDOT", 1, 1 << 16), ("BICGK", 1024, 1024), ("ATAX", 512, 512), ("GEMVER", 512, 1024),
+             ("GESUMMV", 512, 512), ("SGEMVT", 512, 256), ("BICGK", 256, 4096)]
 if MUTATE:
     mf.set_option("codegen_barriers", 0)
     CASES = [("BICGK", 128, 128)]
@@ -40,7 +51,7 @@ def run(plan, sc):
         bufs[b["name"]] = t
     plan.launch(bufs, sc)
     torch.cuda.synchronize()
-    if GENERIC:
+    if GENERIC or FAST:
         plan.check()
 
 
@@ -52,6 +63,19 @@ if GENERIC:
     for s, m, n in USER_SCRIPTS.values():
         for mode in ("fused", "unfused"):
             run(mf.Plan.compile(s, m, n, mode, manifest=lib), {})
+if FAST:
+    for mask in (55, 23, 31, 63):
+        mf.set_option("generic_rewrite", mask)
+        mf.set_option("generic_iterations", 0)
+        for seq, m, n in CASES:
+            run(mf.Plan.sequence(seq, m, n, "fused"), {"alpha": 0.5, "beta": 0.25})
+        mf.set_option("generic_iterations", 8)  # several serial iterations even at these sizes
+        for seq, m, n in CASES:
+            run(mf.Plan.sequence(seq, m, n, "fused"), {"alpha": 0.5, "beta": 0.25})
+    mf.set_option("generic_iterations", 0)
+    mf.set_option("generic_rewrite", 55)
+    print("sanitize target done")
+    sys.exit(0)
 for tma in ((0,) if GENERIC or MUTATE else (0, 1)):
     mf.set_option("tma", tma)
     for seq, m, n in CASES:

@@ -121,40 +121,48 @@ __device__ __forceinline__ double fmacc<double>(double a, double b, double c) {
   return fma(a, b, c);
 }
 
-// Cross-CTA partial sums, parallel and deterministic: 8 lanes cooperate on one
-// float4 slot (lane g of the group sums partials g, g+8, g+16, ... in order;
-// a fixed xor butterfly combines the 8), so a slot with 148 partials costs
-// ~19 dependent L2 loads per lane instead of 148.  Loop trip counts are
-// warp-uniform so every shuffle has all 32 lanes.
+// Cross-CTA partial sums, parallel and deterministic: G lanes cooperate on
+// one float4 slot (lane g of the group sums partials g, g+G, g+2G, ... in
+// order; a fixed xor butterfly combines the G), so a slot with 148 partials
+// costs ~19 dependent L2 loads per lane at G = 8 instead of 148.  G is 8;
+// option "finalize_group" fixes 16 or 32 (measured equal or slower on every
+// shape, profiles/r02_finalize_group.txt: the finalize is not bound by that
+// chain).  A launch-constant G keeps the summation order, and the result, the
+// same on every launch.  Loop trip counts are warp-uniform so every shuffle
+// has all 32 lanes.
 constexpr int kFinGroup = 8;
+
+__device__ __forceinline__ int fin_group(int fixed) {
+  return (fixed == 16 || fixed == 32) ? fixed : kFinGroup;
+}
 
 template <typename ACC>
 __device__ __forceinline__ void group_sum4(const ACC* base, long long stride, int count, bool valid,
-                                           int glane, ACC (&t)[4]) {
+                                           int glane, int G, ACC (&t)[4]) {
   t[0] = t[1] = t[2] = t[3] = ACC(0);
   if (valid)
 #pragma unroll 4
-    for (int b = glane; b < count; b += kFinGroup) {
+    for (int b = glane; b < count; b += G) {
       const ACC* q = base + (long long)b * stride;
 #pragma unroll
       for (int e = 0; e < 4; ++e) t[e] += __ldcg(q + e);
     }
-#pragma unroll
-  for (int off = kFinGroup / 2; off > 0; off >>= 1)
+  for (int off = G / 2; off > 0; off >>= 1)
 #pragma unroll
     for (int e = 0; e < 4; ++e) t[e] += __shfl_xor_sync(0xffffffffu, t[e], off);
 }
 
-// Visits slots [0, total) in warp-uniform rounds; f(slot, valid, glane, lead).
+// Visits slots [0, total) in warp-uniform rounds, G lanes per slot;
+// f(slot, valid, glane, lead).
 template <typename F>
-__device__ __forceinline__ void for_each_slot_grouped(long long total, int tid, int nthreads, F&& f) {
+__device__ __forceinline__ void for_each_slot_grouped(long long total, int tid, int nthreads, int G, F&& f) {
   const int lane = tid & 31;
-  const int glane = lane % kFinGroup;
+  const int glane = lane % G;
   const long long warps_total = (long long)gridDim.x * (nthreads / 32);
   const long long gwarp = (long long)blockIdx.x * (nthreads / 32) + tid / 32;
-  constexpr int per_warp = 32 / kFinGroup;
+  const int per_warp = 32 / G;
   for (long long first = gwarp * per_warp; first < total; first += warps_total * per_warp) {
-    const long long slot = first + lane / kFinGroup;
+    const long long slot = first + lane / G;
     f(slot, slot < total, glane, glane == 0 && slot < total);
   }
 }
@@ -171,15 +179,17 @@ __device__ __forceinline__ void finalize(const MatrixArgs& a, int tid, int nthre
   const long long n4 = a.n / 4, m4 = a.m / 4;
   const long long col_slots = do_cols ? (long long)NCOL * n4 : 0;
   const long long total = col_slots + (need_rows ? (long long)NROW * m4 : 0);
-  for_each_slot_grouped(total, tid, nthreads, [&](long long s, bool valid, int glane, bool lead) {
+  const int G = fin_group(a.fin_g);
+  for_each_slot_grouped(total, tid, nthreads, G, [&](long long s, bool valid, int glane, bool lead) {
     ACC t[4];
     // invalid lanes only occur past the last slot: follow that region's branch
-    // so each warp's shuffles stay convergent (col_slots is a multiple of 8)
+    // so each warp's shuffles stay convergent (col_slots is a multiple of 8,
+    // a warp holds 32 / G <= 4 slots)
     const bool col_branch = valid ? (s < col_slots) : !need_rows;
     if (col_branch) {
       const int c = valid ? (int)(s / n4) : 0;
       const long long j = valid ? (s % n4) * 4 : 0;
-      group_sum4<ACC>(colpart + (long long)c * a.RB * a.n + j, a.n, a.RB, valid && NCOL > 0, glane, t);
+      group_sum4<ACC>(colpart + (long long)c * a.RB * a.n + j, a.n, a.RB, valid && NCOL > 0, glane, G, t);
       if (lead && NCOL > 0) {
         float4 o = make_float4((float)(a.ac[c] * (double)t[0]), (float)(a.ac[c] * (double)t[1]),
                                (float)(a.ac[c] * (double)t[2]), (float)(a.ac[c] * (double)t[3]));
@@ -189,7 +199,7 @@ __device__ __forceinline__ void finalize(const MatrixArgs& a, int tid, int nthre
       const long long q = valid ? s - col_slots : 0;
       const int o = (int)(q / m4);
       const long long i = (q % m4) * 4;
-      group_sum4<ACC>(rowpart + (long long)o * a.CB * a.m + i, a.m, a.CB, valid, glane, t);
+      group_sum4<ACC>(rowpart + (long long)o * a.CB * a.m + i, a.m, a.CB, valid, glane, G, t);
       if (lead) {
         float4 r = make_float4((float)(a.ar[o] * (double)t[0]), (float)(a.ar[o] * (double)t[1]),
                                (float)(a.ar[o] * (double)t[2]), (float)(a.ar[o] * (double)t[3]));
@@ -395,12 +405,13 @@ __device__ __forceinline__ void finalize_columns_peers(const MatrixArgs& a, int 
   const long long slice4 = n4 / pl.nranks;  // n / P is a multiple of 4 (n % 32 == 0, P <= 8)
   const long long P = pl.nranks;
   // Phase A: local sums -> owner's inbox[c][rank][j]
-  for_each_slot_grouped((long long)NCOL * n4, tid, nthreads,
+  const int G = fin_group(a.fin_g);
+  for_each_slot_grouped((long long)NCOL * n4, tid, nthreads, G,
                         [&](long long s, bool valid, int glane, bool lead) {
     const int c = valid ? (int)(s / n4) : 0;
     const long long j4 = valid ? s % n4 : 0, j = j4 * 4;
     ACC t[4];
-    group_sum4<ACC>(colpart + (long long)c * a.RB * a.n + j, a.n, a.RB, valid, glane, t);
+    group_sum4<ACC>(colpart + (long long)c * a.RB * a.n + j, a.n, a.RB, valid, glane, G, t);
     if (!lead) return;
     const int owner = (int)min(j4 / slice4, P - 1);
     float4 v = make_float4((float)t[0], (float)t[1], (float)t[2], (float)t[3]);
@@ -451,12 +462,13 @@ __device__ __forceinline__ void finalize_rows(const MatrixArgs& a, int tid, int 
   if (NROW == 0 || a.CB <= 1) return;
   const ACC* rowpart = static_cast<const ACC*>(a.rowpart);
   const long long m4 = a.m / 4;
-  for_each_slot_grouped((long long)NROW * m4, tid, nthreads,
+  const int G = fin_group(a.fin_g);
+  for_each_slot_grouped((long long)NROW * m4, tid, nthreads, G,
                         [&](long long q, bool valid, int glane, bool lead) {
     const int o = valid ? (int)(q / m4) : 0;
     const long long i = valid ? (q % m4) * 4 : 0;
     ACC t[4];
-    group_sum4<ACC>(rowpart + (long long)o * a.CB * a.m + i, a.m, a.CB, valid, glane, t);
+    group_sum4<ACC>(rowpart + (long long)o * a.CB * a.m + i, a.m, a.CB, valid, glane, G, t);
     if (!lead) return;
     float4 r = make_float4((float)(a.ar[o] * (double)t[0]), (float)(a.ar[o] * (double)t[1]),
                            (float)(a.ar[o] * (double)t[2]), (float)(a.ar[o] * (double)t[3]));

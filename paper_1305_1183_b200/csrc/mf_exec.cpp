@@ -308,6 +308,7 @@ void run_rowres(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc, 
   const EngineOptions& eo = options();
   const int sms = eo.max_sms > 0 ? std::min(eo.max_sms, device_sm_count()) : device_sm_count();
   int grid = 0;
+  a.fin_g = eo.finalize_group;
   if (n > rowres_max_cols()) {  // wide rows: a CTA cluster per row (distributed shared memory)
     const int variant = rowres_cluster_variant(eo.rowres_cluster, n);
     const int bands = rowres_cluster_bands(m, n, sms, variant);
@@ -433,6 +434,7 @@ void run_matrix(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc, 
   a.NG = (a.RB + a.G - 1) / a.G;
   a.tilecnt = ws.tile_counters((size_t)a.CB * a.NG + a.CB + a.RB, s);
   a.tile_fin = eo.matrix_tile_finalize;
+  a.fin_g = eo.finalize_group;
   if (t.tma)
     emit(rec, "launch " + k.name, [=](cudaStream_t st) { return launch_matrix_tma(sh, t, a, grid, st); }, s);
   else

@@ -309,8 +309,9 @@ void run_rowres(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc, 
   const int sms = eo.max_sms > 0 ? std::min(eo.max_sms, device_sm_count()) : device_sm_count();
   int grid = 0;
   a.fin_g = eo.finalize_group;
-  if (n > rowres_max_cols()) {  // wide rows: a CTA cluster per row (distributed shared memory)
-    const int variant = rowres_cluster_variant(eo.rowres_cluster, n);
+  if (n > rowres_max_cols() || eo.rowres_force_cluster) {  // wide rows: a CTA cluster per row (DSMEM)
+    const int variant = n > rowres_max_cols() || eo.rowres_cluster ? rowres_cluster_variant(eo.rowres_cluster, n)
+                                                                   : 7;
     const int bands = rowres_cluster_bands(m, n, sms, variant);
     if (bands <= 0) throw Fault("kernel " + k.name + ": no co-resident CTA cluster for n = " + std::to_string(n));
     a.CB = 1;

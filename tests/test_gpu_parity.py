@@ -42,7 +42,8 @@ def run_plan(torch, plan, vals, outputs_shape):
 
 def out_shapes(plan):
     d = plan.describe()
-    return {b["name"]: ((b["rows"], b["cols"]) if b["rows"] > 1 else (b["cols"],))
+    # a matrix with zero rows is still a matrix (rows == 1 marks a vector)
+    return {b["name"]: ((b["rows"], b["cols"]) if b["rows"] != 1 else (b["cols"],))
             for b in d["buffers"] if b["role"] == "output"}
 
 
@@ -411,6 +412,25 @@ def test_empty_problems(env, seq, m, n):
     got = run_plan(torch, plan, vals, shapes)
     for name, v in got.items():
         assert v.size == 0 or np.all(v == 0), (name, v[:4])
+
+
+@pytest.mark.parametrize("seq,m,n,mode", [("GEMVER", 0, 64, "fused"), ("GEMVER", 64, 0, "fused"),
+                                          ("GEMVER", 0, 96, "unfused"), ("WAXPBY", 1, 0, "fused"),
+                                          ("ATAX", 0, 96, "b200"), ("ATAX", 64, 0, "b200"),
+                                          ("GESUMMV", 0, 64, "unfused"), ("BICGK", 0, 2048, "unfused")])
+def test_empty_problems_vs_oracle(env, seq, m, n, mode):
+    """Empty dimensions against the oracle, including outputs that are not
+    zero: GEMVER with m = 0 has x = beta * B^T y + z = z (an empty column sum
+    plus a map), so the map kernels downstream of an empty reduction must
+    still run."""
+    torch, mf, co = env
+    vals = rand_inputs(seq, m, n, 5)
+    plan = mf.Plan.sequence(seq, m, n, mode)
+    got = run_plan(torch, plan, vals, out_shapes(plan))
+    want = co.execute(seq, m, n, vals)
+    for name in want:
+        w = np.asarray(want[name], np.float32).reshape(got[name].shape)
+        assert np.allclose(got[name], w, rtol=1e-6, atol=1e-7), (seq, name)
 
 
 # Stream-kernel layouts: one CTA per 512-float4 block (default) and a capped

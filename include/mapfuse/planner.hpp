@@ -200,7 +200,8 @@ enum : int {
   kRwStore = 8,
   kRwPrune = 16,
   kRwLatePrefetch = 32,  // depth 2: next tile's loads issued after the current tile's last use
-  kRwAll = 63,
+  kRwWarpVector = 64,    // body copies of a warp-width vector slice held in registers, read by shuffle
+  kRwAll = 127,
   // store folding measured slower (generic BiCGK 220 -> 720 us): the
   // lanes' scattered row atomics replace one contiguous warp atomic per tile
   kRwDefault = kRwRowReduce | kRwDefer | kRwGlobal | kRwPrune | kRwLatePrefetch,

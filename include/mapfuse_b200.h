@@ -270,10 +270,11 @@ int mf_generate(float* dev, int64_t rows, int64_t cols, int64_t ld, uint64_t see
  * "generic_iterations" (0 = per size, else the serial iterations of generic
  * kernels), "generic_by" (0 = default, else block rows of depth-2 generic
  * kernels), "generic_prefetch" (0 = auto, else how many iterations ahead
- * generic kernels issue their loads), "generic_rewrite" (mask, default 31:
+ * generic kernels issue their loads), "generic_rewrite" (mask, default 55:
  * 1 warp row reduction, 2 deferred on-chip accumulators, 4 prologue vectors
- * read from global, 8 row-reduction stores folded, 16 barrier pruning; 0 =
- * the paper's literal tile algorithm), "generic_checked" (0|1: keep per-access
+ * read from global, 8 row-reduction stores folded, 16 barrier pruning, 32
+ * late tile prefetch, 64 warp vectors; 0 = the paper's literal tile
+ * algorithm), "generic_checked" (0|1: keep per-access
  * index checks even when the bounds are proved at launch), "vm_exact" (0|1:
  * vm::launch always counts like the VM), "nvtx" (0|1: NVTX ranges per
  * kernel), "codegen_barriers" (test hook, 0 = codegen omits barriers),

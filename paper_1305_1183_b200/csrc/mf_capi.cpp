@@ -992,7 +992,7 @@ int mf_set_option(const char* key, int value) {
       if (value < 0 || value > 8) throw Invalid("generic_prefetch: 0 (auto) .. 8");
       mapfuse::plan::set_generic_prefetch(value);
     } else if (k == "generic_rewrite") {
-      if (value < 0 || value > mapfuse::plan::kRwAll) throw Invalid("generic_rewrite: a mask in 0 .. 63");
+      if (value < 0 || value > mapfuse::plan::kRwAll) throw Invalid("generic_rewrite: a mask in 0 .. 127");
       mapfuse::plan::set_generic_rewrite(value);
     } else if (k == "generic_iterations") {
       if (value < 0 || value > 4096) throw Invalid("generic_iterations: 0 (auto) .. 4096");

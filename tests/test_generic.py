@@ -396,7 +396,7 @@ def test_uninstrumented_rewrites_fire(generic, seq, m, n, want):
         mf.set_option("generic_rewrite", 55)
 
 
-@pytest.mark.parametrize("mask", [0, 1, 2, 4, 8 + 1, 16, 31, 55, 63])
+@pytest.mark.parametrize("mask", [0, 1, 2, 4, 8 + 1, 16, 31, 55, 63, 119, 127])
 @pytest.mark.parametrize("seq", ["BICGK", "ATAX", "GEMVER", "GESUMMV", "AXPYDOT"])
 def test_rewrite_masks_emit_and_compile(generic, seq, mask):
     mf = generic

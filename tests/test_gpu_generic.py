@@ -115,7 +115,7 @@ def test_prefetch_distance_vs_oracle(generic, seq, m, n, d):
         check_output(seq, name, got[name], want[name], S[name], exact=False)
 
 
-@pytest.mark.parametrize("mask", [0, 1, 3, 23, 31, 55])
+@pytest.mark.parametrize("mask", [0, 1, 3, 23, 31, 55, 119, 127])
 @pytest.mark.parametrize("seq,m,n", [("BICGK", 1024, 2016), ("ATAX", 640, 384), ("GEMVER", 512, 768),
                                      ("GESUMMV", 256, 1024), ("AXPYDOT", 1, 4096)])
 def test_rewrite_masks_vs_reference_vm(generic, seq, m, n, mask):
@@ -136,7 +136,7 @@ def test_rewrite_masks_vs_reference_vm(generic, seq, m, n, mask):
         mf.set_option("generic_rewrite", 55)
 
 
-@pytest.mark.parametrize("mask", [0, 23, 31, 55])
+@pytest.mark.parametrize("mask", [0, 23, 31, 55, 119])
 @pytest.mark.parametrize("seq,m,n", [("AXPYDOT", 1, 100032), ("BICGK", 4096, 4096), ("GEMVER", 2048, 2048)])
 def test_rewrite_masks_vs_oracle(generic, seq, m, n, mask):
     """Larger problems per rewrite mask, whole plan against the C oracle

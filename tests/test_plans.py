@@ -316,7 +316,7 @@ def test_random_kernels_text_boundary_round_trip():
 @pytest.mark.parametrize("key,good,bad", [
     ("matrix_waves", [1, 2, 16], [0, 17]),
     ("matrix_dynamic", [0, 1], [2, -1]),
-    ("generic_rewrite", [0, 23, 55, 63], [-1, 64]),
+    ("generic_rewrite", [0, 23, 55, 127], [-1, 128]),
     ("matrix_tile_finalize", [0, 1, 2], [3]),
 ])
 def test_engine_option_ranges(key, good, bad):

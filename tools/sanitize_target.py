@@ -64,7 +64,7 @@ if GENERIC:
         for mode in ("fused", "unfused"):
             run(mf.Plan.compile(s, m, n, mode, manifest=lib), {})
 if FAST:
-    for mask in (55, 23, 31, 63):
+    for mask in (55, 23, 31, 63, 119, 127):
         mf.set_option("generic_rewrite", mask)
         mf.set_option("generic_iterations", 0)
         for seq, m, n in CASES:

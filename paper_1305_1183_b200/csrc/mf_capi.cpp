@@ -944,6 +944,9 @@ int mf_set_option(const char* key, int value) {
     } else if (k == "finalize_group") {
       if (value != 0 && value != 8 && value != 16 && value != 32) throw Invalid("finalize_group: 0 (auto) | 8 | 16 | 32");
       options().finalize_group = value;
+    } else if (k == "rowres_l2_ahead") {
+      if (value < -1 || value > 8) throw Invalid("rowres_l2_ahead: -1 (auto) .. 8");
+      options().rowres_l2_ahead = value;
     } else if (k == "rowres_force_cluster") {
       if (value != 0 && value != 1) throw Invalid("rowres_force_cluster: 0 | 1");
       options().rowres_force_cluster = value;
@@ -1020,6 +1023,7 @@ int mf_get_option(const char* key) {
   if (k == "matrix_tile_finalize") return options().matrix_tile_finalize;
   if (k == "matrix_waves") return options().matrix_waves;
   if (k == "rowres_force_cluster") return options().rowres_force_cluster;
+  if (k == "rowres_l2_ahead") return options().rowres_l2_ahead;
   if (k == "finalize_group") return options().finalize_group;
   if (k == "matrix_dynamic") return options().matrix_dynamic;
   if (k == "stream_unroll") return options().stream_unroll;

@@ -325,6 +325,7 @@ void run_rowres(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc, 
     return;
   }
   const int variant = rowres_variant(eo.rowres_variant, n);
+  a.l2_ahead = eo.rowres_l2_ahead < 0 ? 0 : eo.rowres_l2_ahead;
   check_cuda(rowres_config(m, n, sms, variant, &a, &grid), ("configure " + k.name).c_str());
   a.colpart = ws.scratch(sizeof(float) * (size_t)a.RB * (size_t)n + 256, s);
   a.bar = ws.counters(s);

@@ -53,6 +53,12 @@ __device__ __forceinline__ void rr_wait(unsigned long long* b, unsigned parity) 
       "r"(parity)
       : "memory");
 }
+// L2 prefetch of a global range (the bulk-copy engine, no shared memory):
+// rows beyond the ring are on their way from DRAM while the ring's stages
+// are still being consumed, so a stage refill reads L2
+__device__ __forceinline__ void rr_prefetch_l2(const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void rr_bulk(void* dst, const void* src, unsigned bytes,
                                         unsigned long long* bar, unsigned long long pol) {
   asm volatile(
@@ -60,6 +66,20 @@ __device__ __forceinline__ void rr_bulk(void* dst, const void* src, unsigned byt
       " [%0], [%1], %2, [%3], %4;" ::"r"(smem_addr(dst)),
       "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(pol)
       : "memory");
+}
+
+// The CTA total of one row's 16 warp partials, in every thread: lane l reads
+// warp (l & 15)'s partial (one shared-memory wavefront per warp instead of 16
+// broadcast reads), then a 16-lane xor butterfly.  Every warp computes the
+// same fixed tree, so t_i is identical across the CTA (and across the
+// stage-held and register-held variants).
+template <int R>
+__device__ __forceinline__ float combine_warps(const float (&red)[kRrWarps][R], int rr, int lane) {
+  static_assert(kRrWarps == 16, "16-lane butterfly");
+  float s = red[lane & 15][rr];
+#pragma unroll
+  for (int off = 8; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  return s;
 }
 
 template <int K, int R>
@@ -89,6 +109,17 @@ __global__ void __launch_bounds__(kRrThreads, 1) rowres_kernel(MatrixArgs a) {
       for (long long i = r0; i < r1; i += R) {
         const long long rows = (r1 - i) < R ? (r1 - i) : R;
         const long long bytes = rows * a.n * 4;
+        // rows i + (stages + d) R, d < l2_ahead: into L2 now (the first
+        // pass also covers the ring's own first stages' successors)
+        for (int d = (i == r0 ? 0 : a.l2_ahead - 1); d >= 0 && d < a.l2_ahead; ++d) {
+          const long long j = i + (long long)(kRrStages + d) * R;
+          if (j < r1) {
+            const long long pb = ((r1 - j) < R ? (r1 - j) : R) * a.n * 4;
+            const char* ps = reinterpret_cast<const char*>(a.M[0] + j * a.ld);
+            for (long long off = 0; off < pb; off += 16384)
+              rr_prefetch_l2(ps + off, (unsigned)((pb - off) < 16384 ? (pb - off) : 16384));
+          }
+        }
         rr_wait(&empty[stage], phase ^ 1u);
         rr_expect_tx(&full[stage], (unsigned)bytes);
         // 16 KB pieces keep several bulk transfers in flight per stage
@@ -152,9 +183,7 @@ __global__ void __launch_bounds__(kRrThreads, 1) rowres_kernel(MatrixArgs a) {
       float ti[R];
 #pragma unroll
       for (int rr = 0; rr < R; ++rr) {
-        float s = red[buf][0][rr];
-#pragma unroll
-        for (int w = 1; w < kRrWarps; ++w) s += red[buf][w][rr];
+        const float s = combine_warps(red[buf], rr, lane);
         // t_i rounded to fp32 exactly as the unfused plan stores it
         ti[rr] = (float)(a.ar[0] * (double)s);
         if (tid == 0 && a.yr[0] && rr < nr) a.yr[0][i0 + rr] = ti[rr];
@@ -280,9 +309,7 @@ __global__ void __launch_bounds__(kRrConsumers, 1) rowres_reg_kernel(MatrixArgs 
     }
 #pragma unroll
     for (int rr = 0; rr < R; ++rr) {
-      float s = red[buf][0][rr];
-#pragma unroll
-      for (int w = 1; w < kRrWarps; ++w) s += red[buf][w][rr];
+      const float s = combine_warps(red[buf], rr, lane);
       // t_i rounded to fp32 exactly as the unfused plan stores it
       const float ti = (float)(a.ar[0] * (double)s);
       if (tid == 0 && a.yr[0] && rr < nr) a.yr[0][i0 + rr] = ti;

@@ -199,6 +199,7 @@ void run_stream(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc, 
   if (n % 4) throw Fault("kernel " + k.name + ": stream length must be a multiple of 4 (padded)");
   StreamArgs a;
   a.n4 = n / 4;
+  a.ld_hint = options().stream_ld_hint;
   for (int i = 0; i < nin; ++i) {
     const DevBuf& b = need(bufs, op.inputs[i], k.name);
     need_len(b, n, op.inputs[i], k.name);

@@ -69,6 +69,18 @@ struct StreamBody {
   }
 };
 
+// read-only 128-bit load; hint 1 asks L2 to fetch the whole 256 B sector group
+__device__ __forceinline__ float4 ld_stream_in(const float4* p, int hint) {
+  if (hint == 1) {
+    float4 v;
+    asm("ld.global.nc.L2::256B.v4.f32 {%0,%1,%2,%3}, [%4];"
+        : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+        : "l"(p));
+    return v;
+  }
+  return __ldg(p);
+}
+
 template <int NIN, int NOUT, bool DOT, int U>
 __global__ void __launch_bounds__(kThreads) stream_kernel(StreamArgs a) {
   // Block-contiguous layout: block b = float4 [b*256*U, (b+1)*256*U) of every
@@ -114,7 +126,7 @@ __global__ void __launch_bounds__(kThreads) stream_kernel(StreamArgs a) {
 #pragma unroll
         for (int u = 0; u < U; ++u)
 #pragma unroll
-          for (int k = 0; k < NIN; ++k) v[u][k] = __ldg(a.in[k] + base + u * kThreads);
+          for (int k = 0; k < NIN; ++k) v[u][k] = ld_stream_in(a.in[k] + base + u * kThreads, a.ld_hint);
 #pragma unroll
         for (int u = 0; u < U; ++u)
           StreamBody<NIN, NOUT, DOT>::apply(a, v[u], base + u * kThreads, acc);
@@ -122,7 +134,7 @@ __global__ void __launch_bounds__(kThreads) stream_kernel(StreamArgs a) {
         for (long long i = base; i < a.n4; i += kThreads) {
           float4 v[NIN];
 #pragma unroll
-          for (int k = 0; k < NIN; ++k) v[k] = __ldg(a.in[k] + i);
+          for (int k = 0; k < NIN; ++k) v[k] = ld_stream_in(a.in[k] + i, a.ld_hint);
           StreamBody<NIN, NOUT, DOT>::apply(a, v, i, acc);
         }
       }

@@ -45,6 +45,7 @@ struct StreamArgs {
   double* part = nullptr;                 // [gridDim.x] per-CTA partials
   unsigned* ticket = nullptr;             // last-CTA-done counter (self-resetting)
   PeerLinks peer;                         // row-/element-sharded runs: the dot finishes across ranks
+  int ld_hint = 0;                        // element-wise loads: 0 plain ld.global.nc, 1 .L2::256B prefetch size
 };
 
 // Depth-2 single-pass matrix kernel (see mf_kernels.cu for the mapping).

@@ -105,6 +105,24 @@ int mf_plan_load(const char* text, mf_plan** out);
  * vm::launch(KernelIR, ...) boundary.  rows/cols: the padded domain. */
 int mf_plan_create(const char* kernel_ir_text, int rows, int cols, mf_plan** out);
 
+/* The device description of the SURVEY's boundary: the
+ * reference's DeviceConfig (proj/include/mapfuse/device.hpp, device.cfg text)
+ * plus the B200 facts a plan sizes itself by. */
+typedef struct {
+  const char* device_config; /* DeviceConfig text (device.cfg format); NULL = the shipped one */
+  int sm_count;              /* SMs the plan's persistent kernels (matrix, row-resident) may occupy;
+                                0 = all of the device's (capped by option max_sms) */
+  int rows, cols;            /* padded domain of the kernel (the VM derives the grid from it) */
+} mf_device_desc;
+
+/* mf_plan_create with a device description: the kernel is checked against
+ * the DeviceConfig's static limits as vm::launch checks them (threads per
+ * block, shared bytes per block: MF_ERR_FAULT, proj/src/vm.cpp:457-460; a
+ * malformed config: MF_ERR_INVALID), and every launch of the plan sizes its
+ * co-resident grids for at most desc->sm_count SMs (the caller keeps the
+ * rest, e.g. for concurrent work). */
+int mf_plan_create_desc(const char* kernel_ir_text, const mf_device_desc* desc, mf_plan** out);
+
 void mf_plan_destroy(mf_plan* plan);
 
 int mf_plan_num_kernels(const mf_plan* plan);

@@ -25,6 +25,7 @@ using namespace mapfuse::b200;
 
 struct mf_plan {
   NativePlan plan;
+  int sms = 0;  // mf_device_desc::sm_count (0 = no per-plan budget)
   // One workspace per stream: launches of one plan on different streams (or
   // from different threads) may overlap on the device, and each needs its own
   // grid-barrier counters, dot ticket, partials and intermediates.  Launches
@@ -388,6 +389,31 @@ int mf_plan_create(const char* kernel_ir_text, int rows, int cols, mf_plan** out
   });
 }
 
+int mf_plan_create_desc(const char* kernel_ir_text, const mf_device_desc* desc, mf_plan** out) {
+  return guarded([&] {
+    if (!kernel_ir_text || !desc || !out) throw Invalid("null argument");
+    if (desc->sm_count < 0 || desc->rows < 0 || desc->cols < 0) throw Invalid("negative device description field");
+    mapfuse::kernel::KernelIR k;
+    mapfuse::vm::DeviceConfig dev;
+    try {
+      k = mapfuse::kernel::parse_kernel_text(kernel_ir_text);
+      dev = mapfuse::vm::parse_device_config(desc->device_config ? std::string(desc->device_config)
+                                                                 : mapfuse::blas::default_device_config_text());
+    } catch (const std::exception& e) {
+      throw Invalid(e.what());
+    }
+    // the VM's static limits (proj/src/vm.cpp:457-460)
+    if (k.threads() > dev.max_threads_per_block)
+      throw Fault("vm fault: block of " + std::to_string(k.threads()) + " threads exceeds device");
+    if (k.shared_bytes_total() > dev.shared_bytes_per_block)
+      throw Fault("vm fault: shared allocation exceeds device limit");
+    auto p = std::make_unique<mf_plan>();
+    p->plan = plan_from_kernel_text(kernel_ir_text, desc->rows, desc->cols);
+    p->sms = desc->sm_count;
+    *out = p.release();
+  });
+}
+
 void mf_plan_destroy(mf_plan* plan) { delete plan; }
 
 int mf_plan_num_kernels(const mf_plan* plan) {
@@ -415,6 +441,7 @@ int mf_plan_kernel_column_outputs(const mf_plan* plan, int k, char* buf, int cap
 int mf_launch(const mf_plan* plan, const mf_buffer* buffers, int nbuf, const mf_scalar* scalars,
               int nscalars, void* stream, mf_stats* stats) {
   return guarded([&] {
+    PlanSmsScope sms_scope(plan ? plan->sms : 0);  // the plan's SM budget (mf_device_desc)
     if (!plan) throw Invalid("null plan");
     auto st = static_cast<cudaStream_t>(stream);
     Workspace& ws = plan->ws(st);
@@ -428,6 +455,7 @@ int mf_launch(const mf_plan* plan, const mf_buffer* buffers, int nbuf, const mf_
 int mf_launch_kernel(const mf_plan* plan, int k, const mf_buffer* buffers, int nbuf,
                      const mf_scalar* scalars, int nscalars, void* stream, mf_stats* stats) {
   return guarded([&] {
+    PlanSmsScope sms_scope(plan ? plan->sms : 0);  // the plan's SM budget (mf_device_desc)
     if (!plan) throw Invalid("null plan");
     auto st = static_cast<cudaStream_t>(stream);
     Workspace& ws = plan->ws(st);
@@ -568,6 +596,7 @@ int mf_measure_routine(const char* manifest, const char* function, const char* r
 int mf_plan_bind(const mf_plan* plan, const mf_buffer* buffers, int nbuf, const mf_scalar* scalars,
                  int nscalars, mf_bound** out) {
   return guarded([&] {
+    PlanSmsScope sms_scope(plan ? plan->sms : 0);  // the plan's SM budget (mf_device_desc)
     if (!plan || !out) throw Invalid("null argument");
     auto b = std::make_unique<mf_bound>();
     b->plan = plan;
@@ -673,6 +702,7 @@ int mf_plan_check(const mf_plan* plan, void* stream) {
 int mf_launch_host(const mf_plan* plan, const mf_buffer* host_buffers, int nbuf,
                    const mf_scalar* scalars, int nscalars, mf_stats* stats) {
   return guarded([&] {
+    PlanSmsScope sms_scope(plan ? plan->sms : 0);  // the plan's SM budget (mf_device_desc)
     if (!plan) throw Invalid("null plan");
     const NativePlan& P = plan->plan;
     std::lock_guard<std::mutex> host_lock(plan->host_mu);  // one host launch of a plan at a time
@@ -815,6 +845,7 @@ int mf_launch_kernel_peers(const mf_plan* plan, int k, mf_peer_group* g, const m
                            int nbuf, const mf_scalar* scalars, int nscalars, void* stream,
                            mf_stats* stats) {
   return guarded([&] {
+    PlanSmsScope sms_scope(plan ? plan->sms : 0);  // the plan's SM budget (mf_device_desc)
     if (!plan) throw Invalid("null plan");
     auto st = static_cast<cudaStream_t>(stream);
     Workspace& ws = plan->ws(st);
@@ -827,6 +858,7 @@ int mf_launch_kernel_peers(const mf_plan* plan, int k, mf_peer_group* g, const m
 int mf_launch_peers(const mf_plan* plan, mf_peer_group* g, const mf_buffer* buffers, int nbuf,
                     const mf_scalar* scalars, int nscalars, void* stream, mf_stats* stats) {
   return guarded([&] {
+    PlanSmsScope sms_scope(plan ? plan->sms : 0);  // the plan's SM budget (mf_device_desc)
     if (!plan || !g) throw Invalid("null plan or peer group");
     const NativePlan& P = plan->plan;
     for (int i = 0; i < (int)P.kernels.size(); ++i)
@@ -879,6 +911,7 @@ int mf_launch_sharded(const mf_plan* const* plans, int ngpus, const int* devices
       for (int g = 0; g < ngpus; ++g) {
         check_cuda(cudaSetDevice(devices[g]), "cudaSetDevice");
         auto st = static_cast<cudaStream_t>(streams[g]);
+        PlanSmsScope sms_scope(plans[g]->sms);
         run_kernel(plans[g]->plan, k, b[g], s, st, plans[g]->ws(st));
       }
       // partial column sums / dots of kernel k, summed over the GPUs before

@@ -50,6 +50,20 @@ void check_cuda(cudaError_t e, const char* what) {
                 ")");
 }
 
+namespace {
+thread_local int t_plan_sms = 0;
+}
+PlanSmsScope::PlanSmsScope(int cap) : saved(t_plan_sms) { t_plan_sms = cap; }
+PlanSmsScope::~PlanSmsScope() { t_plan_sms = saved; }
+
+int device_sm_count();
+int effective_sms() {
+  int s = device_sm_count();
+  if (options().max_sms > 0) s = std::min(s, options().max_sms);
+  if (t_plan_sms > 0) s = std::min(s, t_plan_sms);
+  return s;
+}
+
 int device_sm_count() {
   int dev = 0;
   check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
@@ -307,7 +321,7 @@ void run_rowres(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc, 
   a.ac[0] = coef(op.cols[0].coef, sc, k.name);
   if (m == 0 || n == 0) return zero_outputs(k, bufs, s, rec);
   const EngineOptions& eo = options();
-  const int sms = eo.max_sms > 0 ? std::min(eo.max_sms, device_sm_count()) : device_sm_count();
+  const int sms = effective_sms();
   int grid = 0;
   a.fin_g = eo.finalize_group;
   if (n > rowres_max_cols() || eo.rowres_force_cluster) {  // wide rows: a CTA cluster per row (DSMEM)
@@ -417,7 +431,7 @@ void run_matrix(const NativeKernel& k, const BufMap& bufs, const ScalarMap& sc, 
   t.bulk_store = sh.store && eo.tma_bulk_store != 0;
   if (t.tma && !tma_supported(sh, t)) t.tma = false;
   int grid = 0;
-  const int sms = eo.max_sms > 0 ? std::min(eo.max_sms, device_sm_count()) : device_sm_count();
+  const int sms = effective_sms();
   a.l2_normal = eo.matrix_l2_normal < 0 ? (sh.store ? 1 : 0) : eo.matrix_l2_normal;
   if (t.tma)
     check_cuda(matrix_tma_config(sh, t, m, n, sms, &a, &grid), ("configure " + k.name).c_str());

@@ -81,6 +81,18 @@ struct PeerGroup {
 };
 EngineOptions& options();
 
+// SMs a persistent kernel's grid may use: the device's, capped by option
+// max_sms and by the launching plan's device description (PlanSmsScope,
+// thread-local for the duration of one launch / bind call).
+int effective_sms();
+struct PlanSmsScope {
+  explicit PlanSmsScope(int cap);
+  ~PlanSmsScope();
+  PlanSmsScope(const PlanSmsScope&) = delete;
+  PlanSmsScope& operator=(const PlanSmsScope&) = delete;
+  int saved;
+};
+
 // Device scratch owned by one plan: cross-CTA partials, barrier / ticket
 // counters, unbound intermediates, and (for host launches) device mirrors of
 // host buffers.  Launches of one plan on one stream are serialized by the

@@ -70,8 +70,13 @@ EXPORTS = [
     "mf_plan_check", "mf_vm_launch", "mf_measure_routine", "mf_plan_bind", "mf_bound_launch",
     "mf_bound_graph_launch", "mf_bound_destroy", "mf_plan_count_implementations",
     "mf_plan_implementation", "mf_plan_set_implementation", "mf_launch_peers",
-    "mf_count_implementation_space", "mf_peer_group_check",
+    "mf_count_implementation_space", "mf_peer_group_check", "mf_plan_create_desc",
 ]
+
+
+class MfDeviceDesc(C.Structure):
+    """mf_device_desc (include/mapfuse_b200.h): DeviceConfig text + SM budget + domain."""
+    _fields_ = [("device_config", C.c_char_p), ("sm_count", C.c_int), ("rows", C.c_int), ("cols", C.c_int)]
 
 
 def lib() -> C.CDLL:
@@ -88,6 +93,7 @@ def lib() -> C.CDLL:
         L.mf_compile.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_int, C.c_int, P(C.c_void_p)]
         L.mf_compile_sequence.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int, P(C.c_void_p)]
         L.mf_plan_create.argtypes = [C.c_char_p, C.c_int, C.c_int, P(C.c_void_p)]
+        L.mf_plan_create_desc.argtypes = [C.c_char_p, P(MfDeviceDesc), P(C.c_void_p)]
         L.mf_plan_destroy.argtypes = [C.c_void_p]
         L.mf_plan_num_kernels.argtypes = [C.c_void_p]
         for fn in ("mf_plan_describe",):
@@ -246,9 +252,17 @@ class Plan:
         return float(lib().mf_plan_predicted_us(self.h))
 
     @classmethod
-    def from_kernel_text(cls, text: str, rows: int, cols: int) -> "Plan":
+    def from_kernel_text(cls, text: str, rows: int, cols: int, device_config: Optional[str] = None,
+                         sm_count: int = 0) -> "Plan":
+        """mf_plan_create, or mf_plan_create_desc when a DeviceConfig text or
+        an SM budget is given (the VM's static limits are checked against
+        the config; launches size co-resident grids for sm_count SMs)."""
         h = C.c_void_p()
-        _check(lib().mf_plan_create(text.encode(), rows, cols, C.byref(h)))
+        if device_config is None and sm_count == 0:
+            _check(lib().mf_plan_create(text.encode(), rows, cols, C.byref(h)))
+        else:
+            d = MfDeviceDesc(device_config.encode() if device_config is not None else None, sm_count, rows, cols)
+            _check(lib().mf_plan_create_desc(text.encode(), C.byref(d), C.byref(h)))
         return cls(h.value)
 
     # -- introspection ---------------------------------------------------------

@@ -201,6 +201,35 @@ def test_matrix_tile_schedules(env, waves, dyn, tile_fin):
         mf.set_option("matrix_tile_finalize", 0)
 
 
+@pytest.mark.parametrize("sms", [1, 37, 74])
+@pytest.mark.parametrize("seq,m,n,mode", [("BICGK", 4096, 4096, "fused"), ("ATAX", 4096, 4096, "b200"),
+                                          ("GEMVER", 2048, 2048, "fused")])
+def test_plan_sm_budget(env, seq, m, n, mode, sms):
+    """mf_plan_create_desc's sm_count: each kernel of the plan, re-created from
+    its KernelIR text with an SM budget, sizes its co-resident grid for at most
+    that many SMs (option max_sms per plan) and still matches the oracle."""
+    torch, mf, co = env
+    vals = rand_inputs(seq, m, n, 29)
+    full = mf.Plan.sequence(seq, m, n, mode)
+    shapes = out_shapes(full)
+    bufs = {k: torch.from_numpy(np.ascontiguousarray(v, np.float32)).cuda()
+            for k, v in vals.items() if isinstance(v, np.ndarray)}
+    scal = {k: float(v) for k, v in vals.items() if not isinstance(v, np.ndarray)}
+    d = full.describe()
+    for b in d["buffers"]:
+        if b["name"] not in bufs:
+            shp = (b["rows"], b["cols"]) if b["rows"] != 1 else (b["cols"],)
+            bufs[b["name"]] = torch.zeros(shp, device="cuda")
+    for k in range(full.num_kernels):
+        pk = mf.Plan.from_kernel_text(full.kernel_text(k), m, n, sm_count=sms)
+        pk.launch(bufs, scal)
+    torch.cuda.synchronize()
+    want = co.execute(seq, m, n, vals)
+    S = scale_bound(co, seq, m, n, vals)
+    for name in want:
+        check_output(seq, name, bufs[name].cpu().numpy().reshape(shapes[name]), want[name], S[name])
+
+
 def test_deterministic(env):
     torch, mf, co = env
     vals = rand_inputs("BICGK", 2048, 4096, 3)

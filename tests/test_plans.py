@@ -335,3 +335,35 @@ def test_engine_option_ranges(key, good, bad):
             assert mf.get_option(key) == last
     finally:
         mf.set_option(key, before)
+
+
+def test_plan_create_with_device_description():
+    """mf_plan_create_desc: the KernelIR is checked against
+    the DeviceConfig's static limits as vm::launch checks them
+    (proj/src/vm.cpp:457-460) -- VmFault over the limit, ParseError for a
+    malformed config -- and the SM budget is kept with the plan."""
+    text = mf.Plan.sequence("BICGK", 1024, 1024, "fused").kernel_text(0)
+    p = mf.Plan.from_kernel_text(text, 1024, 1024, sm_count=74)
+    assert p.num_kernels == 1
+    q = mf.Plan.from_kernel_text(text, 1024, 1024, device_config="warp_size 32\nmax_threads_per_block 1024\n"
+                                 "shared_bytes_per_block 232448\nsm_count 148\n")
+    assert q.describe()["kernels"][0]["name"] == p.describe()["kernels"][0]["name"]
+    threads = 1
+    for line in text.splitlines():
+        if line.strip().startswith("block "):
+            bx, by = line.split()[1:3]
+            threads = int(bx) * int(by)
+    with pytest.raises(mf.VmFault, match="threads exceeds device"):
+        mf.Plan.from_kernel_text(text, 1024, 1024,
+                                 device_config="max_threads_per_block %d\n" % max(32, threads // 2))
+    gen = "".join(l + "\n" for l in text.splitlines())
+    mf.set_option("generic", 1)
+    try:  # a generic kernel with a shared tile: over a 1 KB shared limit
+        gtext = mf.Plan.sequence("BICGK", 1024, 1024, "fused").kernel_text(0)
+    finally:
+        mf.set_option("generic", 0)
+    if "shared A" in gtext:
+        with pytest.raises(mf.VmFault, match="shared allocation"):
+            mf.Plan.from_kernel_text(gtext, 1024, 1024, device_config="shared_bytes_per_block 1024\n")
+    with pytest.raises(mf.ParseError):
+        mf.Plan.from_kernel_text(gen, 1024, 1024, device_config="bogus_key 3\n")

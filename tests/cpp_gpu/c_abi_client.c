@@ -41,6 +41,35 @@ int main(void) {
   mf_buffer bad[1] = {{"w", 1, n, w}};
   int rc = mf_launch_host(plan, bad, 1, NULL, 0, &st);
   if (rc != MF_ERR_FAULT) return 1;
+  /* the same kernel re-created from its KernelIR text with a device
+   * description: DeviceConfig limits + an SM budget */
+  int need = mf_plan_kernel_text(plan, 0, NULL, 0);
+  char* text = malloc((size_t)need);
+  mf_plan_kernel_text(plan, 0, text, need);
+  mf_device_desc desc = {NULL, 64, 1, n};
+  mf_plan* p2 = NULL;
+  if (mf_plan_create_desc(text, &desc, &p2) != MF_OK) {
+    fprintf(stderr, "create_desc: %s\n", mf_last_error());
+    return 1;
+  }
+  for (int i = 0; i < n; ++i) x[i] = 0.0f;
+  if (mf_launch_host(p2, bufs, 4, NULL, 0, &st) != MF_OK) {
+    fprintf(stderr, "launch desc plan: %s\n", mf_last_error());
+    return 1;
+  }
+  for (int i = 0; i < n; ++i)
+    if (x[i] != (float)((double)w[i] + (double)y[i] + (double)z[i])) {
+      fprintf(stderr, "desc plan mismatch at %d\n", i);
+      return 1;
+    }
+  mf_device_desc tiny = {"max_threads_per_block 32\n", 0, 1, n};
+  mf_plan* p3 = NULL;
+  if (mf_plan_create_desc(text, &tiny, &p3) != MF_ERR_FAULT) { /* the VM's static limit */
+    fprintf(stderr, "expected a VM fault for a 32-thread device\n");
+    return 1;
+  }
+  mf_plan_destroy(p2);
+  free(text);
   printf("c-abi client ok (%.3f ms, %s)\n", st.ms, mf_version());
   mf_plan_destroy(plan);
   free(w); free(y); free(z); free(x);

@@ -129,7 +129,10 @@ def test_random_script(seed, mode):
         opts = {"tma": int(orng.choice([-1, 0, 1])), "matrix_k": int(orng.choice([2, 4])),
                 "f64acc": int(orng.choice([0, 1])), "matrix_l2_normal": int(orng.choice([-1, 0, 1])),
                 "tma_bulk_store": int(orng.choice([0, 1])), "stream_ctas_per_sm": int(orng.choice([0, 2])),
-                "stream_unroll": int(orng.choice([0, 4])), "tma_consumers": int(orng.choice([0, 256, 512]))}
+                "stream_unroll": int(orng.choice([0, 4])), "tma_consumers": int(orng.choice([0, 256, 512])),
+                "matrix_waves": int(orng.choice([1, 2, 4])), "matrix_dynamic": int(orng.choice([0, 1])),
+                "matrix_tile_finalize": int(orng.choice([0, 1, 2])),
+                "finalize_group": int(orng.choice([0, 16, 32])), "rowres_variant": int(orng.choice([0, 1, 2]))}
     saved = {k: mf.get_option(k) for k in opts}
     try:
         for k, v in opts.items():

@@ -307,7 +307,15 @@ int mf_generate(float* dev, int64_t rows, int64_t cols, int64_t ld, uint64_t see
  * matrix grid), "matrix_l2_normal" (-1 auto: evict-normal for kernels that
  * store a matrix, evict-first otherwise | 0 | 1), "stream_unroll" (0 = 2 |
  * 2 | 4 | 8 float4 per thread per stream), "stream_ctas_per_sm" (0 = one CTA
- * per block, else a capped grid striding over blocks). */
+ * per block, else a capped grid striding over blocks), "matrix_waves" (row
+ * bands per co-resident CTA of the register-fed matrix kernel, 1 .. 16) and
+ * "matrix_dynamic" (0 | 1: tiles after a CTA's first from a counter),
+ * "finalize_group" (0 = 8 | 8 | 16 | 32 lanes per slot in the cross-CTA
+ * finalize), "rowres_force_cluster" (0 | 1: rows of n <= 16384 over a CTA
+ * cluster), "rowres_l2_ahead" (-1 auto = 0 .. 8 rows prefetched into L2
+ * beyond the row-resident ring), "stream_ld_hint" (0 | 1: .L2::256B hint on
+ * element-wise loads).  Round-2 experiments; their defaults are the measured
+ * best (profiles/r02_*). */
 int mf_set_option(const char* key, int value);
 int mf_get_option(const char* key);
 

@@ -871,12 +871,15 @@ RcFn rc_setup(int v, long long n, cudaLaunchConfig_t* cfg, cudaLaunchAttribute* 
 long long rowres_max_cols() { return 4LL * kRrConsumers * 8; }
 long long rowres_cluster_max_cols() { return 16 * 8192; }
 
-// auto: variant 4 (tools/rowres_sweep.py on B200, profiles/r02_rowres_variants.txt:
-// ATAX 131072^2 11.27 ms vs 13.81 / 20.5 / 31.7 ms for variants 1 / 2 / 3)
+// auto (tools/rowres_sweep.py on B200, profiles/r02_rowres_variants.txt):
+// the st.async exchange (variants 4 / 5; 1 / 2 / 3 took 13.8 / 20.5 / 31.7 ms
+// at 131072^2).  Register-held rows (5) against stage-held (4), by cluster
+// size: 2 CTAs 669 vs 607 us (32768^2), 3: -2.4%, 4: -6.5% (65536^2 2.33 vs
+// 2.49 ms), 5: -6.3%, 6: +2%, 7: -3.9%, 8: -3% to +0.5% -- so 5 from clusters
+// of 3 up, 4 for clusters of 2.  Both sum in the same order (bit-identical).
 int rowres_cluster_variant(int requested, long long n) {
   if (requested >= 1 && requested <= 7) return requested;
-  (void)n;
-  return 4;
+  return (n + rowres_max_cols() - 1) / rowres_max_cols() >= 3 ? 5 : 4;
 }
 
 cudaError_t launch_rowres_cluster(MatrixArgs a, int variant, int finalize_grid, cudaStream_t s) {

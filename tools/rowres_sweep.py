@@ -3,7 +3,8 @@ the default, or "rowres_variant" for n <= 16384) on ATAX in planner mode
 b200: device time (median of 7, back-to-back launches are L2-cold at these
 sizes, the L2 is flushed anyway) and the outputs' agreement with variant 1.
 
-python tools/rowres_sweep.py [M:N ...]   (default 131072:131072 32768:32768 65536:65536)
+python tools/rowres_sweep.py [M:N ...]   (default 131072:131072 32768:32768 65536:65536;
+MF_VARIANTS=1,4,5,6,7 by default: round 1 and the st.async variants)
 """
 import os
 import statistics
@@ -39,7 +40,7 @@ def time_plan(plan, bufs, reps=7):
 
 
 specs = sys.argv[1:] or ["131072:131072", "32768:32768", "65536:65536"]
-variants = [int(v) for v in os.environ.get("MF_VARIANTS", "1,2,3").split(",")]
+variants = [int(v) for v in os.environ.get("MF_VARIANTS", "1,4,5,6,7").split(",")]
 OPTION = os.environ.get("MF_SWEEP_OPTION", "rowres_cluster")  # or rowres_variant (n <= 16384)
 for spec in specs:
     m, n = (int(x) for x in spec.split(":"))

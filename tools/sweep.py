@@ -79,6 +79,15 @@ if which in ("matrix", "all"):
         run(seq, m, n, st)
     mf.set_option("tma_consumers", 0)
 if which in ("rowres", "all"):
-    for m, n in ((16384, 16384), (8192, 16384), (16384, 8192), (32768, 4096)):
-        for mode in ("fused", "b200"):
-            run("ATAX", m, n, [{"tma": -1}], mode)
+    for m, n in ((16384, 16384), (8192, 16384), (16384, 8192), (32768, 4096), (65536, 2048)):
+        run("ATAX", m, n, [{"tma": -1}], "fused")
+        run("ATAX", m, n, [{"rowres_variant": v} for v in (1, 2)], "b200")
+    mf.set_option("rowres_variant", 0)
+if which in ("occupancy", "all"):
+    st = [{"tma": 0, "matrix_k": k, "occupancy": o} for k in (2, 4) for o in (1, 2, 3)]
+    for seq, m, n in (("BICGK", 16384, 16384), ("SGEMV", 16384, 16384), ("SGEMVT", 16384, 16384),
+                      ("GESUMMV", 16384, 16384)):
+        run(seq, m, n, st)
+    mf.set_option("tma", -1)
+    mf.set_option("matrix_k", 2)
+    mf.set_option("occupancy", 2)

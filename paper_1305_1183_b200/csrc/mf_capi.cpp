@@ -986,6 +986,9 @@ int mf_set_option(const char* key, int value) {
     } else if (k == "stream_ld_hint") {
       if (value != 0 && value != 1) throw Invalid("stream_ld_hint: 0 | 1");
       options().stream_ld_hint = value;
+    } else if (k == "matrix_reverse") {
+      if (value < -1 || value > 1) throw Invalid("matrix_reverse: -1 (auto) | 0 | 1");
+      options().matrix_reverse = value;
     } else if (k == "matrix_waves") {
       if (value < 1 || value > 16) throw Invalid("matrix_waves: 1 .. 16");
       options().matrix_waves = value;
@@ -1058,6 +1061,7 @@ int mf_get_option(const char* key) {
   if (k == "rowres_variant") return options().rowres_variant;
   if (k == "matrix_tile_finalize") return options().matrix_tile_finalize;
   if (k == "matrix_waves") return options().matrix_waves;
+  if (k == "matrix_reverse") return options().matrix_reverse;
   if (k == "stream_ld_hint") return options().stream_ld_hint;
   if (k == "rowres_force_cluster") return options().rowres_force_cluster;
   if (k == "rowres_l2_ahead") return options().rowres_l2_ahead;

@@ -55,6 +55,8 @@ struct EngineOptions {
   // per CTA) and whether CTAs past their first tile take the next one from a
   // counter (1) or round-robin (0)
   int matrix_waves = 1;
+  int matrix_reverse = -1;  // register-fed matrix kernels: row batches bottom-up within each band:
+                            // -1 auto (after an earlier kernel stored the matrix) | 0 never | 1 always
   int stream_ld_hint = 0;  // element-wise kernels' loads: 0 plain, 1 .L2::256B prefetch-size hint
   int rowres_force_cluster = 0;
   int rowres_l2_ahead = -1;  // row-resident chains: rows prefetched into L2 beyond the ring (-1 auto)  // 1: rows of n <= 16384 also split over a CTA cluster (variant 7 by default)

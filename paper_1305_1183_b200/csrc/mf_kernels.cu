@@ -276,7 +276,11 @@ __global__ void __launch_bounds__(kThreads, 2) matrix_kernel(MatrixArgs a) {
 #pragma unroll
         for (int e = 0; e < 4; ++e) cacc[c][k][e] = ACC(0);
 
-    for (long long i0 = r0; i0 < r1; i0 += R) {
+    // a.rev: the band's batches bottom-up (the last rows a preceding kernel
+    // stored are the ones still in L2)
+    const long long nbatch = (r1 - r0 + R - 1) / R;
+    for (long long bi = 0; bi < nbatch; ++bi) {
+      const long long i0 = r0 + (a.rev ? nbatch - 1 - bi : bi) * R;
       double us[NRANK > 0 ? NRANK : 1][R];
       float xcs[NCOL > 0 ? NCOL : 1][R];
       float4 av[R][NMAT][K];

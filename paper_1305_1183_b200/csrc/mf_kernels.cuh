@@ -72,6 +72,7 @@ struct MatrixArgs {
   PeerLinks peer;                   // nranks > 1: fused cross-GPU column reduction
   int l2_normal = 0;                // matrix loads: 0 evict-first L2 policy, 1 evict-normal
   int l2_ahead = 0;                 // row-resident chains: rows prefetched into L2 beyond the ring
+  int rev = 0;                      // register-fed matrix kernel: each band's row batches bottom-up
   int fin_g = 0;                    // cross-CTA finalize lanes per slot: 0 = 8, or 16 | 32
   int dyn = 0;                      // tiles after blockIdx.x from counter bar[4] (bar[5] counts
                                     // exhausted CTAs; the last one resets both)

@@ -763,6 +763,7 @@ RcFn rc_fn_cl(int variant) {
 
 RcFn rowres_cluster_fn(int variant, int cl) {
   switch (cl) {
+    case 1: return rc_fn_cl<1>(variant);  // rows of n <= 16384 on the cluster kernels' code path
     case 2: return rc_fn_cl<2>(variant);
     case 3: return rc_fn_cl<3>(variant);
     case 4: return rc_fn_cl<4>(variant);

@@ -931,8 +931,10 @@ def main():
         if world == 1 and not args.no_cpu:
             try:
                 cores = os.cpu_count() or 1
-                many = cpu_reference(1 << 24, cores, 3, 1)
-                one = cpu_reference(1 << 22, 1, 3, 1)
+                # the stated workload (the reference arm's n), ~10 s of host
+                # work, and the serial code as written on a 2^24 sample
+                many = cpu_reference(args.n, cores, 10, 1)
+                one = cpu_reference(1 << 24, 1, 5, 1)
                 line["cpu_baseline"] = {k: v for k, v in many.items() if k in
                                         ("value", "unit", "cores", "kind", "sample")}
                 line["cpu_baseline"]["single_core"] = {

@@ -77,7 +77,11 @@ def test_generic_vs_reference_vm(generic, g, mode):
 
 @pytest.mark.parametrize("seq,m,n", [("BICGK", 1024, 2016), ("GEMVER", 512, 768),
                                      ("AXPYDOT", 1, 100032), ("GESUMMV", 256, 1024),
-                                     ("ATAX", 640, 384), ("BICGK", 4096, 4096)])
+                                     ("ATAX", 640, 384), ("BICGK", 4096, 4096),
+                                     # the sizes the generic sweeps time: 8 serial iterations,
+                                     # late prefetch, 32x2 blocks, every default rewrite
+                                     ("BICGK", 16384, 16384), ("GEMVER", 8192, 8192),
+                                     ("ATAX", 8192, 8192), ("GESUMMV", 8192, 8192)])
 def test_generic_larger_vs_oracle(generic, seq, m, n):
     """Grids of thousands of CTAs, serial iterations chosen per size, whole-plan
     launch.  Buffers are padded to 32 as the VM requires (vm.cpp:31-39)."""

@@ -10,6 +10,8 @@ host/cudagen.cpp), plus the user functions of tests/golden/generic.mf.
            reduction, deferred accumulators, global vectors, pruned barriers,
            late prefetch) -- on shapes with several serial iterations; each
            plan also with every rewrite mask of interest (generic_rewrite).
+--cluster: the row-resident chain over CTA clusters (ATAX, mode b200, n >
+           16384: the auto variants 4 / 5 at clusters of 2 .. 8).
 --mutate:  fused BiCGK with codegen's barriers suppressed: the
            racecheck run is EXPECTED to report hazards.
 """
@@ -63,6 +65,11 @@ if GENERIC:
     for s, m, n in USER_SCRIPTS.values():
         for mode in ("fused", "unfused"):
             run(mf.Plan.compile(s, m, n, mode, manifest=lib), {})
+if "--cluster" in sys.argv:
+    for m, n in [(32, 32768), (96, 49152), (64, 65536), (64, 131072)]:
+        run(mf.Plan.sequence("ATAX", m, n, "b200"), {})
+    print("sanitize target done")
+    sys.exit(0)
 if FAST:
     for mask in (55, 23, 31, 63, 119, 127):
         mf.set_option("generic_rewrite", mask)

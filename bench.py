@@ -922,10 +922,25 @@ def main():
         except Exception as ex:  # report, keep the main line
             sharded = {"error": str(ex)[:300]}
         torch.cuda.empty_cache()
+        # the same config's ATAX in planner mode b200: the row-resident chain
+        # over CTA clusters reads A once (BASELINE configs[4]), sampled parity
+        try:
+            sb = copy.copy(sa)
+            sb.mode = "b200"
+            r = run_sharded(sb, torch, mf, rank, world, "ATAX")
+            atax = {"workload": "ATAX fp32 %dx%d, planner mode b200 (row-resident chain over CTA clusters, "
+                                "one read of A) on 1 GPU" % (r["m"], r["n"]),
+                    "value": round(r["value"], 1), "unit": "GB/s", "ms_per_step": round(r["ms_per_step"], 4),
+                    "steps": sb.steps, "frac_per_gpu": round(r["value"] / peak, 4), "kernels": r["kernels"],
+                    "parity": r["parity"]}
+        except Exception as ex:
+            atax = {"error": str(ex)[:300]}
+        torch.cuda.empty_cache()
     if rank == 0:
         line["e2e"] = e2e
         if sharded is not None:
             line["sharded"] = sharded
+            line["atax_b200"] = atax
         if world == 1 and not args.no_suite:
             line["suite"] = run_suite(args, torch, mf)
         if world == 1 and not args.no_cpu:

@@ -39,6 +39,8 @@ def test_bench_single_gpu_line():
     assert d["n_gpus"] == 1 and d["gpu_launches"] == 10 and d["value"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     assert d["sharded"]["value"] > 0 and d["sharded"]["rows_per_rank"] == 4096
+    assert d["sharded"]["parity"]["ok"]
+    assert d["atax_b200"]["value"] > 0 and d["atax_b200"]["parity"]["ok"], d["atax_b200"]
 
 
 def test_bench_two_ranks_on_one_gpu():

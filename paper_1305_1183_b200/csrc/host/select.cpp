@@ -120,9 +120,11 @@ CodegenParams generic_params(const kernel::KernelIR& k, int64_t dom_rows, int64_
     limit = elems / inst;
   }
   const int forced = generic_iterations();
-  // depth 1: 32 iterations when the kernel reduces (half the blocks, half the
-  // global atomics: AXPYDOT 0.47 -> 0.53 of HBM), else 16 (VADD 0.95)
-  int64_t want = forced >= 1 ? forced : (k.depth == 1 ? (accumulates ? 32 : 16) : (accumulates ? 4 : 1));
+  // depth 1: 128 iterations when the kernel reduces (fewer blocks, fewer
+  // same-address global atomics: AXPYDOT 2^24 84 / 64 / 61 / 59 us at
+  // 16 / 32 / 64 / 128 with the round-2 deferred accumulators,
+  // profiles/r02_generic_rewrite.txt), else 16 (VADD 0.94)
+  int64_t want = forced >= 1 ? forced : (k.depth == 1 ? (accumulates ? 128 : 16) : (accumulates ? 4 : 1));
   // depth 2 with accumulators: 8 serial iterations while that still leaves
   // >= 16 waves of 4 blocks per SM (generic BiCGK 16384^2: 196 -> 179 us;
   // 8192^2 shapes have too few tiles and measured equal or slower)
